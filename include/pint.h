@@ -1,0 +1,168 @@
+/*
+ * pint.h — C ABI of libpint: one alpha-circulant preconditioned Richardson iteration
+ * ("Paralpha", arXiv 2103.12571) on the all-at-once Radau IIA collocation system,
+ * computed by hand-written sm_100a CUDA kernels.
+ *
+ * Citations: "P:n" = PAPER.md line n (LaTeX source of arXiv 2103.12571).
+ *
+ * Problem statement: u_t = A u + b on [0, T], u(0) = u0, b == 0,
+ * L equal steps dT = T/L, M right-included Gauss-Radau (Radau IIA) nodes.
+ * The all-at-once system is C u = w with (block matrix P:115-135)
+ *     C = I_L (x) (I_MN - dT Q (x) A) + E (x) (H_M (x) I_N),  E = -1 on the sub-diagonal,
+ *     w = (u0 replicated over the M nodes, 0, ..., 0).
+ * One iteration with parameter alpha (correction form, reading R1):
+ *     u <- u + C_alpha^{-1} (w - C u),   C_alpha = C with -alpha in the (1, L) corner of E.
+ * computed as (north star steps (i)-(v), Alg. 1):
+ *   (i)   r = w - C u, scaled by alpha^{l/L}               (J^{-1})
+ *   (ii)  L-point DFT along time                              (Lemma P:164-171)
+ *   (iii) x1_k = S_k^{-1} x_k, Q G_k^{-1} = S_k D_k S_k^{-1}
+ *   (iv)  (I - d_km dT A) x2 = x1 for every (k, m)
+ *   (v)   y_k = G_k^{-1} S_k x2_k, inverse DFT, alpha^{-l/L}/L, u += c
+ *
+ * Spatial operators (periodic [0,1)^dim, x_j = j/nx, n = y*nx + x, centred 2nd order):
+ *   PINT_OP_HEAT:       A = nu * Laplacian  ((u_{j-1} - 2u_j + u_{j+1}) nx^2 per axis)
+ *   PINT_OP_ADVECTION:  A = -(cx d/dx + cy d/dy)  (-c n/2 (u_{j+1} - u_{j-1}) per axis)
+ *
+ * Data layout: complex128, interleaved (re, im) doubles, u[l][m][n], n fastest.
+ *
+ * Ownership: the caller owns all device memory (u_dev, work_dev); the context keeps
+ * non-owning pointers and carves its small tables out of work_dev.  Host inputs are copied
+ * at call time.  Outputs go to caller buffers.
+ *
+ * Concurrency: a context is not thread-safe.  All device work is stream-ordered on
+ * pint_dist.stream.  pint_iterate only enqueues work (CUDA-graph capturable when
+ * last_step_diff_inf == NULL); pint_residual_norm / pint_get_* synchronise the stream.
+ *
+ * Errors: every function returns pint_status (never throws across the ABI); the message of
+ * the last non-OK status of the calling thread is pint_last_error().  After PINT_ERR_CUDA
+ * the context is poisoned and every later call returns PINT_ERR_STATE.
+ */
+#ifndef PINT_H
+#define PINT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PINT_ABI_VERSION 1
+#define PINT_MAX_M 8            /* Radau IIA nodes supported */
+#define PINT_MAX_SCHEDULE 64    /* alpha values per pint_set_alpha_schedule */
+
+typedef struct pint_ctx pint_ctx;
+
+typedef enum {
+  PINT_OK = 0,
+  PINT_ERR_INVALID = 1,             /* bad argument / unsupported size; nothing was changed   */
+  PINT_ERR_SCHEDULE = 2,            /* alpha outside (0,1), schedule exhausted, m_k < 4 gamma */
+  PINT_ERR_NOT_DIAGONALIZABLE = 3,  /* cond(S_k) > 1e8 or eigenvalue gap < 1e-8 rho(B_k)     */
+  PINT_ERR_NUMERIC = 4,             /* non-finite residual norm                                */
+  PINT_ERR_CUDA = 5,                /* CUDA runtime error (context poisoned)                   */
+  PINT_ERR_NCCL = 6,                /* communication error (context poisoned)                  */
+  PINT_ERR_STATE = 7                /* context poisoned by an earlier CUDA/NCCL error          */
+} pint_status;
+
+typedef enum { PINT_OP_HEAT = 0, PINT_OP_ADVECTION = 1 } pint_op;
+
+typedef struct {
+  int32_t dim;     /* 1 or 2                                                                  */
+  int32_t nx, ny;  /* grid; powers of two, nx >= 4 (ny == 1 if dim == 1, ny >= 4 if dim == 2) */
+  int32_t op;      /* pint_op                                                                 */
+  double nu;       /* heat diffusivity                                                        */
+  double cx, cy;   /* advection velocity (cy ignored in 1-D)                                  */
+  double T;        /* interval length, dT = T / L                                             */
+  int32_t L;       /* time steps, power of two, 1 <= L <= 1024                        */
+  int32_t M;       /* Radau IIA nodes, 1 <= M <= PINT_MAX_M                                   */
+} pint_problem;
+
+typedef struct {
+  int32_t rank, nranks;          /* nranks == 1 in this build (multi-GPU: DESIGN.md §7)       */
+  const void *nccl_unique_id;    /* reserved (NULL)                                            */
+  int32_t device;                /* CUDA device ordinal                                        */
+  void *stream;                  /* cudaStream_t on which all work is enqueued (NULL = legacy) */
+} pint_dist;
+
+/* Bytes of device scratch pint_create needs in work_dev for this problem (0 on invalid input;
+ * then pint_last_error() says why).  Includes one or two L*M*N complex128 work vectors, the
+ * per-alpha factor tables for up to PINT_MAX_SCHEDULE alphas and reduction scratch. */
+size_t pint_workspace_bytes(const pint_problem *p, const pint_dist *d);
+
+/* Creates a context.  u_dev: caller-owned device buffer of L*M*N complex128 (16-byte aligned),
+ * set here to u^(0) = u0 replicated over all (l, m).  work_dev/work_bytes: caller-owned
+ * device scratch (256-byte aligned, >= pint_workspace_bytes).  u0_host: 2N doubles (re, im),
+ * copied.  forcing_host must be NULL (b == 0; forcing is not supported in this build).
+ * Errors: PINT_ERR_INVALID (sizes, alignment, NULL), PINT_ERR_CUDA. */
+pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, void *work_dev,
+                        size_t work_bytes, const double *u0_host, const double *forcing_host,
+                        pint_ctx **out);
+
+/* Algorithm 2's a-priori alpha sequence: gamma = L (3 eps + tau) w_inf,
+ * alpha_{k+1} = sqrt(gamma / m_k), m_{k+1} = 2 sqrt(m_k gamma), m_0 = m0.  Pure host function.
+ * alpha_out: K doubles; m_out: K+1 doubles (nullable).  PINT_ERR_SCHEDULE if m_k < 4 gamma. */
+pint_status pint_adaptive_schedule(int32_t L, double w_inf, double m0, double eps, double tau,
+                                   int32_t K, double *alpha_out, double *m_out);
+
+/* ||w||_inf = ||u0||_inf of the context's initial value (b == 0), for pint_adaptive_schedule. */
+pint_status pint_w_inf(pint_ctx *c, double *w_inf);
+
+/* Copies K alphas (each in (0,1)), builds their per-alpha factor tables on the host in long
+ * double (d_k, r_k, S_k, S_k^{-1}, G_k^{-1} S_k, d_km, PCR level coefficients) and uploads them;
+ * resets the iteration counter to 0.  Errors: PINT_ERR_SCHEDULE, PINT_ERR_NOT_DIAGONALIZABLE,
+ * PINT_ERR_INVALID (K > PINT_MAX_SCHEDULE), PINT_ERR_CUDA. */
+pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K);
+
+/* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:
+ * nullable; if given, n_iter doubles receive ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf (Alg. 2 line 7,
+ * P:421) and the call synchronises the stream.  PINT_ERR_SCHEDULE if the schedule would run out. */
+pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf);
+
+/* ||w - C u||_2 and ||w - C u||_inf of the current iterate (synchronises). PINT_ERR_NUMERIC if
+ * non-finite. */
+pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf);
+
+/* D2H of the whole local iterate (2*L*M*N doubles) — parity checks (synchronises). */
+pint_status pint_get_iterate(pint_ctx *c, double *u_host);
+
+/* D2H of the last node of the last step, u_{L-1, M-1, :} = the solution at T (2N doubles). */
+pint_status pint_get_final_value(pint_ctx *c, double *u_host);
+
+/* Replaces u0 (H2D copy of 2N doubles, changes w) and, if reset_iterate != 0, resets the iterate
+ * to u0 replicated.  Used by the end-to-end benchmark. */
+pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t reset_iterate);
+
+/* Frees context-owned host state; never caller buffers. */
+pint_status pint_destroy(pint_ctx *c);
+
+/* Thread-local message of the last non-OK status. */
+const char *pint_last_error(void);
+
+int32_t pint_abi_version(void);
+
+/* ---- introspection (tests / benchmarks) ------------------------------------------------- */
+
+/* Number of kernel launches one iteration enqueues, and the names of the kernels. */
+int32_t pint_launches_per_iteration(pint_ctx *c);
+
+/* Host copies of the factor tables of schedule entry `a` for frequency k (natural order):
+ * d_k (2 doubles), S_k, S_k^{-1} (2*M*M doubles each, row-major), d_km (2*M doubles).
+ * Any output pointer may be NULL. */
+pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, double *S,
+                             double *Sinv, double *d_km);
+
+/* Radau IIA nodes t (M doubles) and Q (M*M, row-major) as computed by the library (long double,
+ * rounded). */
+pint_status pint_tableau(int32_t M, double *t, double *Q);
+
+/* Stage-level debug entry: runs only stage s of iteration with schedule entry a on the current
+ * buffers: 0 = forward (residual, scale, time DFT, S^-1) u -> X; 1 = spatial solves X -> X';
+ * 2 = backward (G^-1 S, inverse DFT, unscale, u += c).  X/X' can be read with
+ * pint_debug_get_work (which = 0 forward output, 1 solve output), frequency index bit-reversed. */
+pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s);
+pint_status pint_debug_get_work(pint_ctx *c, int32_t which, double *host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINT_H */

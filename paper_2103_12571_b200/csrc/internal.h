@@ -1,0 +1,72 @@
+// Internal (non-ABI) declarations shared by the host side (pint_abi.cpp) and the kernels
+// (kernels.cu).  No torch types anywhere.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pint {
+
+// Per-alpha device tables (pointers into work_dev).  Frequency index p is BIT-REVERSED:
+// slot p holds frequency k = bitrev_L(p) (the time FFT leaves its output in that order).
+struct AlphaTables {
+  const double *scale_fwd;    // [L]       alpha^{l/L}                        (J^{-1})
+  const double *scale_bwd;    // [L]       alpha^{-l/L} / L                   (J and 1/L of V)
+  const double2 *Sinv;        // [L][M][M] S_k^{-1}
+  const double2 *SG;          // [L][M][M] G_k^{-1} S_k = (I - r_k H_M) S_k
+  const double2 *shift;       // [L][M]    s_km = d_km dT
+  const double2 *pcr;         // [L][M][nlev] (p_j, q_j) pairs: 2 double2 per level  (1-D only)
+  const double2 *inv_e;       // [L][M]    1 / e_final of the row-sum-carrying PCR   (1-D only)
+};
+
+struct Geometry {
+  int dim, nx, ny, N, L, M, op;
+  int logL, logN, lognx, logny;
+  double dT;
+  // stencil: (A u)_n = cxm u[x-1] + cxp u[x+1] + cym u[y-1] + cyp u[y+1] + c0 u[n]
+  double cxm, cxp, cym, cyp, c0;
+  double dTQ[8 * 8];          // dT * Q, row-major
+};
+
+struct StaticTables {
+  const double2 *twL;         // [L]  e^{-2 pi i q / L}
+  const double2 *twx;         // [nx] e^{-2 pi i q / nx}
+  const double2 *twy;         // [ny] e^{-2 pi i q / ny}
+  const double2 *lamx;        // [nx] per-axis symbol, natural kx
+  const double2 *lamy;        // [ny]
+  const double2 *u0;          // [N]
+};
+
+struct Buffers {
+  double2 *u;                 // [L][M][N] iterate (caller-owned)
+  double2 *X;                 // [L][M][N] work 1
+  double2 *Y;                 // [L][M][N] work 2 (1-D two-pass PCR only; else == X)
+  double *red;                // reduction scratch (doubles)
+};
+
+// ---- launch wrappers (kernels.cu) -----------------------------------------------------------
+// All return cudaGetLastError() after enqueueing on `st`.
+struct LaunchCfg {
+  int fwd_T;                  // spatial points per forward/backward tile
+  int pcr_mode;               // 0: single-pass line PCR; 1: two-pass (classes + chunks)
+  int pcr_R;                  // residue-class modulus of the two-pass scheme
+  int pcr_T;                  // class columns per CTA
+  int pcr_chunk;              // contiguous chunk length of the small-stride pass
+};
+
+LaunchCfg choose_launch(const Geometry &g);
+size_t fwd_smem_bytes(const Geometry &g, int T);
+
+cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                           const AlphaTables &at, const Buffers &b, cudaStream_t s);
+cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                         const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out);
+cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                            const AlphaTables &at, const Buffers &b, const double2 *x2,
+                            double *diff_slot, cudaStream_t s);
+cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
+                                 double *out2, cudaStream_t s);
+cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,
+                                cudaStream_t s);
+int launches_per_iteration(const Geometry &g, const LaunchCfg &lc);
+
+}  // namespace pint

@@ -1,0 +1,689 @@
+// sm_100a kernels of libpint: one alpha-circulant preconditioned Richardson iteration
+// (arXiv 2103.12571, Alg. 1, correction form) on complex fp64 data u[l][m][n].
+//
+//   fwd_kernel        (i)+(ii)+(iii): residual w - C u, alpha^{l/L} scale,
+//                     L-point DIF FFT along time in shared memory (Lemma P:164-171),
+//                     S_k^{-1} node transform                         u -> X
+//   pcr_*_kernel      (iv) 1-D: (I - d_km dT A) x2 = x1 by parallel cyclic reduction on
+//                     the constant-coefficient cyclic tridiagonal, row-sum carried   X -> X|Y
+//   fft2d_*_kernel    (iv) 2-D: x2 = F^{-1}[F x1 / (1 - s lambda)] (3 passes)        X -> X
+//   bwd_kernel        (v): G_k^{-1} S_k, inverse DIT FFT along time from
+//                     bit-reversed order, alpha^{-l/L}/L, u += c    X -> u
+//
+// Design notes: everything is HBM-bandwidth bound (AI < 4 flop/B, fp64), so the
+// kernels are organised around full-tile shared-memory staging with 16-byte coalesced global
+// accesses; no tensor cores (no dense contraction on this path).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace pint {
+
+// ---------------------------------------------------------------------------------------------
+// complex helpers
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+// acc + a * b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ int brev(int x, int bits) {
+  return bits == 0 ? 0 : (int)(__brev((unsigned)x) >> (32 - bits));
+}
+
+// ---------------------------------------------------------------------------------------------
+// shared-memory FFT engine: in-place radix-2 stages fused in register groups of 2^B.
+// Element (column c, position p) lives at sm[c*cs + p*ps].  tw[q] = e^{-2 pi i q / n}.
+// DIF (forward, e^{-}): natural input -> bit-reversed output.
+// DIT (inverse, e^{+}): bit-reversed input -> natural output.
+
+template <int B>
+__device__ __forceinline__ void dif_group(double2 *sm, int ncols, int cs, int ps, int n, int m0,
+                                          const double2 *__restrict__ tw) {
+  constexpr int R = 1 << B;
+  const int s = m0 >> B;
+  const int nb = n >> B;
+  const int nitems = ncols * nb;
+  for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
+    int c, jj;
+    if (cs == 1) { c = item % ncols; jj = item / ncols; } else { jj = item % nb; c = item / nb; }
+    const int blk = jj / s, j0 = jj - blk * s;
+    double2 *base = sm + c * cs + (blk * m0 + j0) * ps;
+    double2 v[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) v[t] = base[t * s * ps];
+#pragma unroll
+    for (int st = 0; st < B; ++st) {
+      const int half_t = 1 << (B - 1 - st);
+      const int twmul = n / (m0 >> st);
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        if (t & half_t) continue;
+        const int j = j0 + (t & ((R >> st) - 1)) * s;
+        double2 a = v[t], b = v[t + half_t];
+        v[t] = cadd(a, b);
+        v[t + half_t] = (j == 0) ? csub(a, b) : cmul(csub(a, b), __ldg(tw + j * twmul));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) base[t * s * ps] = v[t];
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void dit_group(double2 *sm, int ncols, int cs, int ps, int n, int s,
+                                          const double2 *__restrict__ tw) {
+  constexpr int R = 1 << B;
+  const int Mg = s << B;
+  const int nb = n >> B;
+  const int nitems = ncols * nb;
+  for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
+    int c, jj;
+    if (cs == 1) { c = item % ncols; jj = item / ncols; } else { jj = item % nb; c = item / nb; }
+    const int blk = jj / s, j0 = jj - blk * s;
+    double2 *base = sm + c * cs + (blk * Mg + j0) * ps;
+    double2 v[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) v[t] = base[t * s * ps];
+#pragma unroll
+    for (int st = 0; st < B; ++st) {
+      const int half_t = 1 << st;
+      const int twmul = n / ((2 * s) << st);
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        if (t & half_t) continue;
+        const int j = j0 + (t & ((2 << st) - 1)) * s;
+        double2 a = v[t];
+        double2 b = (j == 0) ? v[t + half_t] : cmulc(v[t + half_t], __ldg(tw + j * twmul));
+        v[t] = cadd(a, b);
+        v[t + half_t] = csub(a, b);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) base[t * s * ps] = v[t];
+  }
+}
+
+// group sizes: split log2 n into ceil(log2 n / 4) groups of <= 4 stages, as even as possible
+__device__ __forceinline__ int group_size(int logn, int done) {
+  int left = logn - done;
+  int ngroups = (left + 3) / 4;
+  return (left + ngroups - 1) / ngroups;
+}
+
+// forward transform (DIF) of ncols columns of length n; ends with __syncthreads()
+__device__ void fft_dif(double2 *sm, int ncols, int cs, int ps, int n, int logn, const double2 *tw) {
+  int done = 0, m0 = n;
+  while (done < logn) {
+    int b = group_size(logn, done);
+    switch (b) {
+      case 1: dif_group<1>(sm, ncols, cs, ps, n, m0, tw); break;
+      case 2: dif_group<2>(sm, ncols, cs, ps, n, m0, tw); break;
+      case 3: dif_group<3>(sm, ncols, cs, ps, n, m0, tw); break;
+      default: dif_group<4>(sm, ncols, cs, ps, n, m0, tw); break;
+    }
+    __syncthreads();
+    done += b;
+    m0 >>= b;
+  }
+}
+
+// inverse transform (DIT, conjugate twiddles, no 1/n); ends with __syncthreads()
+__device__ void fft_dit_inv(double2 *sm, int ncols, int cs, int ps, int n, int logn, const double2 *tw) {
+  int done = 0, s = 1;
+  while (done < logn) {
+    int b = group_size(logn, done);
+    switch (b) {
+      case 1: dit_group<1>(sm, ncols, cs, ps, n, s, tw); break;
+      case 2: dit_group<2>(sm, ncols, cs, ps, n, s, tw); break;
+      case 3: dit_group<3>(sm, ncols, cs, ps, n, s, tw); break;
+      default: dit_group<4>(sm, ncols, cs, ps, n, s, tw); break;
+    }
+    __syncthreads();
+    done += b;
+    s <<= b;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// residual of one (l, n) for all nodes: r_m = w_m - u_m + dT sum_j Q_mj (A u_j) + u_{l-1, M-1}
+// (C = I_L (x) C_coll + E (x) H; w_0 = u0 replicated, w_{l>0} = 0 since b == 0)
+
+template <int M>
+__device__ __forceinline__ void residual_point(const Geometry &g, const double2 *__restrict__ u,
+                                               const double2 *__restrict__ u0, int l, int n,
+                                               double2 r[M]) {
+  const size_t plane = (size_t)M * g.N;
+  const double2 *ul = u + (size_t)l * plane;
+  const int x = n & (g.nx - 1);
+  const int y = n >> g.lognx;
+  const int nxm = (y << g.lognx) + ((x - 1) & (g.nx - 1));
+  const int nxp = (y << g.lognx) + ((x + 1) & (g.nx - 1));
+  double2 uc[M], Au[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double2 *uj = ul + (size_t)j * g.N;
+    double2 c = __ldg(uj + n), a = __ldg(uj + nxm), b = __ldg(uj + nxp);
+    uc[j] = c;
+    double2 s;
+    s.x = g.c0 * c.x + g.cxm * a.x + g.cxp * b.x;
+    s.y = g.c0 * c.y + g.cxm * a.y + g.cxp * b.y;
+    if (g.dim == 2) {
+      const int nym = (((y - 1) & (g.ny - 1)) << g.lognx) + x;
+      const int nyp = (((y + 1) & (g.ny - 1)) << g.lognx) + x;
+      double2 d = __ldg(uj + nym), e = __ldg(uj + nyp);
+      s.x += g.cym * d.x + g.cyp * e.x;
+      s.y += g.cym * d.y + g.cyp * e.y;
+    }
+    Au[j] = s;
+  }
+  double2 base = make_double2(0.0, 0.0);
+  if (l == 0) base = __ldg(u0 + n);
+  else base = __ldg(u + (size_t)(l - 1) * plane + (size_t)(M - 1) * g.N + n);
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    double2 acc = csub(base, uc[m]);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double q = g.dTQ[m * M + j];
+      acc.x = fma(q, Au[j].x, acc.x);
+      acc.y = fma(q, Au[j].y, acc.y);
+    }
+    r[m] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// forward: u -> X[p][m][n] = (S_p^{-1} (FFT_l alpha^{l/L} r))  (p bit-reversed frequency)
+
+template <int M>
+__global__ void __launch_bounds__(256) fwd_kernel(Geometry g, StaticTables st, AlphaTables at,
+                                                  const double2 *__restrict__ u, double2 *__restrict__ X,
+                                                  int T) {
+  extern __shared__ double2 sm[];  // [L][M][T]
+  const int n0 = blockIdx.x * T;
+  const int L = g.L;
+  const size_t plane = (size_t)M * g.N;
+  const int items = L * T;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int t = it % T, l = it / T;
+    double2 r[M];
+    residual_point<M>(g, u, st.u0, l, n0 + t, r);
+    const double sc = __ldg(at.scale_fwd + l);
+#pragma unroll
+    for (int m = 0; m < M; ++m) sm[(l * M + m) * T + t] = cscale(r[m], sc);
+  }
+  __syncthreads();
+  fft_dif(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int t = it % T, p = it / T;
+    double2 v[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) v[j] = sm[(p * M + j) * T + t];
+    const double2 *Si = at.Sinv + (size_t)p * M * M;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = cfma(__ldg(Si + m * M + j), v[j], acc);
+      X[(size_t)p * plane + (size_t)m * g.N + n0 + t] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// backward: X2 -> u += alpha^{-l/L}/L IFFT_p (G_p^{-1} S_p X2)
+
+__device__ __forceinline__ unsigned long long dbl_bits(double v) { return (unsigned long long)__double_as_longlong(v); }
+
+template <int M>
+__global__ void __launch_bounds__(256) bwd_kernel(Geometry g, StaticTables st, AlphaTables at,
+                                                  const double2 *__restrict__ X2, double2 *__restrict__ u,
+                                                  int T, unsigned long long *diff_slot) {
+  extern __shared__ double2 sm[];  // [L][M][T]
+  __shared__ double red[32];
+  const int n0 = blockIdx.x * T;
+  const int L = g.L;
+  const size_t plane = (size_t)M * g.N;
+  const int items = L * T;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int t = it % T, p = it / T;
+    double2 v[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) v[j] = __ldg(X2 + (size_t)p * plane + (size_t)j * g.N + n0 + t);
+    const double2 *SG = at.SG + (size_t)p * M * M;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = cfma(__ldg(SG + m * M + j), v[j], acc);
+      sm[(p * M + m) * T + t] = acc;
+    }
+  }
+  __syncthreads();
+  fft_dit_inv(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  double dmax = 0.0;
+  const int all = L * M * T;
+  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+    const int t = idx % T;
+    const int m = (idx / T) % M;
+    const int l = idx / (M * T);
+    const double2 c = cscale(sm[idx], __ldg(at.scale_bwd + l));
+    double2 *up = u + (size_t)l * plane + (size_t)m * g.N + n0 + t;
+    double2 uo = *up;
+    *up = cadd(uo, c);
+    if (l == L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
+  }
+  if (diff_slot) {
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+      atomicMax(diff_slot, dbl_bits(v));  // non-negative doubles order like their bit patterns
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// 1-D spatial solves: (I - s A) x = y, A cyclic tridiagonal with constant coefficients.
+// PCR level j (h = 2^j) on the circulant system: y_i <- y_i - p_j y_{i-h} - q_j y_{i+h} with
+// p_j = a_j/b_j, q_j = c_j/b_j; last level (h = N/2, i-h == i+h): y_i <- y_i - p y_{i+h}; then
+// x = y / e_final.  Level coefficients come from the host (long double, row sum e = a+b+c carried,
+// DESIGN.md reading R6).  The level operators are circulant, hence commute: the two-pass scheme
+// applies the large strides (closed on residue classes mod R) first, then the small strides on
+// contiguous chunks with halos.
+
+constexpr int kPcrThreads = 256;
+constexpr int kPcrIPT = 16;   // items per thread held in registers per level
+
+// Lines of length nq at element stride R (residue classes mod R), T consecutive classes per CTA.
+// Applies coefficient levels j_off .. nlev-1 (the last is the pair level) and multiplies by 1/e.
+__global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry g, AlphaTables at,
+                                                                  double2 *__restrict__ X, int R, int T,
+                                                                  int j_off) {
+  extern __shared__ double2 sm[];  // [nq][T]
+  const int N = g.N;
+  const int nq = N / R;
+  const int lognq = g.logN - j_off;
+  const int groups = R / T;
+  const int line = blockIdx.x / groups;
+  const int r0 = (blockIdx.x - line * groups) * T;
+  double2 *xl = X + (size_t)line * N;
+  const int items = nq * T;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int tt = it % T, q = it / T;
+    sm[it] = xl[(size_t)q * R + r0 + tt];
+  }
+  __syncthreads();
+  const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
+  for (int jj = 0; jj < lognq; ++jj) {
+    const int j = j_off + jj;
+    const double2 pj = __ldg(coef + 2 * j), qj = __ldg(coef + 2 * j + 1);
+    const int h = 1 << jj;
+    const bool pair = (jj == lognq - 1);
+    double2 nv[kPcrIPT];
+#pragma unroll
+    for (int k = 0; k < kPcrIPT; ++k) {
+      const int it = threadIdx.x + k * kPcrThreads;
+      if (it < items) {
+        const int tt = it % T, q = it / T;
+        const double2 yc = sm[it];
+        const double2 yp = sm[((q + h) & (nq - 1)) * T + tt];
+        double2 v = csub(yc, cmul(pair ? pj : qj, yp));
+        if (!pair) v = csub(v, cmul(pj, sm[((q - h) & (nq - 1)) * T + tt]));
+        nv[k] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPcrIPT; ++k) {
+      const int it = threadIdx.x + k * kPcrThreads;
+      if (it < items) sm[it] = nv[k];
+    }
+    __syncthreads();
+  }
+  const double2 ie = __ldg(at.inv_e + line);
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int tt = it % T, q = it / T;
+    xl[(size_t)q * R + r0 + tt] = cmul(sm[it], ie);
+  }
+}
+
+// Small-stride levels 0..jA-1 on contiguous chunks of C with halos of H >= 2^jA - 1 (redundant
+// halo computation, out of place X -> Y).
+constexpr int kChunkThreads = 512;
+constexpr int kChunkIPT = 10;
+
+__global__ void __launch_bounds__(kChunkThreads) pcr_chunk_kernel(const Geometry g, AlphaTables at,
+                                                                  const double2 *__restrict__ X,
+                                                                  double2 *__restrict__ Y, int C, int H,
+                                                                  int jA) {
+  extern __shared__ double2 sm[];  // [C + 2H]
+  const int N = g.N;
+  const int chunks = N / C;
+  const int line = blockIdx.x / chunks;
+  const int n0 = (blockIdx.x - line * chunks) * C;
+  const double2 *xl = X + (size_t)line * N;
+  const int S = C + 2 * H;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) sm[i] = __ldg(xl + ((n0 - H + i) & (N - 1)));
+  __syncthreads();
+  const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
+  int lo = 0;
+  for (int j = 0; j < jA; ++j) {
+    const int h = 1 << j;
+    lo += h;  // valid region after this level: [lo, S - lo)
+    const double2 pj = __ldg(coef + 2 * j), qj = __ldg(coef + 2 * j + 1);
+    const int cnt = S - 2 * lo;
+    double2 nv[kChunkIPT];
+#pragma unroll
+    for (int k = 0; k < kChunkIPT; ++k) {
+      const int i = lo + threadIdx.x + k * kChunkThreads;
+      if (i < lo + cnt) nv[k] = csub(csub(sm[i], cmul(pj, sm[i - h])), cmul(qj, sm[i + h]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kChunkIPT; ++k) {
+      const int i = lo + threadIdx.x + k * kChunkThreads;
+      if (i < lo + cnt) sm[i] = nv[k];
+    }
+    __syncthreads();
+  }
+  double2 *yl = Y + (size_t)line * N;
+  for (int i = threadIdx.x; i < C; i += blockDim.x) yl[n0 + i] = sm[H + i];
+}
+
+// ---------------------------------------------------------------------------------------------
+// 2-D spatial solves by FFT: row DIF (x) -> column pass [DIF (y), * 1/((1 - s lambda) nx ny),
+// DIT (y)] -> row DIT (x).  Spectral positions are bit-reversed between the passes.
+
+constexpr int kFftThreads = 256;
+
+template <bool INV>
+__global__ void __launch_bounds__(kFftThreads) fft2d_rows_kernel(const Geometry g, StaticTables st,
+                                                                 double2 *__restrict__ X, int rows_per_cta) {
+  extern __shared__ double2 sm[];  // [rows][nx]
+  const int nx = g.nx;
+  double2 *base = X + (size_t)blockIdx.x * rows_per_cta * nx;
+  const int items = rows_per_cta * nx;
+  for (int i = threadIdx.x; i < items; i += blockDim.x) sm[i] = base[i];
+  __syncthreads();
+  if (INV) fft_dit_inv(sm, rows_per_cta, nx, 1, nx, g.lognx, st.twx);
+  else fft_dif(sm, rows_per_cta, nx, 1, nx, g.lognx, st.twx);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) base[i] = sm[i];
+}
+
+__global__ void __launch_bounds__(kFftThreads) fft2d_cols_kernel(const Geometry g, StaticTables st,
+                                                                 AlphaTables at, double2 *__restrict__ X,
+                                                                 int T) {
+  extern __shared__ double2 sm[];  // [ny][T]
+  const int nx = g.nx, ny = g.ny;
+  const int groups = nx / T;
+  const int line = blockIdx.x / groups;           // line = p*M + m
+  const int kx0 = (blockIdx.x - line * groups) * T;
+  double2 *xl = X + (size_t)line * g.N;
+  const int items = ny * T;
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i % T, y = i / T;
+    sm[i] = xl[(size_t)y * nx + kx0 + tt];
+  }
+  __syncthreads();
+  fft_dif(sm, T, 1, T, ny, g.logny, st.twy);
+  const double2 s = __ldg(at.shift + line);
+  const double inv_n = 1.0 / ((double)nx * (double)ny);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i % T, py = i / T;
+    const int kx = brev(kx0 + tt, g.lognx), ky = brev(py, g.logny);
+    const double2 lam = cadd(__ldg(st.lamx + kx), __ldg(st.lamy + ky));
+    // D = 1 - s * lam ;  value * inv_n / D
+    const double2 sl = cmul(s, lam);
+    const double dr = 1.0 - sl.x, di = -sl.y;
+    const double den = inv_n / (dr * dr + di * di);
+    const double2 v = sm[i];
+    sm[i] = make_double2((v.x * dr + v.y * di) * den, (v.y * dr - v.x * di) * den);
+  }
+  __syncthreads();
+  fft_dit_inv(sm, T, 1, T, ny, g.logny, st.twy);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i % T, y = i / T;
+    xl[(size_t)y * nx + kx0 + tt] = sm[i];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// residual norms and initialisation
+
+template <int M>
+__global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables st,
+                                                      const double2 *__restrict__ u, double *partial) {
+  __shared__ double s2[32], sm_[32];
+  double acc2 = 0.0, accm = 0.0;
+  const long long total = (long long)g.L * g.N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(i / g.N), n = (int)(i - (long long)l * g.N);
+    double2 r[M];
+    residual_point<M>(g, u, st.u0, l, n, r);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const double a2 = r[m].x * r[m].x + r[m].y * r[m].y;
+      acc2 += a2;
+      accm = fmax(accm, sqrt(a2));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+    accm = fmax(accm, __shfl_xor_sync(0xffffffffu, accm, o));
+  }
+  if ((threadIdx.x & 31) == 0) { s2[threadIdx.x >> 5] = acc2; sm_[threadIdx.x >> 5] = accm; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s2[w]; b = fmax(b, sm_[w]); }
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void reduce_partials_kernel(const double *partial, int nblocks, double *out) {
+  // one warp, fixed order -> deterministic
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nblocks; i += 32) { a += partial[2 * i]; b = fmax(b, partial[2 * i + 1]); }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if (threadIdx.x == 0) { out[0] = sqrt(a); out[1] = b; }
+}
+
+__global__ void init_iterate_kernel(Geometry g, const double2 *__restrict__ u0, double2 *__restrict__ u) {
+  const long long total = (long long)g.L * g.M * g.N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    u[i] = __ldg(u0 + (i % g.N));
+}
+
+// ---------------------------------------------------------------------------------------------
+// host-side launch logic
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+size_t fwd_smem_bytes(const Geometry &g, int T) { return (size_t)g.L * g.M * T * sizeof(double2); }
+
+LaunchCfg choose_launch(const Geometry &g) {
+  LaunchCfg lc{};
+  // forward/backward tile: as many spatial points as fit ~100 KB (2 CTAs per SM), <= 16
+  int T = 16;
+  while (T > 1 && fwd_smem_bytes(g, T) > 100 * 1024) T >>= 1;
+  while (T > g.N) T >>= 1;
+  lc.fwd_T = T;
+  if (g.dim == 1) {
+    if (g.N <= 4096) {
+      lc.pcr_mode = 0;
+      lc.pcr_R = 1;
+      lc.pcr_T = 1;
+    } else {
+      lc.pcr_mode = 1;
+      int jA = g.logN / 2;            // R = 2^jA classes of length N/R
+      lc.pcr_R = 1 << jA;
+      int nq = g.N / lc.pcr_R;
+      int t = 4096 / nq;
+      if (t > lc.pcr_R) t = lc.pcr_R;
+      if (t < 1) t = 1;
+      lc.pcr_T = t;
+      lc.pcr_chunk = 4096;
+      if (lc.pcr_chunk > g.N) lc.pcr_chunk = g.N;
+    }
+  }
+  return lc;
+}
+
+int launches_per_iteration(const Geometry &g, const LaunchCfg &lc) {
+  if (g.dim == 2) return 5;
+  return lc.pcr_mode == 0 ? 3 : 4;
+}
+
+static cudaError_t set_smem(const void *fn, size_t bytes) {
+  if (bytes > 48 * 1024)
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+#define PINT_DISPATCH_M(M_, ...)       \
+  switch (M_) {                        \
+    case 1: { constexpr int MM = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int MM = 2; __VA_ARGS__; } break; \
+    case 3: { constexpr int MM = 3; __VA_ARGS__; } break; \
+    case 4: { constexpr int MM = 4; __VA_ARGS__; } break; \
+    case 5: { constexpr int MM = 5; __VA_ARGS__; } break; \
+    case 6: { constexpr int MM = 6; __VA_ARGS__; } break; \
+    case 7: { constexpr int MM = 7; __VA_ARGS__; } break; \
+    default: { constexpr int MM = 8; __VA_ARGS__; } break; \
+  }
+
+cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                           const AlphaTables &at, const Buffers &b, cudaStream_t s) {
+  const int T = lc.fwd_T;
+  const size_t smem = fwd_smem_bytes(g, T);
+  const int grid = g.N / T;
+  cudaError_t e = cudaSuccess;
+  PINT_DISPATCH_M(g.M, {
+    e = set_smem((const void *)fwd_kernel<MM>, smem);
+    if (e == cudaSuccess) fwd_kernel<MM><<<grid, 256, smem, s>>>(g, st, at, b.u, b.X, T);
+  });
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                         const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out) {
+  cudaError_t e;
+  const int lines = g.L * g.M;
+  if (g.dim == 1) {
+    if (lc.pcr_mode == 0) {
+      const size_t smem = (size_t)g.N * sizeof(double2);
+      if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
+      pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0);
+      *out = b.X;
+    } else {
+      const int R = lc.pcr_R, T = lc.pcr_T, jA = 0;
+      (void)jA;
+      const int jOff = __builtin_ctz((unsigned)R);
+      const int nq = g.N / R;
+      size_t smem = (size_t)nq * T * sizeof(double2);
+      if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
+      pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      const int C = lc.pcr_chunk, H = R;
+      smem = (size_t)(C + 2 * H) * sizeof(double2);
+      if ((e = set_smem((const void *)pcr_chunk_kernel, smem)) != cudaSuccess) return e;
+      pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smem, s>>>(g, at, b.X, b.Y, C, H, jOff);
+      *out = b.Y;
+    }
+  } else {
+    // rows: 4096 elements per CTA
+    int rpc = 4096 / g.nx;
+    if (rpc < 1) rpc = 1;
+    const long long rows = (long long)lines * g.ny;
+    while (rpc > 1 && rows % rpc) rpc >>= 1;
+    size_t smem = (size_t)rpc * g.nx * sizeof(double2);
+    if ((e = set_smem((const void *)fft2d_rows_kernel<false>, smem)) != cudaSuccess) return e;
+    if ((e = set_smem((const void *)fft2d_rows_kernel<true>, smem)) != cudaSuccess) return e;
+    fft2d_rows_kernel<false><<<(unsigned)(rows / rpc), kFftThreads, smem, s>>>(g, st, b.X, rpc);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int T = 4096 / g.ny;
+    if (T < 1) T = 1;
+    if (T > g.nx) T = g.nx;
+    if (T > 16) T = 16;
+    size_t smc = (size_t)g.ny * T * sizeof(double2);
+    if ((e = set_smem((const void *)fft2d_cols_kernel, smc)) != cudaSuccess) return e;
+    fft2d_cols_kernel<<<lines * (g.nx / T), kFftThreads, smc, s>>>(g, st, at, b.X, T);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    fft2d_rows_kernel<true><<<(unsigned)(rows / rpc), kFftThreads, smem, s>>>(g, st, b.X, rpc);
+    *out = b.X;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                            const AlphaTables &at, const Buffers &b, const double2 *x2,
+                            double *diff_slot, cudaStream_t s) {
+  const int T = lc.fwd_T;
+  const size_t smem = fwd_smem_bytes(g, T);
+  const int grid = g.N / T;
+  cudaError_t e = cudaSuccess;
+  PINT_DISPATCH_M(g.M, {
+    e = set_smem((const void *)bwd_kernel<MM>, smem);
+    if (e == cudaSuccess)
+      bwd_kernel<MM><<<grid, 256, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+  });
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
+                                 double *out2, cudaStream_t s) {
+  const long long total = (long long)g.L * g.N;
+  int blocks = (int)((total + 255) / 256);
+  const int cap = 148 * 8;  // partials scratch is sized for 148*8 blocks (pint_abi.cpp layout)
+  if (blocks > cap) blocks = cap;
+  PINT_DISPATCH_M(g.M, { resnorm_kernel<MM><<<blocks, 256, 0, s>>>(g, st, b.u, b.red); });
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  reduce_partials_kernel<<<1, 32, 0, s>>>(b.red, blocks, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b, cudaStream_t s) {
+  const long long total = (long long)g.L * g.M * g.N;
+  long long blocks = (total + 255) / 256;
+  if (blocks > num_sms() * 32) blocks = num_sms() * 32;
+  init_iterate_kernel<<<(int)blocks, 256, 0, s>>>(g, st.u0, b.u);
+  return cudaGetLastError();
+}
+
+}  // namespace pint

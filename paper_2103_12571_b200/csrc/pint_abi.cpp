@@ -1,0 +1,528 @@
+// C ABI of libpint (include/pint.h): validation, host factor tables (long double), workspace
+// carving and the stream-ordered iteration driver.  Every step of the iteration runs in the
+// kernels of kernels.cu; this file only builds tables and enqueues launches.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pint.h"
+#include "host_numerics.h"
+#include "internal.h"
+
+using namespace pint;
+
+namespace {
+
+thread_local std::string g_err;
+
+pint_status fail(pint_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t vec_bytes;      // one L*M*N complex128 vector
+  size_t off_X, off_Y;
+  size_t off_static, static_bytes;
+  size_t off_alpha, alpha_bytes_each;
+  size_t off_red, red_bytes;
+  size_t total;
+  bool two_vectors;
+};
+
+}  // namespace
+
+struct pint_ctx {
+  pint_problem prob;
+  pint_dist dist;
+  Geometry g;
+  LaunchCfg lc;
+  Layout lay;
+  cudaStream_t stream;
+  char *work;
+  double2 *u;
+  StaticTables st;
+  std::vector<AlphaTables> at;
+  std::vector<double> alphas;
+  int k = 0;
+  bool poisoned = false;
+  std::vector<ld> t, Q;
+  std::vector<double> u0;          // host copy (2N)
+  // host copies of the factor tables (natural frequency order) for introspection
+  std::vector<std::vector<cld>> h_S, h_Sinv, h_dkm;
+  std::vector<std::vector<cld>> h_dk;
+};
+
+static pint_status validate(const pint_problem *p, const pint_dist *d) {
+  if (!p) return fail(PINT_ERR_INVALID, "problem is NULL");
+  if (p->dim != 1 && p->dim != 2) return fail(PINT_ERR_INVALID, "dim must be 1 or 2");
+  if (!is_pow2(p->nx) || p->nx < 4) return fail(PINT_ERR_INVALID, "nx must be a power of two >= 4");
+  if (p->dim == 1 && p->ny != 1) return fail(PINT_ERR_INVALID, "ny must be 1 in 1-D");
+  if (p->dim == 2 && (!is_pow2(p->ny) || p->ny < 4)) return fail(PINT_ERR_INVALID, "ny must be a power of two >= 4");
+  if (p->nx > (1 << 20) || p->ny > 4096) return fail(PINT_ERR_INVALID, "grid too large");
+  if (p->dim == 2 && (p->nx > 4096)) return fail(PINT_ERR_INVALID, "2-D nx must be <= 4096");
+  if (p->op != PINT_OP_HEAT && p->op != PINT_OP_ADVECTION) return fail(PINT_ERR_INVALID, "unknown op");
+  if (!is_pow2(p->L) || p->L > 1024) return fail(PINT_ERR_INVALID, "L must be a power of two <= 1024 (P:592)");
+  if (p->M < 1 || p->M > PINT_MAX_M) return fail(PINT_ERR_INVALID, "M must be in [1, 8]");
+  if (!(p->T > 0) || !std::isfinite(p->T)) return fail(PINT_ERR_INVALID, "T must be > 0");
+  if (!std::isfinite(p->nu) || !std::isfinite(p->cx) || !std::isfinite(p->cy))
+    return fail(PINT_ERR_INVALID, "non-finite coefficient");
+  if (d) {
+    if (d->nranks != 1 || d->rank != 0)
+      return fail(PINT_ERR_INVALID, "this build runs one rank per problem (nranks == 1)");
+  }
+  return PINT_OK;
+}
+
+static Geometry make_geometry(const pint_problem *p) {
+  Geometry g{};
+  g.dim = p->dim;
+  g.nx = p->nx;
+  g.ny = p->dim == 2 ? p->ny : 1;
+  g.N = g.nx * g.ny;
+  g.L = p->L;
+  g.M = p->M;
+  g.op = p->op;
+  g.logL = ilog2(g.L);
+  g.logN = ilog2(g.N);
+  g.lognx = ilog2(g.nx);
+  g.logny = ilog2(g.ny);
+  g.dT = p->T / p->L;
+  const double nx = g.nx, ny = g.ny;
+  if (p->op == PINT_OP_HEAT) {
+    g.cxm = g.cxp = p->nu * nx * nx;
+    g.c0 = -2.0 * p->nu * nx * nx;
+    if (g.dim == 2) {
+      g.cym = g.cyp = p->nu * ny * ny;
+      g.c0 += -2.0 * p->nu * ny * ny;
+    }
+  } else {
+    g.cxm = p->cx * nx / 2.0;   // -c n/2 (u_{j+1} - u_{j-1})
+    g.cxp = -p->cx * nx / 2.0;
+    if (g.dim == 2) {
+      g.cym = p->cy * ny / 2.0;
+      g.cyp = -p->cy * ny / 2.0;
+    }
+    g.c0 = 0.0;
+  }
+  return g;
+}
+
+static Layout make_layout(const Geometry &g, const LaunchCfg &lc) {
+  Layout L{};
+  L.vec_bytes = (size_t)g.L * g.M * g.N * sizeof(double2);
+  L.two_vectors = (g.dim == 1 && lc.pcr_mode == 1);
+  size_t off = 0;
+  L.off_X = off;
+  off = align_up(off + L.vec_bytes, 256);
+  L.off_Y = L.two_vectors ? off : L.off_X;
+  if (L.two_vectors) off = align_up(off + L.vec_bytes, 256);
+  L.off_static = off;
+  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N) * sizeof(double2);
+  off = align_up(off + L.static_bytes, 256);
+  L.off_alpha = off;
+  const size_t LM = (size_t)g.L * g.M;
+  size_t per = 2 * g.L * sizeof(double);                                 // scale_fwd, scale_bwd
+  per = align_up(per, 16);
+  per += 2 * LM * g.M * sizeof(double2);                                   // Sinv, SG
+  per += LM * sizeof(double2);                                             // shift
+  if (g.dim == 1) per += LM * g.logN * 2 * sizeof(double2) + LM * sizeof(double2);  // pcr, inv_e
+  L.alpha_bytes_each = align_up(per, 256);
+  off += L.alpha_bytes_each * PINT_MAX_SCHEDULE;
+  L.off_red = off;
+  L.red_bytes = (size_t)(148 * 8 * 2 + 64 + PINT_MAX_SCHEDULE * 8) * sizeof(double) * 2;
+  off = align_up(off + L.red_bytes, 256);
+  L.total = off;
+  return L;
+}
+
+#define CUDA_TRY(c, expr)                                                                 \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      if (c) (c)->poisoned = true;                                                        \
+      return fail(PINT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+    }                                                                                     \
+  } while (0)
+
+extern "C" {
+
+int32_t pint_abi_version(void) { return PINT_ABI_VERSION; }
+
+const char *pint_last_error(void) { return g_err.c_str(); }
+
+size_t pint_workspace_bytes(const pint_problem *p, const pint_dist *d) {
+  if (validate(p, d) != PINT_OK) return 0;
+  Geometry g = make_geometry(p);
+  return make_layout(g, choose_launch(g)).total;
+}
+
+pint_status pint_tableau(int32_t M, double *t, double *Q) {
+  if (M < 1 || M > PINT_MAX_M) return fail(PINT_ERR_INVALID, "M must be in [1, 8]");
+  std::vector<ld> tt, QQ;
+  if (!radau_tableau(M, tt, QQ)) return fail(PINT_ERR_NUMERIC, "Radau root finding failed");
+  for (int i = 0; i < M; ++i) if (t) t[i] = (double)tt[i];
+  for (int i = 0; i < M * M; ++i) if (Q) Q[i] = (double)QQ[i];
+  return PINT_OK;
+}
+
+pint_status pint_adaptive_schedule(int32_t L, double w_inf, double m0, double eps, double tau,
+                                   int32_t K, double *alpha_out, double *m_out) {
+  if (K < 0 || K > 4096 || (K > 0 && !alpha_out)) return fail(PINT_ERR_INVALID, "bad K / output");
+  std::vector<double> a, m;
+  std::string err;
+  if (!adaptive_schedule(L, w_inf, m0, eps, tau, K, a, m, err)) return fail(PINT_ERR_SCHEDULE, err);
+  for (int i = 0; i < K; ++i) alpha_out[i] = a[i];
+  if (m_out) for (int i = 0; i <= K; ++i) m_out[i] = m[i];
+  return PINT_OK;
+}
+
+pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, void *work_dev,
+                        size_t work_bytes, const double *u0_host, const double *forcing_host,
+                        pint_ctx **out) {
+  if (!out) return fail(PINT_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  pint_status s = validate(p, d);
+  if (s != PINT_OK) return s;
+  if (!d) return fail(PINT_ERR_INVALID, "dist is NULL");
+  if (!u_dev || !work_dev || !u0_host) return fail(PINT_ERR_INVALID, "NULL buffer");
+  if (forcing_host) return fail(PINT_ERR_INVALID, "forcing b != 0 is not supported in this build");
+  if (((uintptr_t)u_dev) % 16) return fail(PINT_ERR_INVALID, "u_dev must be 16-byte aligned");
+  if (((uintptr_t)work_dev) % 256) return fail(PINT_ERR_INVALID, "work_dev must be 256-byte aligned");
+  Geometry g = make_geometry(p);
+  LaunchCfg lc = choose_launch(g);
+  Layout lay = make_layout(g, lc);
+  if (work_bytes < lay.total) return fail(PINT_ERR_INVALID, "work_bytes < pint_workspace_bytes");
+
+  pint_ctx *c = new pint_ctx();
+  c->prob = *p;
+  c->dist = *d;
+  c->g = g;
+  c->lc = lc;
+  c->lay = lay;
+  c->stream = (cudaStream_t)d->stream;
+  c->work = (char *)work_dev;
+  c->u = (double2 *)u_dev;
+  if (!radau_tableau(p->M, c->t, c->Q)) {
+    delete c;
+    return fail(PINT_ERR_NUMERIC, "Radau root finding failed");
+  }
+  for (int m = 0; m < p->M; ++m)
+    for (int j = 0; j < p->M; ++j) c->g.dTQ[m * p->M + j] = (double)((ld)p->T / p->L * c->Q[m * p->M + j]);
+
+  cudaError_t e = cudaSetDevice(d->device);
+  if (e != cudaSuccess) { delete c; return fail(PINT_ERR_CUDA, cudaGetErrorString(e)); }
+
+  // static tables: twiddles, symbols, u0
+  std::vector<double2> host(lay.static_bytes / sizeof(double2));
+  size_t o = 0;
+  auto tw = [&](int n) {
+    for (int q = 0; q < n; ++q) {
+      cld w = unit_root(q, n, -1);
+      host[o++] = make_double2((double)w.real(), (double)w.imag());
+    }
+  };
+  size_t o_twL = o; tw(g.L);
+  size_t o_twx = o; tw(g.nx);
+  size_t o_twy = o; tw(g.ny);
+  auto lam = [&](int n, double coef) {
+    for (int k = 0; k < n; ++k) {
+      if (p->op == PINT_OP_HEAT) {
+        ld sn = sinl(3.141592653589793238462643383279502884L * k / n);
+        host[o++] = make_double2((double)(-4.0L * coef * (ld)n * n * sn * sn), 0.0);
+      } else {
+        cld w = unit_root(k, n, +1);  // sin(2 pi k / n) = Im e^{+2 pi i k/n}
+        host[o++] = make_double2(0.0, (double)(-(ld)coef * n * w.imag()));
+      }
+    }
+  };
+  size_t o_lx = o; lam(g.nx, p->op == PINT_OP_HEAT ? p->nu : p->cx);
+  size_t o_ly = o; lam(g.ny, p->op == PINT_OP_HEAT ? p->nu : p->cy);
+  if (g.dim == 1) for (size_t i = o_ly; i < o_ly + g.ny; ++i) host[i] = make_double2(0, 0);
+  size_t o_u0 = o;
+  c->u0.assign(u0_host, u0_host + 2 * (size_t)g.N);
+  for (int n = 0; n < g.N; ++n) host[o++] = make_double2(u0_host[2 * n], u0_host[2 * n + 1]);
+  double2 *sbase = (double2 *)(c->work + lay.off_static);
+  CUDA_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+  c->st.twL = sbase + o_twL;
+  c->st.twx = sbase + o_twx;
+  c->st.twy = sbase + o_twy;
+  c->st.lamx = sbase + o_lx;
+  c->st.lamy = sbase + o_ly;
+  c->st.u0 = sbase + o_u0;
+  Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
+            (double *)(c->work + lay.off_red)};
+  CUDA_TRY(c, launch_init_iterate(c->g, c->st, b, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // host staging buffer goes out of scope
+  *out = c;
+  return PINT_OK;
+}
+
+static Buffers buffers(pint_ctx *c) {
+  return Buffers{c->u, (double2 *)(c->work + c->lay.off_X), (double2 *)(c->work + c->lay.off_Y),
+                 (double *)(c->work + c->lay.off_red)};
+}
+
+pint_status pint_w_inf(pint_ctx *c, double *w_inf) {
+  if (!c || !w_inf) return fail(PINT_ERR_INVALID, "NULL argument");
+  double m = 0;
+  for (int n = 0; n < c->g.N; ++n) m = std::fmax(m, std::hypot(c->u0[2 * n], c->u0[2 * n + 1]));
+  *w_inf = m;
+  return PINT_OK;
+}
+
+pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (K < 0 || K > PINT_MAX_SCHEDULE || (K > 0 && !alpha))
+    return fail(PINT_ERR_INVALID, "K must be in [0, PINT_MAX_SCHEDULE]");
+  for (int a = 0; a < K; ++a)
+    if (!(alpha[a] > 0.0 && alpha[a] < 1.0)) return fail(PINT_ERR_SCHEDULE, "alpha must be in (0, 1)");
+  const Geometry &g = c->g;
+  const int L = g.L, M = g.M;
+  const ld dT = (ld)c->prob.T / L;
+  // A's stencil as (sub, diag, super) for the 1-D PCR coefficients
+  ld aA, bA, cA;
+  if (c->prob.op == PINT_OP_HEAT) {
+    aA = (ld)c->prob.nu * g.nx * g.nx; cA = aA; bA = -2 * aA;
+  } else {
+    aA = (ld)c->prob.cx * g.nx / 2; cA = -aA; bA = 0;
+  }
+  std::vector<AlphaTables> tabs(K);
+  std::vector<std::vector<cld>> hS(K), hSi(K), hD(K), hdk(K);
+  std::vector<char> blob(c->lay.alpha_bytes_each);
+  for (int a = 0; a < K; ++a) {
+    std::memset(blob.data(), 0, blob.size());
+    const ld al = alpha[a];
+    double *sf = (double *)blob.data();
+    double *sb = sf + L;
+    size_t off = align_up(2 * L * sizeof(double), 16);
+    double2 *Sinv = (double2 *)(blob.data() + off); off += (size_t)L * M * M * sizeof(double2);
+    double2 *SG = (double2 *)(blob.data() + off); off += (size_t)L * M * M * sizeof(double2);
+    double2 *shift = (double2 *)(blob.data() + off); off += (size_t)L * M * sizeof(double2);
+    double2 *pcr = nullptr, *inv_e = nullptr;
+    size_t off_pcr = 0, off_inv = 0;
+    if (g.dim == 1) {
+      off_pcr = off;
+      pcr = (double2 *)(blob.data() + off); off += (size_t)L * M * g.logN * 2 * sizeof(double2);
+      off_inv = off;
+      inv_e = (double2 *)(blob.data() + off); off += (size_t)L * M * sizeof(double2);
+    }
+    for (int l = 0; l < L; ++l) {
+      sf[l] = (double)powl(al, (ld)l / L);               // alpha^{l/L}
+      sb[l] = (double)(powl(al, -(ld)l / L) / L);        // alpha^{-l/L} / L
+    }
+    hS[a].resize((size_t)L * M * M);
+    hSi[a].resize((size_t)L * M * M);
+    hD[a].resize((size_t)L * M);
+    hdk[a].resize(L);
+    const ld aroot = powl(al, 1.0L / L);
+    for (int k = 0; k < L; ++k) {
+      const int p = bitrev(k, g.logL);
+      const cld dk = -aroot * unit_root(k, L, -1);        // d_k = -alpha^{1/L} e^{-2 pi i k/L}
+      const cld rk = dk / (1.0L + dk);                     // r_k = d_k / (1 + d_k)
+      hdk[a][k] = dk;
+      std::vector<cld> B((size_t)M * M);
+      for (int m = 0; m < M; ++m)
+        for (int j = 0; j < M; ++j)
+          B[(size_t)m * M + j] = c->Q[(size_t)m * M + j] - (j == M - 1 ? rk * c->t[m] : cld(0));  // Q - r D_t H
+      std::vector<cld> lam, S, Si;
+      ld cond, gap;
+      if (!eig_diagonalize(M, B, lam, S, Si, cond, gap)) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "Q G_k^{-1} not safely diagonalisable for alpha=%.6g, k=%d (cond=%.3Lg gap=%.3Lg)",
+                 (double)al, k, cond, gap);
+        return fail(PINT_ERR_NOT_DIAGONALIZABLE, buf);
+      }
+      for (int i = 0; i < M * M; ++i) { hS[a][(size_t)k * M * M + i] = S[i]; hSi[a][(size_t)k * M * M + i] = Si[i]; }
+      for (int m = 0; m < M; ++m) hD[a][(size_t)k * M + m] = lam[m];
+      for (int m = 0; m < M; ++m)
+        for (int j = 0; j < M; ++j) {
+          cld v = Si[(size_t)m * M + j];
+          Sinv[((size_t)p * M + m) * M + j] = make_double2((double)v.real(), (double)v.imag());
+          cld w = S[(size_t)m * M + j] - rk * S[(size_t)(M - 1) * M + j];   // (I - r H_M) S
+          SG[((size_t)p * M + m) * M + j] = make_double2((double)w.real(), (double)w.imag());
+        }
+      for (int m = 0; m < M; ++m) {
+        const cld s = lam[m] * dT;                          // (I - d_km dT A)
+        shift[(size_t)p * M + m] = make_double2((double)s.real(), (double)s.imag());
+        if (g.dim == 1) {
+          // row-sum-carrying PCR coefficients (reading R6): e = a + b + c = 1 - s*(aA+bA+cA)
+          cld ca = -s * aA, cc = -s * cA;
+          cld e = 1.0L - s * (aA + bA + cA);
+          cld cb = e - ca - cc;
+          double2 *lev = pcr + ((size_t)p * M + m) * g.logN * 2;
+          for (int j = 0; j < g.logN - 1; ++j) {
+            cld pj = ca / cb, qj = cc / cb;
+            lev[2 * j] = make_double2((double)pj.real(), (double)pj.imag());
+            lev[2 * j + 1] = make_double2((double)qj.real(), (double)qj.imag());
+            cld e2 = e * (e - 2.0L * (ca + cc)) / cb;
+            cld a2 = -ca * ca / cb, c2 = -cc * cc / cb;
+            ca = a2; cc = c2; e = e2; cb = e - ca - cc;
+          }
+          cld pl = (ca + cc) / cb;                          // pair level: i-h == i+h
+          lev[2 * (g.logN - 1)] = make_double2((double)pl.real(), (double)pl.imag());
+          lev[2 * (g.logN - 1) + 1] = make_double2(0.0, 0.0);
+          e = e * (e - 2.0L * (ca + cc)) / cb;
+          cld ie = 1.0L / e;
+          inv_e[(size_t)p * M + m] = make_double2((double)ie.real(), (double)ie.imag());
+        }
+      }
+    }
+    char *dst = c->work + c->lay.off_alpha + (size_t)a * c->lay.alpha_bytes_each;
+    CUDA_TRY(c, cudaMemcpyAsync(dst, blob.data(), blob.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    AlphaTables &t = tabs[a];
+    t.scale_fwd = (const double *)dst;
+    t.scale_bwd = (const double *)dst + L;
+    size_t o2 = align_up(2 * L * sizeof(double), 16);
+    t.Sinv = (const double2 *)(dst + o2); o2 += (size_t)L * M * M * sizeof(double2);
+    t.SG = (const double2 *)(dst + o2); o2 += (size_t)L * M * M * sizeof(double2);
+    t.shift = (const double2 *)(dst + o2); o2 += (size_t)L * M * sizeof(double2);
+    t.pcr = g.dim == 1 ? (const double2 *)(dst + off_pcr) : nullptr;
+    t.inv_e = g.dim == 1 ? (const double2 *)(dst + off_inv) : nullptr;
+  }
+  c->at = tabs;
+  c->alphas.assign(alpha, alpha + K);
+  c->h_S = hS;
+  c->h_Sinv = hSi;
+  c->h_dkm = hD;
+  c->h_dk = hdk;
+  c->k = 0;
+  return PINT_OK;
+}
+
+static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
+  Buffers b = buffers(c);
+  const AlphaTables &at = c->at[a];
+  CUDA_TRY(c, launch_forward(c->g, c->lc, c->st, at, b, c->stream));
+  double2 *x2 = nullptr;
+  CUDA_TRY(c, launch_solve(c->g, c->lc, c->st, at, b, c->stream, &x2));
+  CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, diff_slot, c->stream));
+  return PINT_OK;
+}
+
+pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (n_iter < 0) return fail(PINT_ERR_INVALID, "n_iter < 0");
+  if (c->k + n_iter > (int)c->alphas.size())
+    return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
+  double *slots = nullptr;
+  if (last_step_diff_inf && n_iter > 0) {
+    slots = (double *)(c->work + c->lay.off_red) + 148 * 8 * 2 + 64;
+    if (n_iter > PINT_MAX_SCHEDULE) return fail(PINT_ERR_INVALID, "n_iter too large");
+    CUDA_TRY(c, cudaMemsetAsync(slots, 0, n_iter * sizeof(double), c->stream));
+  }
+  for (int i = 0; i < n_iter; ++i) {
+    pint_status s = run_iteration(c, c->k, slots ? slots + i : nullptr);
+    if (s != PINT_OK) return s;
+    c->k++;
+  }
+  if (slots) {
+    CUDA_TRY(c, cudaMemcpyAsync(last_step_diff_inf, slots, n_iter * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  return PINT_OK;
+}
+
+pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  Buffers b = buffers(c);
+  double *out2 = (double *)(c->work + c->lay.off_red) + 148 * 8 * 2;
+  CUDA_TRY(c, launch_residual_norm(c->g, c->st, b, out2, c->stream));
+  double h[2];
+  CUDA_TRY(c, cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (l2) *l2 = h[0];
+  if (linf) *linf = h[1];
+  if (!std::isfinite(h[0]) || !std::isfinite(h[1])) return fail(PINT_ERR_NUMERIC, "non-finite residual");
+  return PINT_OK;
+}
+
+pint_status pint_get_iterate(pint_ctx *c, double *u_host) {
+  if (!c || !u_host) return fail(PINT_ERR_INVALID, "NULL argument");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u, c->lay.vec_bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PINT_OK;
+}
+
+pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
+  if (!c || !u_host) return fail(PINT_ERR_INVALID, "NULL argument");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  const size_t off = ((size_t)(c->g.L - 1) * c->g.M + (c->g.M - 1)) * c->g.N;
+  CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u + off, (size_t)c->g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PINT_OK;
+}
+
+pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t reset_iterate) {
+  if (!c || !u0_host) return fail(PINT_ERR_INVALID, "NULL argument");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  c->u0.assign(u0_host, u0_host + 2 * (size_t)c->g.N);
+  CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, u0_host, (size_t)c->g.N * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+  if (reset_iterate) {
+    CUDA_TRY(c, launch_init_iterate(c->g, c->st, buffers(c), c->stream));
+    c->k = 0;
+  }
+  return PINT_OK;
+}
+
+pint_status pint_destroy(pint_ctx *c) {
+  delete c;
+  return PINT_OK;
+}
+
+int32_t pint_launches_per_iteration(pint_ctx *c) {
+  if (!c) return -1;
+  return launches_per_iteration(c->g, c->lc);
+}
+
+pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, double *S, double *Sinv,
+                             double *d_km) {
+  if (!c || a < 0 || a >= (int)c->h_S.size() || k < 0 || k >= c->g.L)
+    return fail(PINT_ERR_INVALID, "bad schedule entry / frequency");
+  const int M = c->g.M;
+  if (d_k) { d_k[0] = (double)c->h_dk[a][k].real(); d_k[1] = (double)c->h_dk[a][k].imag(); }
+  for (int i = 0; i < M * M; ++i) {
+    if (S) { S[2 * i] = (double)c->h_S[a][(size_t)k * M * M + i].real(); S[2 * i + 1] = (double)c->h_S[a][(size_t)k * M * M + i].imag(); }
+    if (Sinv) { Sinv[2 * i] = (double)c->h_Sinv[a][(size_t)k * M * M + i].real(); Sinv[2 * i + 1] = (double)c->h_Sinv[a][(size_t)k * M * M + i].imag(); }
+  }
+  if (d_km)
+    for (int m = 0; m < M; ++m) { d_km[2 * m] = (double)c->h_dkm[a][(size_t)k * M + m].real(); d_km[2 * m + 1] = (double)c->h_dkm[a][(size_t)k * M + m].imag(); }
+  return PINT_OK;
+}
+
+pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s) {
+  if (!c || a < 0 || a >= (int)c->at.size()) return fail(PINT_ERR_INVALID, "bad schedule entry");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  Buffers b = buffers(c);
+  const AlphaTables &at = c->at[a];
+  if (s == 0) CUDA_TRY(c, launch_forward(c->g, c->lc, c->st, at, b, c->stream));
+  else if (s == 1) { double2 *x2; CUDA_TRY(c, launch_solve(c->g, c->lc, c->st, at, b, c->stream, &x2)); }
+  else if (s == 2) {
+    double2 *x2 = (c->g.dim == 1 && c->lc.pcr_mode == 1) ? b.Y : b.X;
+    CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, nullptr, c->stream));
+  } else return fail(PINT_ERR_INVALID, "stage must be 0, 1 or 2");
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PINT_OK;
+}
+
+pint_status pint_debug_get_work(pint_ctx *c, int32_t which, double *host) {
+  if (!c || !host) return fail(PINT_ERR_INVALID, "NULL argument");
+  Buffers b = buffers(c);
+  const double2 *src = which == 0 ? b.X : ((c->g.dim == 1 && c->lc.pcr_mode == 1) ? b.Y : b.X);
+  CUDA_TRY(c, cudaMemcpyAsync(host, src, c->lay.vec_bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PINT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+"""Thin ctypes binding of libpint (include/pint.h).  Argument marshalling only: every step of the
+iteration runs in the library's CUDA kernels.  PyTorch supplies device memory and the stream.
+
+There is NO fallback: if libpint.so is missing or no CUDA device is present the product path
+raises.  (The CPU oracle lives in oracle/ and is test infrastructure only.)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpint.so")
+
+PINT_OK = 0
+STATUS = {0: "PINT_OK", 1: "PINT_ERR_INVALID", 2: "PINT_ERR_SCHEDULE", 3: "PINT_ERR_NOT_DIAGONALIZABLE",
+          4: "PINT_ERR_NUMERIC", 5: "PINT_ERR_CUDA", 6: "PINT_ERR_NCCL", 7: "PINT_ERR_STATE"}
+OPS = {"heat": 0, "advection": 1}
+MAX_SCHEDULE = 64
+
+# every symbol include/pint.h declares (checked by tests/test_abi.py)
+EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pint_w_inf",
+           "pint_set_alpha_schedule", "pint_iterate", "pint_residual_norm", "pint_get_iterate",
+           "pint_get_final_value", "pint_set_initial_value", "pint_destroy", "pint_last_error",
+           "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
+           "pint_debug_stage", "pint_debug_get_work"]
+
+
+class PintError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("op", ctypes.c_int32), ("nu", ctypes.c_double), ("cx", ctypes.c_double),
+                ("cy", ctypes.c_double), ("T", ctypes.c_double), ("L", ctypes.c_int32),
+                ("M", ctypes.c_int32)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
+                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads libpint.so (raises if missing — there is no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libpint.so not built at {path}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, D, vp, dp = ctypes.POINTER(Problem), ctypes.POINTER(Dist), ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)
+    i32 = ctypes.c_int32
+    sig = {
+        "pint_workspace_bytes": (ctypes.c_size_t, [P, D]),
+        "pint_create": (i32, [P, D, vp, vp, ctypes.c_size_t, dp, dp, ctypes.POINTER(vp)]),
+        "pint_adaptive_schedule": (i32, [i32, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                         i32, dp, dp]),
+        "pint_w_inf": (i32, [vp, dp]),
+        "pint_set_alpha_schedule": (i32, [vp, dp, i32]),
+        "pint_iterate": (i32, [vp, i32, dp]),
+        "pint_residual_norm": (i32, [vp, dp, dp]),
+        "pint_get_iterate": (i32, [vp, dp]),
+        "pint_get_final_value": (i32, [vp, dp]),
+        "pint_set_initial_value": (i32, [vp, dp, i32]),
+        "pint_destroy": (i32, [vp]),
+        "pint_last_error": (ctypes.c_char_p, []),
+        "pint_abi_version": (i32, []),
+        "pint_launches_per_iteration": (i32, [vp]),
+        "pint_get_factors": (i32, [vp, i32, i32, dp, dp, dp, dp]),
+        "pint_tableau": (i32, [i32, dp, dp]),
+        "pint_debug_stage": (i32, [vp, i32, i32]),
+        "pint_debug_get_work": (i32, [vp, i32, dp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != PINT_OK:
+        raise PintError(st, _lib.pint_last_error().decode())
+
+
+def _dp(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def make_problem(p) -> Problem:
+    """p: any object with dim, nx, ny, op, nu, cx, cy, T, L, M (e.g. workloads.Problem)."""
+    return Problem(p.dim, p.nx, p.ny if p.dim == 2 else 1, OPS[p.op], p.nu, p.cx, p.cy, p.T, p.L, p.M)
+
+
+def tableau(M: int):
+    lib = load_library()
+    t = np.zeros(M)
+    Q = np.zeros((M, M))
+    _check(lib.pint_tableau(M, _dp(t), _dp(Q)))
+    return t, Q
+
+
+def adaptive_schedule(L: int, w_inf: float, m0: float, K: int, eps: float = 2.0 ** -52, tau: float = 0.0):
+    lib = load_library()
+    a = np.zeros(max(K, 1))
+    m = np.zeros(K + 1)
+    _check(lib.pint_adaptive_schedule(L, w_inf, m0, eps, tau, K, _dp(a), _dp(m)))
+    return a[:K].copy(), m
+
+
+class Solver:
+    """One Paralpha context on one GPU.  Device buffers are torch tensors (complex128)."""
+
+    def __init__(self, problem, u0: np.ndarray, device: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("pint needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.problem = problem
+        self.cp = make_problem(problem)
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.dist = Dist(0, 1, None, device, ctypes.c_void_p(self.stream.cuda_stream))
+        nbytes = self.lib.pint_workspace_bytes(ctypes.byref(self.cp), ctypes.byref(self.dist))
+        if nbytes == 0:
+            raise PintError(1, self.lib.pint_last_error().decode())
+        self.L, self.M, self.N = problem.L, problem.M, problem.nx * (problem.ny if problem.dim == 2 else 1)
+        self.u = torch.empty((self.L, self.M, self.N), dtype=torch.complex128, device=self.device)
+        self.work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        u0h = np.ascontiguousarray(np.asarray(u0, dtype=np.complex128)).view(np.float64)
+        ctx = ctypes.c_void_p()
+        _check(self.lib.pint_create(ctypes.byref(self.cp), ctypes.byref(self.dist), ctypes.c_void_p(self.u.data_ptr()),
+                                    ctypes.c_void_p(self.work.data_ptr()), nbytes, _dp(u0h), None, ctypes.byref(ctx)))
+        self.ctx = ctx
+        self.workspace_bytes = nbytes
+
+    # -- schedule
+    def w_inf(self) -> float:
+        v = ctypes.c_double()
+        _check(self.lib.pint_w_inf(self.ctx, ctypes.byref(v)))
+        return v.value
+
+    def set_alpha_schedule(self, alphas: Sequence[float]):
+        a = np.ascontiguousarray(np.asarray(alphas, dtype=np.float64))
+        _check(self.lib.pint_set_alpha_schedule(self.ctx, _dp(a), len(a)))
+
+    # -- iteration
+    def iterate(self, n: int = 1, want_diff: bool = False):
+        if want_diff:
+            d = np.zeros(n)
+            _check(self.lib.pint_iterate(self.ctx, n, _dp(d)))
+            return d
+        _check(self.lib.pint_iterate(self.ctx, n, None))
+        return None
+
+    def residual_norm(self):
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(self.lib.pint_residual_norm(self.ctx, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def get_iterate(self) -> np.ndarray:
+        out = np.empty((self.L, self.M, self.N), dtype=np.complex128)
+        _check(self.lib.pint_get_iterate(self.ctx, _dp(out.view(np.float64))))
+        return out
+
+    def get_final_value(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.N, dtype=np.complex128)
+        _check(self.lib.pint_get_final_value(self.ctx, _dp(out.view(np.float64))))
+        return out
+
+    def set_initial_value(self, u0: np.ndarray, reset: bool = True):
+        u0h = np.ascontiguousarray(np.asarray(u0, dtype=np.complex128)).view(np.float64)
+        _check(self.lib.pint_set_initial_value(self.ctx, _dp(u0h), 1 if reset else 0))
+
+    def launches_per_iteration(self) -> int:
+        return int(self.lib.pint_launches_per_iteration(self.ctx))
+
+    def factors(self, a: int, k: int):
+        M = self.M
+        dk = np.zeros(2)
+        S = np.zeros(2 * M * M)
+        Si = np.zeros(2 * M * M)
+        dkm = np.zeros(2 * M)
+        _check(self.lib.pint_get_factors(self.ctx, a, k, _dp(dk), _dp(S), _dp(Si), _dp(dkm)))
+        c = lambda v: v.view(np.complex128)
+        return c(dk)[0], c(S).reshape(M, M), c(Si).reshape(M, M), c(dkm)
+
+    def debug_stage(self, a: int, s: int):
+        _check(self.lib.pint_debug_stage(self.ctx, a, s))
+
+    def debug_work(self, which: int) -> np.ndarray:
+        out = np.empty((self.L, self.M, self.N), dtype=np.complex128)
+        _check(self.lib.pint_debug_get_work(self.ctx, which, _dp(out.view(np.float64))))
+        return out
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.pint_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,105 @@
+"""C-ABI library: loads, exports every symbol include/pint.h declares, host-only entry points and
+validation (no kernel launches — runs without a GPU)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2103_12571_b200 as P
+import workloads as W
+from oracle.collocation import Tableau
+from oracle.schedule import adaptive_schedule as oracle_schedule
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "pint.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pint_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = P.load_library()
+    declared = header_functions()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(P.EXPORTS) == declared
+    assert lib.pint_abi_version() == 1
+
+
+def test_nm_shows_extern_c_symbols():
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", P.pint.LIB_PATH], capture_output=True, text=True).stdout
+    for name in header_functions():
+        assert re.search(rf"\bT {name}$", out, flags=re.M), name
+
+
+@pytest.mark.parametrize("M", range(1, 9))
+def test_library_tableau_matches_oracle(M):
+    t, Q = P.tableau(M)
+    tab = Tableau(M)
+    np.testing.assert_allclose(t, tab.t, atol=2e-16)
+    np.testing.assert_allclose(Q, tab.Q, atol=1e-15 if M <= 5 else 5e-13)
+    assert t[-1] == 1.0
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_library_schedule_matches_oracle(cfg):
+    p = W.CONFIGS[cfg]
+    w_inf = float(np.abs(p.u0()).max()) if cfg != 5 else 1.0
+    a_lib, m_lib = P.adaptive_schedule(p.L, w_inf, p.m0, p.iters)
+    a_or, m_or = oracle_schedule(p.L, w_inf, p.m0, p.iters)
+    np.testing.assert_allclose(a_lib, a_or, rtol=1e-14)
+    np.testing.assert_allclose(m_lib, m_or, rtol=1e-14)
+
+
+def test_schedule_error_path():
+    with pytest.raises(P.PintError) as e:
+        P.adaptive_schedule(1, 1.0, 1e-30, 3)
+    assert e.value.status == 2
+
+
+def _ws(**kw):
+    lib = P.load_library()
+    base = dict(dim=1, nx=64, ny=1, op="heat", nu=1.0, cx=0.0, cy=0.0, T=0.1, L=4, M=2)
+    base.update(kw)
+
+    class Pr:
+        pass
+
+    pr = Pr()
+    for k, v in base.items():
+        setattr(pr, k, v)
+    cp = P.make_problem(pr)
+    d = P.pint.Dist(0, 1, None, 0, None)
+    return lib.pint_workspace_bytes(ctypes.byref(cp), ctypes.byref(d)), lib.pint_last_error().decode()
+
+
+def test_workspace_and_validation():
+    n, _ = _ws()
+    assert n >= 4 * 2 * 64 * 16
+    n3, _ = _ws(nx=65536, L=256, M=3, nu=1e-2, T=1.0)
+    assert n3 >= 2 * 256 * 3 * 65536 * 16        # two work vectors for the two-pass PCR
+    n5, _ = _ws(dim=2, nx=1024, ny=1024, op="advection", cx=1.0, cy=0.5, L=512, M=4, T=1.0)
+    assert 512 * 4 * 1024 * 1024 * 16 <= n5 < 1.1 * 512 * 4 * 1024 * 1024 * 16
+    for bad, msg in [(dict(L=3), "power of two"), (dict(nx=48), "power of two"), (dict(M=9), "M must"),
+                     (dict(dim=3), "dim"), (dict(T=-1.0), "T must"), (dict(dim=2, ny=1), "ny")]:
+        n, err = _ws(**bad)
+        assert n == 0 and msg in err, (bad, err)
+
+
+def test_create_rejects_null_and_nranks():
+    lib = P.load_library()
+
+    class Pr:
+        dim, nx, ny, op, nu, cx, cy, T, L, M = 1, 64, 1, "heat", 1.0, 0.0, 0.0, 0.1, 4, 2
+
+    cp = P.make_problem(Pr)
+    d = P.pint.Dist(0, 2, None, 0, None)
+    ctx = ctypes.c_void_p()
+    st = lib.pint_create(ctypes.byref(cp), ctypes.byref(d), None, None, 0, None, None, ctypes.byref(ctx))
+    assert st == 1 and "nranks" in lib.pint_last_error().decode()

@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, per iteration, on the same
+seeded inputs.  Bar (north star): relative l2 <= 1e-9 after every iteration."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle.paralpha import ModeOracle, Oracle, mode_coefficients, relative_l2
+from oracle.schedule import adaptive_schedule as oracle_schedule
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def _solver(p, u0):
+    import paper_2103_12571_b200 as P
+    return P.Solver(p, u0)
+
+
+def schedules(p, u0, s=None):
+    """(oracle alphas, library alphas) — each side computes its own."""
+    if p.alpha_mode == "fixed":
+        a = [p.alpha_fixed] * p.iters
+        return a, a
+    w_inf = float(np.abs(u0).max())
+    a_or, _ = oracle_schedule(p.L, w_inf, p.m0, p.iters, p.eps, p.tau)
+    import paper_2103_12571_b200 as P
+    w_lib = s.w_inf() if s is not None else w_inf
+    a_lib, _ = P.adaptive_schedule(p.L, w_lib, p.m0, p.iters, p.eps, p.tau)
+    np.testing.assert_allclose(a_lib, a_or, rtol=1e-14)
+    return list(a_or), list(a_lib)
+
+
+def run_parity(p, tier="auto", iters=None):
+    u0 = p.u0()
+    s = _solver(p, u0)
+    a_or, a_lib = schedules(p, u0, s)
+    s.set_alpha_schedule(a_lib)
+    o = Oracle(p, u0, tier)
+    u = o.initial()
+    np.testing.assert_array_equal(s.get_iterate(), u)
+    errs = []
+    for k in range(iters or p.iters):
+        u = o.iterate(u, a_or[k])
+        s.iterate(1)
+        ug = s.get_iterate()
+        errs.append(relative_l2(ug, u))
+    s.close()
+    assert max(errs) <= TOL, errs
+    return errs
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_parity_full_size(cfg):
+    run_parity(W.CONFIGS[cfg])
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_parity_reduced(cfg):
+    run_parity(W.reduced(cfg))
+
+
+@pytest.mark.parametrize("p", W.edge_cases(), ids=lambda p: p.name)
+def test_parity_edge_cases(p):
+    run_parity(p, tier="dense")
+
+
+def test_parity_two_pass_pcr_small():
+    """1-D with N > 4096 switches to the two-pass (classes + chunks) PCR; keep the oracle fast."""
+    p = W.CONFIGS[3].replace(name="twopass_N16384_L8", nx=16384, L=8, iters=4)
+    run_parity(p)
+
+
+def test_last_step_diff_and_residual_norm():
+    p = W.CONFIGS[2].replace(L=16, iters=4)
+    u0 = p.u0()
+    s = _solver(p, u0)
+    a = [1e-5, 1e-4, 1e-3, 1e-2]
+    s.set_alpha_schedule(a)
+    o = Oracle(p, u0)
+    u = o.initial()
+    for k in range(4):
+        un = o.iterate(u, a[k])
+        d = s.iterate(1, want_diff=True)[0]
+        ref = float(np.abs(un[-1] - u[-1]).max())
+        assert d == pytest.approx(ref, rel=1e-6, abs=1e-14)
+        l2, linf = s.residual_norm()
+        rl2, rlinf = o.residual_norms(un)
+        assert l2 == pytest.approx(rl2, rel=1e-3, abs=1e-13) and linf == pytest.approx(rlinf, rel=1e-3, abs=1e-13)
+        u = un
+    np.testing.assert_allclose(s.get_final_value(), u[-1, -1], rtol=0, atol=1e-10 * np.abs(u).max())
+
+
+def test_schedule_exhausted_and_bad_alpha():
+    import paper_2103_12571_b200 as P
+    p = W.CONFIGS[1]
+    s = _solver(p, p.u0())
+    s.set_alpha_schedule([1e-4])
+    s.iterate(1)
+    with pytest.raises(P.PintError) as e:
+        s.iterate(1)
+    assert e.value.status == 2
+    with pytest.raises(P.PintError) as e:
+        s.set_alpha_schedule([1.5])
+    assert e.value.status == 2
+    s.iterate(0)  # empty call is a no-op
+
+
+def test_factor_tables_diagonalise():
+    """Host tables: S D S^{-1} = Q - r_k D_t H_M and d_k = -alpha^{1/L} e^{-2 pi i k/L}."""
+    from oracle.collocation import Tableau
+    p = W.CONFIGS[2].replace(L=16)
+    s = _solver(p, p.u0())
+    s.set_alpha_schedule([1e-5, 0.3])
+    tab = Tableau(p.M)
+    for a, al in enumerate([1e-5, 0.3]):
+        for k in range(p.L):
+            dk, S, Si, dkm = s.factors(a, k)
+            assert dk == pytest.approx(-al ** (1 / p.L) * np.exp(-2j * np.pi * k / p.L), abs=1e-15)
+            r = dk / (1 + dk)
+            B = tab.Q - r * tab.Dt @ tab.H
+            np.testing.assert_allclose(S @ np.diag(dkm) @ Si, B, atol=1e-13)
+            np.testing.assert_allclose(S @ Si, np.eye(p.M), atol=1e-13)
+
+
+# ---- full BASELINE sizes: sampled spatial modes (the oracle computes each mode exactly) ----------
+
+def _mode_sample(p, cfg):
+    rng = np.random.default_rng(100 + cfg)
+    if cfg == 3:
+        k = np.arange(1, 17)
+        kx = np.concatenate([k, p.nx - k, rng.integers(0, p.nx, 8)])
+        ky = np.zeros_like(kx)
+    elif cfg == 4:
+        ks = W.fourier2d_wavevectors(32)
+        pick = rng.choice(len(ks), 48, replace=False)
+        kx = np.array([ks[i][0] % p.nx for i in pick] + list(rng.integers(0, p.nx, 8)))
+        ky = np.array([ks[i][1] % p.ny for i in pick] + list(rng.integers(0, p.ny, 8)))
+    else:
+        kx = np.concatenate([np.arange(0, 6).repeat(6), rng.integers(0, p.nx, 12)])
+        ky = np.concatenate([np.tile(np.arange(0, 6), 6), rng.integers(0, p.ny, 12)])
+    return kx, ky
+
+
+def _gpu_project(s, p, kx, ky):
+    """uhat[l, m, j] = sum_n u[l, m, n] e^{-2 pi i (kx x/nx + ky y/ny)} of the device iterate, via
+    torch matmuls on the GPU (test-side measurement only)."""
+    import torch
+    dev = s.u.device
+    xs = torch.arange(p.nx, device=dev, dtype=torch.int64)
+    ys = torch.arange(p.ny, device=dev, dtype=torch.int64)
+    kxt = torch.as_tensor(np.asarray(kx), device=dev, dtype=torch.int64)
+    kyt = torch.as_tensor(np.asarray(ky), device=dev, dtype=torch.int64)
+    ex = torch.exp(-2j * np.pi * ((xs[:, None] * kxt[None, :]) % p.nx).to(torch.float64) / p.nx)  # (nx, K)
+    ey = torch.exp(-2j * np.pi * ((ys[:, None] * kyt[None, :]) % p.ny).to(torch.float64) / p.ny)  # (ny, K)
+    L, M = p.L, p.M
+    out = torch.empty((L * M, len(kx)), dtype=torch.complex128, device=dev)
+    U = s.u.view(L * M, p.ny, p.nx)
+    chunk = max(1, (1 << 27) // (p.N * 4))
+    for i in range(0, L * M, chunk):
+        a = torch.matmul(U[i:i + chunk], ex)              # (c, ny, K)
+        out[i:i + chunk] = (a * ey[None]).sum(1)
+    torch.cuda.synchronize()
+    return out.view(L, M, len(kx)).cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_parity_full_size_sampled_modes(cfg):
+    p = W.CONFIGS[cfg]
+    u0 = p.u0()
+    s = _solver(p, u0)
+    a_or, a_lib = schedules(p, u0, s)
+    s.set_alpha_schedule(a_lib)
+    kx, ky = _mode_sample(p, cfg)
+    mo = ModeOracle(p, mode_coefficients(p, u0, kx, ky), kx, ky)
+    uh = mo.initial()
+    errs = []
+    for k in range(p.iters):
+        uh = mo.iterate(uh, a_or[k])
+        s.iterate(1)
+        g = _gpu_project(s, p, kx, ky)
+        errs.append(float(np.linalg.norm((g - uh).ravel()) / np.linalg.norm(uh.ravel())))
+    s.close()
+    assert max(errs) <= TOL, errs
