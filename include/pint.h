@@ -145,6 +145,15 @@ int32_t pint_abi_version(void);
 /* Number of kernel launches one iteration enqueues, and the names of the kernels. */
 int32_t pint_launches_per_iteration(pint_ctx *c);
 
+/* Runs n_iter iterations like pint_iterate (same kernels, same launch configuration) and records a
+ * CUDA event after every launch on the context stream; kernel_ms[i] (pint_launches_per_iteration
+ * entries) receives the average duration of launch i of an iteration.  Synchronises every
+ * iteration. */
+pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms);
+
+/* Name of launch i of an iteration ("" if out of range). */
+const char *pint_kernel_name(pint_ctx *c, int32_t i);
+
 /* Host copies of the factor tables of schedule entry `a` for frequency k (natural order):
  * d_k (2 doubles), S_k, S_k^{-1} (2*M*M doubles each, row-major), d_km (2*M doubles).
  * Any output pointer may be NULL. */

@@ -68,5 +68,14 @@ cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, cons
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,
                                 cudaStream_t s);
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc);
+const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i);
+
+// Optional per-launch event recorder (pint_iterate_profiled): when set, every launch wrapper
+// records ev[n++] on the launch stream right after each kernel it enqueues.
+struct Recorder {
+  cudaEvent_t *ev;
+  int n, cap;
+};
+void set_recorder(Recorder *r);
 
 }  // namespace pint

@@ -521,6 +521,12 @@ __global__ void init_iterate_kernel(Geometry g, const double2 *__restrict__ u0, 
 // ---------------------------------------------------------------------------------------------
 // host-side launch logic
 
+static thread_local Recorder *g_rec = nullptr;
+void set_recorder(Recorder *r) { g_rec = r; }
+static inline void rec(cudaStream_t s) {
+  if (g_rec && g_rec->n < g_rec->cap) cudaEventRecord(g_rec->ev[g_rec->n++], s);
+}
+
 static int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -567,10 +573,20 @@ int launches_per_iteration(const Geometry &g, const LaunchCfg &lc) {
   return lc.pcr_mode == 0 ? 3 : 4;
 }
 
+const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i) {
+  static const char *k1a[] = {"fwd_kernel", "pcr_classes_kernel", "bwd_kernel"};
+  static const char *k1b[] = {"fwd_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
+  static const char *k2[] = {"fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
+                             "fft2d_rows_kernel<inv>", "bwd_kernel"};
+  const int n = launches_per_iteration(g, lc);
+  if (i < 0 || i >= n) return "";
+  if (g.dim == 2) return k2[i];
+  return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
+}
+
 static cudaError_t set_smem(const void *fn, size_t bytes) {
-  if (bytes > 48 * 1024)
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  return cudaSuccess;
+  // always opt in: static shared memory (reduction scratch) adds to the dynamic bytes
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 #define PINT_DISPATCH_M(M_, ...)       \
@@ -595,6 +611,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     e = set_smem((const void *)fwd_kernel<MM>, smem);
     if (e == cudaSuccess) fwd_kernel<MM><<<grid, 256, smem, s>>>(g, st, at, b.u, b.X, T);
   });
+  rec(s);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -608,6 +625,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       const size_t smem = (size_t)g.N * sizeof(double2);
       if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
       pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0);
+      rec(s);
       *out = b.X;
     } else {
       const int R = lc.pcr_R, T = lc.pcr_T, jA = 0;
@@ -617,11 +635,13 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       size_t smem = (size_t)nq * T * sizeof(double2);
       if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
       pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff);
+      rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       const int C = lc.pcr_chunk, H = R;
       smem = (size_t)(C + 2 * H) * sizeof(double2);
       if ((e = set_smem((const void *)pcr_chunk_kernel, smem)) != cudaSuccess) return e;
       pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smem, s>>>(g, at, b.X, b.Y, C, H, jOff);
+      rec(s);
       *out = b.Y;
     }
   } else {
@@ -634,6 +654,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     if ((e = set_smem((const void *)fft2d_rows_kernel<false>, smem)) != cudaSuccess) return e;
     if ((e = set_smem((const void *)fft2d_rows_kernel<true>, smem)) != cudaSuccess) return e;
     fft2d_rows_kernel<false><<<(unsigned)(rows / rpc), kFftThreads, smem, s>>>(g, st, b.X, rpc);
+    rec(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     int T = 4096 / g.ny;
     if (T < 1) T = 1;
@@ -642,8 +663,10 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     size_t smc = (size_t)g.ny * T * sizeof(double2);
     if ((e = set_smem((const void *)fft2d_cols_kernel, smc)) != cudaSuccess) return e;
     fft2d_cols_kernel<<<lines * (g.nx / T), kFftThreads, smc, s>>>(g, st, at, b.X, T);
+    rec(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     fft2d_rows_kernel<true><<<(unsigned)(rows / rpc), kFftThreads, smem, s>>>(g, st, b.X, rpc);
+    rec(s);
     *out = b.X;
   }
   return cudaGetLastError();
@@ -661,6 +684,7 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
     if (e == cudaSuccess)
       bwd_kernel<MM><<<grid, 256, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
   });
+  rec(s);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -481,6 +481,42 @@ pint_status pint_destroy(pint_ctx *c) {
   return PINT_OK;
 }
 
+pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms) {
+  if (!c || !kernel_ms) return fail(PINT_ERR_INVALID, "NULL argument");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (c->k + n_iter > (int)c->alphas.size())
+    return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
+  const int nk = launches_per_iteration(c->g, c->lc);
+  std::vector<cudaEvent_t> ev(nk + 1);
+  for (auto &e : ev) CUDA_TRY(c, cudaEventCreate(&e));
+  for (int i = 0; i < nk; ++i) kernel_ms[i] = 0.0;
+  pint_status st = PINT_OK;
+  for (int it = 0; it < n_iter && st == PINT_OK; ++it) {
+    Recorder r{ev.data() + 1, 0, nk};
+    CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
+    set_recorder(&r);
+    st = run_iteration(c, c->k, nullptr);
+    set_recorder(nullptr);
+    if (st != PINT_OK) break;
+    c->k++;
+    CUDA_TRY(c, cudaEventSynchronize(ev[nk]));
+    for (int i = 0; i < nk; ++i) {
+      float ms = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      kernel_ms[i] += ms;
+    }
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  if (st == PINT_OK && n_iter > 0)
+    for (int i = 0; i < nk; ++i) kernel_ms[i] /= n_iter;
+  return st;
+}
+
+const char *pint_kernel_name(pint_ctx *c, int32_t i) {
+  if (!c) return "";
+  return kernel_name(c->g, c->lc, i);
+}
+
 int32_t pint_launches_per_iteration(pint_ctx *c) {
   if (!c) return -1;
   return launches_per_iteration(c->g, c->lc);

@@ -26,7 +26,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_set_alpha_schedule", "pint_iterate", "pint_residual_norm", "pint_get_iterate",
            "pint_get_final_value", "pint_set_initial_value", "pint_destroy", "pint_last_error",
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
-           "pint_debug_stage", "pint_debug_get_work"]
+           "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name"]
 
 
 class PintError(RuntimeError):
@@ -80,6 +80,8 @@ def load_library(path: str = LIB_PATH):
         "pint_tableau": (i32, [i32, dp, dp]),
         "pint_debug_stage": (i32, [vp, i32, i32]),
         "pint_debug_get_work": (i32, [vp, i32, dp]),
+        "pint_iterate_profiled": (i32, [vp, i32, dp]),
+        "pint_kernel_name": (ctypes.c_char_p, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -188,6 +190,15 @@ class Solver:
 
     def launches_per_iteration(self) -> int:
         return int(self.lib.pint_launches_per_iteration(self.ctx))
+
+    def kernel_names(self):
+        return [self.lib.pint_kernel_name(self.ctx, i).decode() for i in range(self.launches_per_iteration())]
+
+    def iterate_profiled(self, n: int) -> np.ndarray:
+        """Average per-launch device time (ms) of each kernel of an iteration over n iterations."""
+        out = np.zeros(self.launches_per_iteration())
+        _check(self.lib.pint_iterate_profiled(self.ctx, n, _dp(out)))
+        return out
 
     def factors(self, a: int, k: int):
         M = self.M
