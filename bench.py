@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the Paralpha hot path: one alpha-circulant preconditioned Richardson iteration
+(arXiv 2103.12571) per step, metric = space-time unknowns updated per second (L*M*N / t_iter).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl pint|reference]
+
+N > 1 is launched by torchrun (one process per GPU).  Default workload: BASELINE.json config 5
+(2-D advection 1024^2, M=4, L=512; 2.1e9 unknowns, 34.4 GB per vector — fits one B200).
+Prints ONE JSON line on rank 0.  See DESIGN.md §6 for the measurement recipe.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "space-time unknowns updated/s per Richardson iteration (fp64), 1/2/4/8 B200, % HBM roof"
+UNIT = "unknowns/s"
+
+# algorithmic HBM bytes per unknown of each launch (compulsory reads + writes)
+ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32, "fft2d_rows_kernel<fwd>": 32,
+              "fft2d_cols_kernel": 32, "fft2d_rows_kernel<inv>": 32, "bwd_kernel": 48}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def schedule_for(p, w_inf, n):
+    """The config's alpha sequence (fixed, or Algorithm 2 from the library), repeated to length n."""
+    import paper_2103_12571_b200 as P
+    if p.alpha_mode == "fixed":
+        base = [p.alpha_fixed] * p.iters
+    else:
+        base = list(P.adaptive_schedule(p.L, w_inf, p.m0, p.iters, p.eps, p.tau)[0])
+    return [base[i % len(base)] for i in range(n)]
+
+
+def cpu_oracle_rate(p, target_s: float, seed: int = 0):
+    """The oracle (oracle/paralpha.py ModeOracle, as it stands) on a bounded sample of the workload:
+    a random subset of the spatial Fourier modes (each an independent L*M-unknown subproblem of the
+    same iteration), one iteration with the config's first alpha.  Returns (unknowns/s, sample text, s)."""
+    from oracle.paralpha import ModeOracle, mode_coefficients
+    from oracle.schedule import adaptive_schedule
+    u0 = p.u0()
+    if p.alpha_mode == "fixed":
+        a = p.alpha_fixed
+    else:
+        a = adaptive_schedule(p.L, float(np.abs(u0).max()), p.m0, 1, p.eps, p.tau)[0][0]
+    rng = np.random.default_rng(seed)
+
+    def run(nmodes):
+        kx = rng.integers(0, p.nx, nmodes)
+        ky = rng.integers(0, p.ny, nmodes)
+        uh0 = mode_coefficients(p, u0, kx, ky)       # setup (projection of u0), not timed
+        mo = ModeOracle(p, uh0, kx, ky)
+        uh = mo.initial()
+        t0 = time.perf_counter()
+        mo.iterate(uh, a)
+        return time.perf_counter() - t0
+
+    n = 16
+    dt = run(n)
+    while dt < target_s / 4 and n < p.N:
+        n = min(p.N, n * 4)
+        dt = run(n)
+    rate = p.L * p.M * n / dt
+    return rate, f"{n} of {p.N} spatial Fourier modes x all L*M={p.L * p.M} (one iteration, ModeOracle)", dt
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def run_reference(args, p, rank, world):
+    """--impl reference: the CPU oracle as it stands, on this arm's config/metric (rank 0 only)."""
+    if rank != 0:
+        return None
+    per_step = []
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        rate, sample, dt = cpu_oracle_rate(p, target_s=args.ref_step_s, seed=i)
+        if i >= args.warmup:
+            per_step.append((rate, dt))
+    rates = [r for r, _ in per_step]
+    value = float(np.median(rates))
+    cores = threads_used()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(np.median([d for _, d in per_step]) * 1e3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+            "data": "synthetic (workloads.py seeded generators)", "impl": "reference",
+            "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
+                       "unknowns": p.U},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="pint", choices=["pint", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-target-s", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=6.0)
+    args = ap.parse_args()
+    rank, world, local = env_rank()
+    p = W.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        line = run_reference(args, p, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2103_12571_b200 as P
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    u0 = p.u0()
+    s = P.Solver(p, u0, device=local)
+    stream = s.stream
+    w_inf = s.w_inf()
+    nlaunch = s.launches_per_iteration()
+    names = s.kernel_names()
+
+    # ---- device-timed region: W warm-up + K timed iterations, inputs resident in HBM ----------
+    s.set_alpha_schedule(schedule_for(p, w_inf, min(64, args.warmup + args.steps)))
+    for _ in range(args.warmup):
+        s.iterate(1)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        done = 0
+        while done < args.steps:
+            n = min(args.steps - done, 64 - args.warmup if done == 0 else 64)
+            if done > 0:
+                s.set_alpha_schedule(schedule_for(p, w_inf, n))  # only for K > 61 (host work, re-timed)
+            s.iterate(n)
+            done += n
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    value = world * p.U / (ms * 1e-3)
+
+    # ---- per-kernel device times (same kernels, events after every launch) ---------------------
+    nprof = max(3, min(args.steps, 10))
+    s.set_alpha_schedule(schedule_for(p, w_inf, nprof + 1))
+    s.iterate(1)
+    kms = s.iterate_profiled(nprof)
+    peak, peak_src = measured_peaks()
+    top = int(np.argmax(kms))
+    top_name = names[top]
+    algo = ALGO_BYTES.get(top_name, 32) * p.U
+    achieved = algo / (kms[top] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(p.name, {}).get(top_name)
+        except Exception:
+            traffic = None
+    model_bytes = sum(ALGO_BYTES.get(n_, 32) for n_ in names)
+    roofline = {"bound": "hbm", "kernel": top_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algo_bytes_per_launch": algo,
+                "kernel_share_of_step": float(kms[top] / kms.sum()),
+                "per_kernel_ms": {n_: float(v) for n_, v in zip(names, kms)},
+                "iteration": {"model_bytes_per_unknown": model_bytes,
+                              "achieved_gbs": model_bytes * p.U / (ms * 1e-3) / 1e9,
+                              "frac": model_bytes * p.U / (ms * 1e-3) / 1e9 / peak,
+                              "floor96_frac": 96 * p.U / (ms * 1e-3) / 1e9 / peak}}
+
+    # ---- end to end through the public API with host buffers -----------------------------------
+    e2e = None
+    if not args.no_e2e:
+        u0_pin = torch.from_numpy(u0.view(np.float64).copy()).pin_memory()
+        out_pin = torch.empty(2 * p.N, dtype=torch.float64).pin_memory()
+        u0_np = u0_pin.numpy()
+        out_np = out_pin.numpy()
+        s.set_alpha_schedule(schedule_for(p, w_inf, min(64, args.warmup + args.steps)))
+        ke = min(args.steps, 64 - args.warmup)
+
+        def e2e_step():
+            s.set_initial_value(u0_np.view(np.complex128), reset=False)   # H2D of the step's input
+            s.iterate(1)
+            s.get_final_value(out_np.view(np.complex128))                 # D2H of the result (syncs)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ems = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3)) / ke
+        e2e = {"value": world * p.U / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * p.N,
+               "d2h_bytes_per_step": 16 * p.N, "ms_per_step": ems,
+               "what": "per step: H2D u0 (pinned) -> pint_iterate(1) -> D2H u_{L-1,M-1} (solution at T)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, sample, _ = cpu_oracle_rate(p, target_s=args.cpu_target_s)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads_used(), "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "c128 (fp64)",
+                "data": "synthetic (workloads.py seeded generators; BASELINE.json config recipe)",
+                "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
+                           "unknowns": p.U, "bytes_per_vector": 16 * p.U,
+                           "l2": "inputs larger than L2 (no flush)" if 16 * p.U > 126e6 else "L2-resident",
+                           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": nlaunch * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
