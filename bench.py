@@ -30,7 +30,8 @@ UNIT = "unknowns/s"
 
 # algorithmic HBM bytes per unknown of each launch (compulsory reads + writes)
 ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32, "fft2d_rows_kernel<fwd>": 32,
-              "fft2d_cols_kernel": 32, "fft2d_rows_kernel<inv>": 32, "bwd_kernel": 48}
+              "fft2d_cols_kernel": 32, "fft2d_rows_kernel<inv>": 32, "bwd_kernel": 48, "residual2d_kernel": 32,
+              "tfft_fwd_kernel": 32, "tfft_bwd_kernel": 48}
 
 
 def env_rank():
@@ -185,9 +186,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
+    ap.add_argument("--grid", type=int, default=0, help="profiling only: override nx (and ny in 2-D)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     p = W.CONFIGS[args.config]
+    if args.grid:
+        p = p.replace(name=p.name + f"_grid{args.grid}", nx=args.grid, ny=args.grid if p.dim == 2 else 1)
 
     if args.impl == "reference":
         line = run_reference(args, p, rank, world)

@@ -46,7 +46,8 @@ struct Buffers {
 // ---- launch wrappers (kernels.cu) -----------------------------------------------------------
 // All return cudaGetLastError() after enqueueing on `st`.
 struct LaunchCfg {
-  int fwd_T;                  // spatial points per forward/backward tile
+  int fwd_T;                  // spatial points per forward/backward tile (all l x all m, 1-D)
+  int tfft_T;                 // spatial points per 2-D time-FFT tile (all l x one m)
   int pcr_mode;               // 0: single-pass line PCR; 1: two-pass (classes + chunks)
   int pcr_R;                  // residue-class modulus of the two-pass scheme
   int pcr_T;                  // class columns per CTA

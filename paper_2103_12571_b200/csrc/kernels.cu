@@ -16,148 +16,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "device_common.cuh"
 #include "internal.h"
 
 namespace pint {
-
-// ---------------------------------------------------------------------------------------------
-// complex helpers
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-// a * conj(b)
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
-}
-// acc + a * b
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y);
-  acc.y = fma(a.y, b.x, acc.y);
-  return acc;
-}
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-__device__ __forceinline__ int brev(int x, int bits) {
-  return bits == 0 ? 0 : (int)(__brev((unsigned)x) >> (32 - bits));
-}
-
-// ---------------------------------------------------------------------------------------------
-// shared-memory FFT engine: in-place radix-2 stages fused in register groups of 2^B.
-// Element (column c, position p) lives at sm[c*cs + p*ps].  tw[q] = e^{-2 pi i q / n}.
-// DIF (forward, e^{-}): natural input -> bit-reversed output.
-// DIT (inverse, e^{+}): bit-reversed input -> natural output.
-
-template <int B>
-__device__ __forceinline__ void dif_group(double2 *sm, int ncols, int cs, int ps, int n, int m0,
-                                          const double2 *__restrict__ tw) {
-  constexpr int R = 1 << B;
-  const int s = m0 >> B;
-  const int nb = n >> B;
-  const int nitems = ncols * nb;
-  for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
-    int c, jj;
-    if (cs == 1) { c = item % ncols; jj = item / ncols; } else { jj = item % nb; c = item / nb; }
-    const int blk = jj / s, j0 = jj - blk * s;
-    double2 *base = sm + c * cs + (blk * m0 + j0) * ps;
-    double2 v[R];
-#pragma unroll
-    for (int t = 0; t < R; ++t) v[t] = base[t * s * ps];
-#pragma unroll
-    for (int st = 0; st < B; ++st) {
-      const int half_t = 1 << (B - 1 - st);
-      const int twmul = n / (m0 >> st);
-#pragma unroll
-      for (int t = 0; t < R; ++t) {
-        if (t & half_t) continue;
-        const int j = j0 + (t & ((R >> st) - 1)) * s;
-        double2 a = v[t], b = v[t + half_t];
-        v[t] = cadd(a, b);
-        v[t + half_t] = (j == 0) ? csub(a, b) : cmul(csub(a, b), __ldg(tw + j * twmul));
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < R; ++t) base[t * s * ps] = v[t];
-  }
-}
-
-template <int B>
-__device__ __forceinline__ void dit_group(double2 *sm, int ncols, int cs, int ps, int n, int s,
-                                          const double2 *__restrict__ tw) {
-  constexpr int R = 1 << B;
-  const int Mg = s << B;
-  const int nb = n >> B;
-  const int nitems = ncols * nb;
-  for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
-    int c, jj;
-    if (cs == 1) { c = item % ncols; jj = item / ncols; } else { jj = item % nb; c = item / nb; }
-    const int blk = jj / s, j0 = jj - blk * s;
-    double2 *base = sm + c * cs + (blk * Mg + j0) * ps;
-    double2 v[R];
-#pragma unroll
-    for (int t = 0; t < R; ++t) v[t] = base[t * s * ps];
-#pragma unroll
-    for (int st = 0; st < B; ++st) {
-      const int half_t = 1 << st;
-      const int twmul = n / ((2 * s) << st);
-#pragma unroll
-      for (int t = 0; t < R; ++t) {
-        if (t & half_t) continue;
-        const int j = j0 + (t & ((2 << st) - 1)) * s;
-        double2 a = v[t];
-        double2 b = (j == 0) ? v[t + half_t] : cmulc(v[t + half_t], __ldg(tw + j * twmul));
-        v[t] = cadd(a, b);
-        v[t + half_t] = csub(a, b);
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < R; ++t) base[t * s * ps] = v[t];
-  }
-}
-
-// group sizes: split log2 n into ceil(log2 n / 4) groups of <= 4 stages, as even as possible
-__device__ __forceinline__ int group_size(int logn, int done) {
-  int left = logn - done;
-  int ngroups = (left + 3) / 4;
-  return (left + ngroups - 1) / ngroups;
-}
-
-// forward transform (DIF) of ncols columns of length n; ends with __syncthreads()
-__device__ void fft_dif(double2 *sm, int ncols, int cs, int ps, int n, int logn, const double2 *tw) {
-  int done = 0, m0 = n;
-  while (done < logn) {
-    int b = group_size(logn, done);
-    switch (b) {
-      case 1: dif_group<1>(sm, ncols, cs, ps, n, m0, tw); break;
-      case 2: dif_group<2>(sm, ncols, cs, ps, n, m0, tw); break;
-      case 3: dif_group<3>(sm, ncols, cs, ps, n, m0, tw); break;
-      default: dif_group<4>(sm, ncols, cs, ps, n, m0, tw); break;
-    }
-    __syncthreads();
-    done += b;
-    m0 >>= b;
-  }
-}
-
-// inverse transform (DIT, conjugate twiddles, no 1/n); ends with __syncthreads()
-__device__ void fft_dit_inv(double2 *sm, int ncols, int cs, int ps, int n, int logn, const double2 *tw) {
-  int done = 0, s = 1;
-  while (done < logn) {
-    int b = group_size(logn, done);
-    switch (b) {
-      case 1: dit_group<1>(sm, ncols, cs, ps, n, s, tw); break;
-      case 2: dit_group<2>(sm, ncols, cs, ps, n, s, tw); break;
-      case 3: dit_group<3>(sm, ncols, cs, ps, n, s, tw); break;
-      default: dit_group<4>(sm, ncols, cs, ps, n, s, tw); break;
-    }
-    __syncthreads();
-    done += b;
-    s <<= b;
-  }
-}
 
 // ---------------------------------------------------------------------------------------------
 // residual of one (l, n) for all nodes: r_m = w_m - u_m + dT sum_j Q_mj (A u_j) + u_{l-1, M-1}
@@ -208,85 +70,137 @@ __device__ __forceinline__ void residual_point(const Geometry &g, const double2 
 }
 
 // ---------------------------------------------------------------------------------------------
-// forward: u -> X[p][m][n] = (S_p^{-1} (FFT_l alpha^{l/L} r))  (p bit-reversed frequency)
+// Time-transform tile kernels.  Tile: all l x all m x T consecutive n, element (l, m, t) at
+// sm[swz((l*M + m)*T + t)] (row index l*M + m; a "row" is T consecutive n of one (l, m)).
+//
+// fwd_kernel<M, RESID=true,  NODE=true>   1-D:  u -> X = S_p^{-1} FFT_l(alpha^{l/L} (w - C u))
+// fwd_kernel<M, RESID=false, NODE=false>  2-D:  X (= alpha^{l/L} r from residual2d_kernel) -> FFT_l in place
+// bwd_kernel<M, NODE=true>                1-D:  u += alpha^{-l/L}/L IFFT_p(G_p^{-1} S_p X2)
+// bwd_kernel<M, NODE=false>               2-D:  u += alpha^{-l/L}/L IFFT_p(X2)  (G^{-1}S applied in the row pass)
 
-template <int M>
-__global__ void __launch_bounds__(256) fwd_kernel(Geometry g, StaticTables st, AlphaTables at,
-                                                  const double2 *__restrict__ u, double2 *__restrict__ X,
-                                                  int T) {
-  extern __shared__ double2 sm[];  // [L][M][T]
+constexpr int kTileThreads = 256;
+constexpr int kTileMinBlocks = 3;
+
+template <int M, bool RESID, bool NODE>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    fwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ u,
+               double2 *__restrict__ X, int T) {
+  extern __shared__ double2 sm[];
   const int n0 = blockIdx.x * T;
   const int L = g.L;
   const size_t plane = (size_t)M * g.N;
-  const int items = L * T;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int t = it % T, l = it / T;
-    double2 r[M];
-    residual_point<M>(g, u, st.u0, l, n0 + t, r);
-    const double sc = __ldg(at.scale_fwd + l);
+  const int rows = L * M;
+  const int all = rows * T;
+  if (RESID) {
+    // (i) residual + alpha^{l/L} scale, one (l, t) per work item
+    const int items = L * T;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int t = it % T, l = it / T;
+      double2 r[M];
+      residual_point<M>(g, u, st.u0, l, n0 + t, r);
+      const double sc = __ldg(at.scale_fwd + l);
 #pragma unroll
-    for (int m = 0; m < M; ++m) sm[(l * M + m) * T + t] = cscale(r[m], sc);
+      for (int m = 0; m < M; ++m) sm[swz((l * M + m) * T + t)] = cscale(r[m], sc);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+      const int t = idx % T, row = idx / T;
+      cp_async16(sm + swz(idx), X + (size_t)row * g.N + n0 + t);
+    }
+    cp_async_wait_all();
   }
   __syncthreads();
+  // (ii) L-point DIF FFT along l for the M*T columns
   fft_dif(sm, M * T, 1, M * T, L, g.logL, st.twL);
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int t = it % T, p = it / T;
-    double2 v[M];
+  if (NODE) {
+    // (iii) node transform, one (p, m) row of T outputs per work item (row m of S_p^{-1} loaded once)
+    for (int it = threadIdx.x; it < rows; it += blockDim.x) {
+      const int m = it % M, p = it / M;
+      double2 srow[M];
 #pragma unroll
-    for (int j = 0; j < M; ++j) v[j] = sm[(p * M + j) * T + t];
-    const double2 *Si = at.Sinv + (size_t)p * M * M;
+      for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
+      double2 *dst = X + (size_t)p * plane + (size_t)m * g.N + n0;
+      for (int t = 0; t < T; ++t) {
+        double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int j = 0; j < M; ++j) acc = cfma(__ldg(Si + m * M + j), v[j], acc);
-      X[(size_t)p * plane + (size_t)m * g.N + n0 + t] = acc;
+        for (int j = 0; j < M; ++j) acc = cfma(srow[j], sm[swz((p * M + j) * T + t)], acc);
+        dst[t] = acc;
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+      const int t = idx % T, row = idx / T;
+      X[(size_t)row * g.N + n0 + t] = sm[swz(idx)];
     }
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// backward: X2 -> u += alpha^{-l/L}/L IFFT_p (G_p^{-1} S_p X2)
-
 __device__ __forceinline__ unsigned long long dbl_bits(double v) { return (unsigned long long)__double_as_longlong(v); }
 
-template <int M>
-__global__ void __launch_bounds__(256) bwd_kernel(Geometry g, StaticTables st, AlphaTables at,
-                                                  const double2 *__restrict__ X2, double2 *__restrict__ u,
-                                                  int T, unsigned long long *diff_slot) {
-  extern __shared__ double2 sm[];  // [L][M][T]
+template <int M, bool NODE>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
+               double2 *__restrict__ u, int T, unsigned long long *diff_slot) {
+  extern __shared__ double2 sm[];
   __shared__ double red[32];
   const int n0 = blockIdx.x * T;
   const int L = g.L;
-  const size_t plane = (size_t)M * g.N;
-  const int items = L * T;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int t = it % T, p = it / T;
-    double2 v[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) v[j] = __ldg(X2 + (size_t)p * plane + (size_t)j * g.N + n0 + t);
-    const double2 *SG = at.SG + (size_t)p * M * M;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int j = 0; j < M; ++j) acc = cfma(__ldg(SG + m * M + j), v[j], acc);
-      sm[(p * M + m) * T + t] = acc;
-    }
-  }
-  __syncthreads();
-  fft_dit_inv(sm, M * T, 1, M * T, L, g.logL, st.twL);
-  double dmax = 0.0;
-  const int all = L * M * T;
+  const int rows = L * M;
+  const int all = rows * T;
+  // async tile load X2[p][m][n0..n0+T) -> sm, and an L2 prefetch of the u tile for the update
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx % T;
-    const int m = (idx / T) % M;
-    const int l = idx / (M * T);
-    const double2 c = cscale(sm[idx], __ldg(at.scale_bwd + l));
-    double2 *up = u + (size_t)l * plane + (size_t)m * g.N + n0 + t;
-    double2 uo = *up;
-    *up = cadd(uo, c);
-    if (l == L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
+    const int t = idx % T, row = idx / T;
+    cp_async16(sm + swz(idx), X2 + (size_t)row * g.N + n0 + t);
+  }
+  for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
+  cp_async_wait_all();
+  __syncthreads();
+  if (NODE) {
+    // (v-a) y = G_p^{-1} S_p x2 in place, one (p, t) per work item
+    const int items = L * T;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int t = it % T, p = it / T;
+      double2 v[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) v[j] = sm[swz((p * M + j) * T + t)];
+      const double2 *SG = at.SG + (size_t)p * M * M;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) acc = cfma(__ldg(SG + m * M + j), v[j], acc);
+        sm[swz((p * M + m) * T + t)] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  // (v-b) inverse DIT FFT from bit-reversed p to natural l
+  fft_dit_inv(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  // (v-c) u += alpha^{-l/L}/L c, loads batched for memory-level parallelism
+  double dmax = 0.0;
+  constexpr int kB = 4;
+  for (int base = threadIdx.x; base < all; base += kB * blockDim.x) {
+    double2 uo[kB];
+    double sc[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int idx = base + k * blockDim.x;
+      if (idx < all) {
+        const int t = idx % T, row = idx / T;
+        uo[k] = u[(size_t)row * g.N + n0 + t];
+        sc[k] = __ldg(at.scale_bwd + row / M);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int idx = base + k * blockDim.x;
+      if (idx < all) {
+        const int t = idx % T, row = idx / T;
+        const double2 c = cscale(sm[swz(idx)], sc[k]);
+        u[(size_t)row * g.N + n0 + t] = cadd(uo[k], c);
+        if (row / M == L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
+      }
+    }
   }
   if (diff_slot) {
     for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -297,6 +211,143 @@ __global__ void __launch_bounds__(256) bwd_kernel(Geometry g, StaticTables st, A
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
       atomicMax(diff_slot, dbl_bits(v));  // non-negative doubles order like their bit patterns
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// 2-D time-transform tiles: one node m per CTA (the node transforms live in the row passes), so
+// the tile is all l x T consecutive n with T = 64 KB / (16 L) (T = 8 for L = 512: 128-byte rows).
+// Element (l, t) at sm[swz(l*T + t)]; CTA b covers node m = b / (N/T), n0 = (b % (N/T)) * T.
+
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tfft_fwd_kernel(Geometry g, StaticTables st, double2 *__restrict__ X, int T) {
+  extern __shared__ double2 sm[];
+  const int per = g.N / T;
+  const int m = blockIdx.x / per;
+  const int n0 = (blockIdx.x - m * per) * T;
+  const size_t lstride = (size_t)g.M * g.N;
+  double2 *base = X + (size_t)m * g.N + n0;
+  const int all = g.L * T;
+  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+    const int t = idx % T, l = idx / T;
+    cp_async16(sm + swz(idx), base + (size_t)l * lstride + t);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  fft_dif(sm, T, 1, T, g.L, g.logL, st.twL);
+  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+    const int t = idx % T, p = idx / T;
+    base[(size_t)p * lstride + t] = sm[swz(idx)];
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tfft_bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
+                    double2 *__restrict__ u, int T, unsigned long long *diff_slot) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  const int per = g.N / T;
+  const int m = blockIdx.x / per;
+  const int n0 = (blockIdx.x - m * per) * T;
+  const size_t lstride = (size_t)g.M * g.N;
+  const double2 *xb = X2 + (size_t)m * g.N + n0;
+  double2 *ub = u + (size_t)m * g.N + n0;
+  const int all = g.L * T;
+  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+    const int t = idx % T, p = idx / T;
+    cp_async16(sm + swz(idx), xb + (size_t)p * lstride + t);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  fft_dit_inv(sm, T, 1, T, g.L, g.logL, st.twL);
+  double dmax = 0.0;
+  constexpr int kB = 4;
+  for (int b0 = threadIdx.x; b0 < all; b0 += kB * blockDim.x) {
+    double2 uo[kB];
+    double sc[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int idx = b0 + k * blockDim.x;
+      if (idx < all) {
+        const int t = idx % T, l = idx / T;
+        uo[k] = ub[(size_t)l * lstride + t];
+        sc[k] = __ldg(at.scale_bwd + l);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int idx = b0 + k * blockDim.x;
+      if (idx < all) {
+        const int t = idx % T, l = idx / T;
+        const double2 c = cscale(sm[swz(idx)], sc[k]);
+        ub[(size_t)l * lstride + t] = cadd(uo[k], c);
+        if (l == g.L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
+      }
+    }
+  }
+  if (diff_slot) {
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+      atomicMax(diff_slot, dbl_bits(v));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// 2-D residual: X[l][m][n] = alpha^{l/L} (w - C u)[l][m][n] on spatial blocks BY x BX with a
+// one-point halo staged in shared memory (all M nodes of one l per CTA).
+
+template <int M>
+__global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
+                                                         const double2 *__restrict__ u,
+                                                         double2 *__restrict__ X, int BX, int BY) {
+  extern __shared__ double2 sm[];  // [M][BY+2][BX+2]
+  const int bxs = g.nx / BX, bys = g.ny / BY;
+  int b = blockIdx.x;
+  const int bx = b % bxs; b /= bxs;
+  const int by = b % bys;
+  const int l = b / bys;
+  const int x0 = bx * BX, y0 = by * BY;
+  const int W = BX + 2, H = BY + 2;
+  const size_t plane = (size_t)M * g.N;
+  const double2 *ul = u + (size_t)l * plane;
+  const int tot = M * W * H;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int xx = i % W, r = i / W;
+    const int yy = r % H, j = r / H;
+    const int x = (x0 + xx - 1) & (g.nx - 1), y = (y0 + yy - 1) & (g.ny - 1);
+    cp_async16(sm + i, ul + (size_t)j * g.N + ((size_t)y << g.lognx) + x);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
+  if (ty >= BY) return;
+  const int n = ((y0 + ty) << g.lognx) + x0 + tx;
+  double2 base = (l == 0) ? __ldg(st.u0 + n) : __ldg(u + (size_t)(l - 1) * plane + (size_t)(M - 1) * g.N + n);
+  double2 uc[M], Au[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double2 *s = sm + (j * H + ty + 1) * W + tx + 1;
+    const double2 c = s[0], a = s[-1], bb = s[1], d = s[-W], e = s[W];
+    uc[j] = c;
+    Au[j].x = g.c0 * c.x + g.cxm * a.x + g.cxp * bb.x + g.cym * d.x + g.cyp * e.x;
+    Au[j].y = g.c0 * c.y + g.cxm * a.y + g.cxp * bb.y + g.cym * d.y + g.cyp * e.y;
+  }
+  const double sc = __ldg(at.scale_fwd + l);
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    double2 acc = csub(base, uc[m]);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const double q = g.dTQ[m * M + j];
+      acc.x = fma(q, Au[j].x, acc.x);
+      acc.y = fma(q, Au[j].y, acc.y);
+    }
+    X[(size_t)l * plane + (size_t)m * g.N + n] = cscale(acc, sc);
   }
 }
 
@@ -414,24 +465,72 @@ __global__ void __launch_bounds__(kChunkThreads) pcr_chunk_kernel(const Geometry
 
 constexpr int kFftThreads = 256;
 
-template <bool INV>
-__global__ void __launch_bounds__(kFftThreads) fft2d_rows_kernel(const Geometry g, StaticTables st,
-                                                                 double2 *__restrict__ X, int rows_per_cta) {
-  extern __shared__ double2 sm[];  // [rows][nx]
+// Row pass with the node transform of frequency p fused in: one CTA per (p, group of YG rows y),
+// holding the M rows (p, m, y) of every y of the group.  Forward: x1 = S_p^{-1} x, then x-DIF FFT.
+// Inverse: x-DIT inverse FFT, then y = G_p^{-1} S_p x2.  All threads of a CTA share p, so the
+// M x M table loads are warp-uniform (broadcast).
+template <int M, bool INV>
+__global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
+    fft2d_rows_kernel(const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X, int YG) {
+  extern __shared__ double2 sm[];  // [YG][M][nx], swizzled
   const int nx = g.nx;
-  double2 *base = X + (size_t)blockIdx.x * rows_per_cta * nx;
-  const int items = rows_per_cta * nx;
-  for (int i = threadIdx.x; i < items; i += blockDim.x) sm[i] = base[i];
+  const int ygroups = g.ny / YG;
+  const int p = blockIdx.x / ygroups;
+  const int y0 = (blockIdx.x - p * ygroups) * YG;
+  const size_t plane = (size_t)M * g.N;
+  double2 *xp = X + (size_t)p * plane;
+  const int items = YG * M * nx;
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int x = i % nx, r = i / nx;
+    const int m = r % M, yy = r / M;
+    cp_async16(sm + swz(i), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << g.lognx) + x);
+  }
+  cp_async_wait_all();
   __syncthreads();
-  if (INV) fft_dit_inv(sm, rows_per_cta, nx, 1, nx, g.lognx, st.twx);
-  else fft_dif(sm, rows_per_cta, nx, 1, nx, g.lognx, st.twx);
-  for (int i = threadIdx.x; i < items; i += blockDim.x) base[i] = sm[i];
+  const double2 *tab = (INV ? at.SG : at.Sinv) + (size_t)p * M * M;
+  if (!INV) {
+    for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
+      const int x = c % nx, yy = c / nx;
+      double2 v[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) v[j] = sm[swz((yy * M + j) * nx + x)];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) acc = cfma(__ldg(tab + m * M + j), v[j], acc);
+        sm[swz((yy * M + m) * nx + x)] = acc;
+      }
+    }
+    __syncthreads();
+    fft_dif(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
+  } else {
+    fft_dit_inv(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
+    for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
+      const int x = c % nx, yy = c / nx;
+      double2 v[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) v[j] = sm[swz((yy * M + j) * nx + x)];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) acc = cfma(__ldg(tab + m * M + j), v[j], acc);
+        sm[swz((yy * M + m) * nx + x)] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int x = i % nx, r = i / nx;
+    const int m = r % M, yy = r / M;
+    xp[(size_t)m * g.N + ((size_t)(y0 + yy) << g.lognx) + x] = sm[swz(i)];
+  }
 }
 
-__global__ void __launch_bounds__(kFftThreads) fft2d_cols_kernel(const Geometry g, StaticTables st,
-                                                                 AlphaTables at, double2 *__restrict__ X,
-                                                                 int T) {
-  extern __shared__ double2 sm[];  // [ny][T]
+__global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
+    fft2d_cols_kernel(const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X, int T) {
+  extern __shared__ double2 sm[];  // [ny][T], swizzled
   const int nx = g.nx, ny = g.ny;
   const int groups = nx / T;
   const int line = blockIdx.x / groups;           // line = p*M + m
@@ -440,8 +539,9 @@ __global__ void __launch_bounds__(kFftThreads) fft2d_cols_kernel(const Geometry 
   const int items = ny * T;
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
     const int tt = i % T, y = i / T;
-    sm[i] = xl[(size_t)y * nx + kx0 + tt];
+    cp_async16(sm + swz(i), xl + (size_t)y * nx + kx0 + tt);
   }
+  cp_async_wait_all();
   __syncthreads();
   fft_dif(sm, T, 1, T, ny, g.logny, st.twy);
   const double2 s = __ldg(at.shift + line);
@@ -450,18 +550,18 @@ __global__ void __launch_bounds__(kFftThreads) fft2d_cols_kernel(const Geometry 
     const int tt = i % T, py = i / T;
     const int kx = brev(kx0 + tt, g.lognx), ky = brev(py, g.logny);
     const double2 lam = cadd(__ldg(st.lamx + kx), __ldg(st.lamy + ky));
-    // D = 1 - s * lam ;  value * inv_n / D
+    // value * inv_n / (1 - s lam)
     const double2 sl = cmul(s, lam);
     const double dr = 1.0 - sl.x, di = -sl.y;
     const double den = inv_n / (dr * dr + di * di);
-    const double2 v = sm[i];
-    sm[i] = make_double2((v.x * dr + v.y * di) * den, (v.y * dr - v.x * di) * den);
+    const double2 v = sm[swz(i)];
+    sm[swz(i)] = make_double2((v.x * dr + v.y * di) * den, (v.y * dr - v.x * di) * den);
   }
   __syncthreads();
   fft_dit_inv(sm, T, 1, T, ny, g.logny, st.twy);
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
     const int tt = i % T, y = i / T;
-    xl[(size_t)y * nx + kx0 + tt] = sm[i];
+    xl[(size_t)y * nx + kx0 + tt] = sm[swz(i)];
   }
 }
 
@@ -544,9 +644,13 @@ LaunchCfg choose_launch(const Geometry &g) {
   LaunchCfg lc{};
   // forward/backward tile: as many spatial points as fit ~100 KB (2 CTAs per SM), <= 16
   int T = 16;
-  while (T > 1 && fwd_smem_bytes(g, T) > 100 * 1024) T >>= 1;
+  while (T > 1 && fwd_smem_bytes(g, T) > 64 * 1024) T >>= 1;
   while (T > g.N) T >>= 1;
   lc.fwd_T = T;
+  int T2 = 32;
+  while (T2 > 1 && (size_t)g.L * T2 * sizeof(double2) > 64 * 1024) T2 >>= 1;
+  while (T2 > g.N) T2 >>= 1;
+  lc.tfft_T = T2;
   if (g.dim == 1) {
     if (g.N <= 4096) {
       lc.pcr_mode = 0;
@@ -569,15 +673,15 @@ LaunchCfg choose_launch(const Geometry &g) {
 }
 
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc) {
-  if (g.dim == 2) return 5;
+  if (g.dim == 2) return 6;
   return lc.pcr_mode == 0 ? 3 : 4;
 }
 
 const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i) {
   static const char *k1a[] = {"fwd_kernel", "pcr_classes_kernel", "bwd_kernel"};
   static const char *k1b[] = {"fwd_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
-  static const char *k2[] = {"fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
-                             "fft2d_rows_kernel<inv>", "bwd_kernel"};
+  static const char *k2[] = {"residual2d_kernel", "tfft_fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
+                             "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
   const int n = launches_per_iteration(g, lc);
   if (i < 0 || i >= n) return "";
   if (g.dim == 2) return k2[i];
@@ -601,24 +705,50 @@ static cudaError_t set_smem(const void *fn, size_t bytes) {
     default: { constexpr int MM = 8; __VA_ARGS__; } break; \
   }
 
+// 2-D residual block: BX x BY points, BX*BY <= 256
+static void residual_block(const Geometry &g, int &BX, int &BY) {
+  BX = g.nx < 32 ? g.nx : 32;
+  BY = 256 / BX;
+  if (BY > g.ny) BY = g.ny;
+}
+
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                            const AlphaTables &at, const Buffers &b, cudaStream_t s) {
   const int T = lc.fwd_T;
   const size_t smem = fwd_smem_bytes(g, T);
   const int grid = g.N / T;
   cudaError_t e = cudaSuccess;
-  PINT_DISPATCH_M(g.M, {
-    e = set_smem((const void *)fwd_kernel<MM>, smem);
-    if (e == cudaSuccess) fwd_kernel<MM><<<grid, 256, smem, s>>>(g, st, at, b.u, b.X, T);
-  });
-  rec(s);
+  if (g.dim == 1) {
+    PINT_DISPATCH_M(g.M, {
+      e = set_smem((const void *)fwd_kernel<MM, true, true>, smem);
+      if (e == cudaSuccess) fwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+    });
+    rec(s);
+  } else {
+    int BX, BY;
+    residual_block(g, BX, BY);
+    const size_t rs = (size_t)g.M * (BX + 2) * (BY + 2) * sizeof(double2);
+    const int rgrid = g.L * (g.nx / BX) * (g.ny / BY);
+    PINT_DISPATCH_M(g.M, {
+      e = set_smem((const void *)residual2d_kernel<MM>, rs);
+      if (e == cudaSuccess) residual2d_kernel<MM><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
+    });
+    rec(s);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int T2 = lc.tfft_T;
+    const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
+    e = set_smem((const void *)tfft_fwd_kernel, sm2);
+    if (e == cudaSuccess) tfft_fwd_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, b.X, T2);
+    rec(s);
+  }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                          const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out) {
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
   const int lines = g.L * g.M;
   if (g.dim == 1) {
     if (lc.pcr_mode == 0) {
@@ -628,8 +758,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       rec(s);
       *out = b.X;
     } else {
-      const int R = lc.pcr_R, T = lc.pcr_T, jA = 0;
-      (void)jA;
+      const int R = lc.pcr_R, T = lc.pcr_T;
       const int jOff = __builtin_ctz((unsigned)R);
       const int nq = g.N / R;
       size_t smem = (size_t)nq * T * sizeof(double2);
@@ -645,16 +774,20 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       *out = b.Y;
     }
   } else {
-    // rows: 4096 elements per CTA
-    int rpc = 4096 / g.nx;
-    if (rpc < 1) rpc = 1;
-    const long long rows = (long long)lines * g.ny;
-    while (rpc > 1 && rows % rpc) rpc >>= 1;
-    size_t smem = (size_t)rpc * g.nx * sizeof(double2);
-    if ((e = set_smem((const void *)fft2d_rows_kernel<false>, smem)) != cudaSuccess) return e;
-    if ((e = set_smem((const void *)fft2d_rows_kernel<true>, smem)) != cudaSuccess) return e;
-    fft2d_rows_kernel<false><<<(unsigned)(rows / rpc), kFftThreads, smem, s>>>(g, st, b.X, rpc);
+    // row passes: one frequency p and YG rows y per CTA (M*YG*nx <= 4096 elements = 64 KB)
+    int YG = 4096 / (g.M * g.nx);
+    if (YG < 1) YG = 1;
+    if (YG > g.ny) YG = g.ny;
+    while (g.ny % YG) YG >>= 1;
+    const size_t smem = (size_t)YG * g.M * g.nx * sizeof(double2);
+    const unsigned rgrid = (unsigned)(g.L * (g.ny / YG));
+    PINT_DISPATCH_M(g.M, {
+      e = set_smem((const void *)fft2d_rows_kernel<MM, false>, smem);
+      if (e == cudaSuccess) e = set_smem((const void *)fft2d_rows_kernel<MM, true>, smem);
+      if (e == cudaSuccess) fft2d_rows_kernel<MM, false><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+    });
     rec(s);
+    if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     int T = 4096 / g.ny;
     if (T < 1) T = 1;
@@ -665,7 +798,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     fft2d_cols_kernel<<<lines * (g.nx / T), kFftThreads, smc, s>>>(g, st, at, b.X, T);
     rec(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    fft2d_rows_kernel<true><<<(unsigned)(rows / rpc), kFftThreads, smem, s>>>(g, st, b.X, rpc);
+    PINT_DISPATCH_M(g.M, { fft2d_rows_kernel<MM, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG); });
     rec(s);
     *out = b.X;
   }
@@ -679,11 +812,20 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   const size_t smem = fwd_smem_bytes(g, T);
   const int grid = g.N / T;
   cudaError_t e = cudaSuccess;
-  PINT_DISPATCH_M(g.M, {
-    e = set_smem((const void *)bwd_kernel<MM>, smem);
+  if (g.dim == 1) {
+    PINT_DISPATCH_M(g.M, {
+      e = set_smem((const void *)bwd_kernel<MM, true>, smem);
+      if (e == cudaSuccess)
+        bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+    });
+  } else {
+    const int T2 = lc.tfft_T;
+    const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
+    e = set_smem((const void *)tfft_bwd_kernel, sm2);
     if (e == cudaSuccess)
-      bwd_kernel<MM><<<grid, 256, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
-  });
+      tfft_bwd_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
+                                                                    (unsigned long long *)diff_slot);
+  }
   rec(s);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
