@@ -71,7 +71,7 @@ __device__ __forceinline__ void residual_point(const Geometry &g, const double2 
 
 // ---------------------------------------------------------------------------------------------
 // Time-transform tile kernels.  Tile: all l x all m x T consecutive n, element (l, m, t) at
-// sm[swz((l*M + m)*T + t)] (row index l*M + m; a "row" is T consecutive n of one (l, m)).
+// sm[sidx<false>((l*M + m)*T + t)] (row index l*M + m; a "row" is T consecutive n of one (l, m)).
 //
 // fwd_kernel<M, RESID=true,  NODE=true>   1-D:  u -> X = S_p^{-1} FFT_l(alpha^{l/L} (w - C u))
 // fwd_kernel<M, RESID=false, NODE=false>  2-D:  X (= alpha^{l/L} r from residual2d_kernel) -> FFT_l in place
@@ -79,13 +79,15 @@ __device__ __forceinline__ void residual_point(const Geometry &g, const double2 
 // bwd_kernel<M, NODE=false>               2-D:  u += alpha^{-l/L}/L IFFT_p(X2)  (G^{-1}S applied in the row pass)
 
 constexpr int kTileThreads = 256;
-constexpr int kTileMinBlocks = 3;
+constexpr int kTileMinBlocks = 3;   // time tiles: radix <= 8, 80 registers
+constexpr int kSpaceMinBlocks = 2;  // spatial FFT passes: radix <= 16, 128 registers
 
 template <int M, bool RESID, bool NODE>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     fwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ u,
                double2 *__restrict__ X, int T) {
   extern __shared__ double2 sm[];
+  const int lT = 31 - __clz(T);
   const int n0 = blockIdx.x * T;
   const int L = g.L;
   const size_t plane = (size_t)M * g.N;
@@ -95,23 +97,23 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     // (i) residual + alpha^{l/L} scale, one (l, t) per work item
     const int items = L * T;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int t = it % T, l = it / T;
+      const int t = it & (T - 1), l = it >> lT;
       double2 r[M];
       residual_point<M>(g, u, st.u0, l, n0 + t, r);
       const double sc = __ldg(at.scale_fwd + l);
 #pragma unroll
-      for (int m = 0; m < M; ++m) sm[swz((l * M + m) * T + t)] = cscale(r[m], sc);
+      for (int m = 0; m < M; ++m) sm[sidx<false>((l * M + m) * T + t)] = cscale(r[m], sc);
     }
   } else {
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-      const int t = idx % T, row = idx / T;
-      cp_async16(sm + swz(idx), X + (size_t)row * g.N + n0 + t);
+      const int t = idx & (T - 1), row = idx >> lT;
+      cp_async16(sm + sidx<false>(idx), X + (size_t)row * g.N + n0 + t);
     }
     cp_async_wait_all();
   }
   __syncthreads();
   // (ii) L-point DIF FFT along l for the M*T columns
-  fft_dif(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  fft_dif<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);
   if (NODE) {
     // (iii) node transform, one (p, m) row of T outputs per work item (row m of S_p^{-1} loaded once)
     for (int it = threadIdx.x; it < rows; it += blockDim.x) {
@@ -123,14 +125,14 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       for (int t = 0; t < T; ++t) {
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < M; ++j) acc = cfma(srow[j], sm[swz((p * M + j) * T + t)], acc);
+        for (int j = 0; j < M; ++j) acc = cfma(srow[j], sm[sidx<false>((p * M + j) * T + t)], acc);
         dst[t] = acc;
       }
     }
   } else {
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-      const int t = idx % T, row = idx / T;
-      X[(size_t)row * g.N + n0 + t] = sm[swz(idx)];
+      const int t = idx & (T - 1), row = idx >> lT;
+      X[(size_t)row * g.N + n0 + t] = sm[sidx<false>(idx)];
     }
   }
 }
@@ -143,14 +145,15 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
                double2 *__restrict__ u, int T, unsigned long long *diff_slot) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
+  const int lT = 31 - __clz(T);
   const int n0 = blockIdx.x * T;
   const int L = g.L;
   const int rows = L * M;
   const int all = rows * T;
   // async tile load X2[p][m][n0..n0+T) -> sm, and an L2 prefetch of the u tile for the update
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx % T, row = idx / T;
-    cp_async16(sm + swz(idx), X2 + (size_t)row * g.N + n0 + t);
+    const int t = idx & (T - 1), row = idx >> lT;
+    cp_async16(sm + sidx<false>(idx), X2 + (size_t)row * g.N + n0 + t);
   }
   for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
   cp_async_wait_all();
@@ -159,23 +162,23 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     // (v-a) y = G_p^{-1} S_p x2 in place, one (p, t) per work item
     const int items = L * T;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int t = it % T, p = it / T;
+      const int t = it & (T - 1), p = it >> lT;
       double2 v[M];
 #pragma unroll
-      for (int j = 0; j < M; ++j) v[j] = sm[swz((p * M + j) * T + t)];
+      for (int j = 0; j < M; ++j) v[j] = sm[sidx<false>((p * M + j) * T + t)];
       const double2 *SG = at.SG + (size_t)p * M * M;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int j = 0; j < M; ++j) acc = cfma(__ldg(SG + m * M + j), v[j], acc);
-        sm[swz((p * M + m) * T + t)] = acc;
+        sm[sidx<false>((p * M + m) * T + t)] = acc;
       }
     }
     __syncthreads();
   }
   // (v-b) inverse DIT FFT from bit-reversed p to natural l
-  fft_dit_inv(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  fft_dit_inv<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);
   // (v-c) u += alpha^{-l/L}/L c, loads batched for memory-level parallelism
   double dmax = 0.0;
   constexpr int kB = 4;
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     for (int k = 0; k < kB; ++k) {
       const int idx = base + k * blockDim.x;
       if (idx < all) {
-        const int t = idx % T, row = idx / T;
+        const int t = idx & (T - 1), row = idx >> lT;
         uo[k] = u[(size_t)row * g.N + n0 + t];
         sc[k] = __ldg(at.scale_bwd + row / M);
       }
@@ -195,8 +198,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     for (int k = 0; k < kB; ++k) {
       const int idx = base + k * blockDim.x;
       if (idx < all) {
-        const int t = idx % T, row = idx / T;
-        const double2 c = cscale(sm[swz(idx)], sc[k]);
+        const int t = idx & (T - 1), row = idx >> lT;
+        const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
         u[(size_t)row * g.N + n0 + t] = cadd(uo[k], c);
         if (row / M == L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
       }
@@ -217,11 +220,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 // ---------------------------------------------------------------------------------------------
 // 2-D time-transform tiles: one node m per CTA (the node transforms live in the row passes), so
 // the tile is all l x T consecutive n with T = 64 KB / (16 L) (T = 8 for L = 512: 128-byte rows).
-// Element (l, t) at sm[swz(l*T + t)]; CTA b covers node m = b / (N/T), n0 = (b % (N/T)) * T.
+// Element (l, t) at sm[sidx<false>(l*T + t)]; CTA b covers node m = b / (N/T), n0 = (b % (N/T)) * T.
 
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tfft_fwd_kernel(Geometry g, StaticTables st, double2 *__restrict__ X, int T) {
   extern __shared__ double2 sm[];
+  const int lT = 31 - __clz(T);
   const int per = g.N / T;
   const int m = blockIdx.x / per;
   const int n0 = (blockIdx.x - m * per) * T;
@@ -229,15 +233,15 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   double2 *base = X + (size_t)m * g.N + n0;
   const int all = g.L * T;
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx % T, l = idx / T;
-    cp_async16(sm + swz(idx), base + (size_t)l * lstride + t);
+    const int t = idx & (T - 1), l = idx >> lT;
+    cp_async16(sm + sidx<false>(idx), base + (size_t)l * lstride + t);
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_dif(sm, T, 1, T, g.L, g.logL, st.twL);
+  fft_dif<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx % T, p = idx / T;
-    base[(size_t)p * lstride + t] = sm[swz(idx)];
+    const int t = idx & (T - 1), p = idx >> lT;
+    base[(size_t)p * lstride + t] = sm[sidx<false>(idx)];
   }
 }
 
@@ -246,6 +250,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
                     double2 *__restrict__ u, int T, unsigned long long *diff_slot) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
+  const int lT = 31 - __clz(T);
   const int per = g.N / T;
   const int m = blockIdx.x / per;
   const int n0 = (blockIdx.x - m * per) * T;
@@ -254,12 +259,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   double2 *ub = u + (size_t)m * g.N + n0;
   const int all = g.L * T;
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx % T, p = idx / T;
-    cp_async16(sm + swz(idx), xb + (size_t)p * lstride + t);
+    const int t = idx & (T - 1), p = idx >> lT;
+    cp_async16(sm + sidx<false>(idx), xb + (size_t)p * lstride + t);
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_dit_inv(sm, T, 1, T, g.L, g.logL, st.twL);
+  fft_dit_inv<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
   double dmax = 0.0;
   constexpr int kB = 4;
   for (int b0 = threadIdx.x; b0 < all; b0 += kB * blockDim.x) {
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     for (int k = 0; k < kB; ++k) {
       const int idx = b0 + k * blockDim.x;
       if (idx < all) {
-        const int t = idx % T, l = idx / T;
+        const int t = idx & (T - 1), l = idx >> lT;
         uo[k] = ub[(size_t)l * lstride + t];
         sc[k] = __ldg(at.scale_bwd + l);
       }
@@ -278,8 +283,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     for (int k = 0; k < kB; ++k) {
       const int idx = b0 + k * blockDim.x;
       if (idx < all) {
-        const int t = idx % T, l = idx / T;
-        const double2 c = cscale(sm[swz(idx)], sc[k]);
+        const int t = idx & (T - 1), l = idx >> lT;
+        const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
         ub[(size_t)l * lstride + t] = cadd(uo[k], c);
         if (l == g.L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
       }
@@ -316,9 +321,10 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   const size_t plane = (size_t)M * g.N;
   const double2 *ul = u + (size_t)l * plane;
   const int tot = M * W * H;
+  const FastDiv fW((unsigned)W), fH((unsigned)H);
   for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-    const int xx = i % W, r = i / W;
-    const int yy = r % H, j = r / H;
+    const int r = (int)fW.div((unsigned)i), xx = i - r * W;
+    const int j = (int)fH.div((unsigned)r), yy = r - j * H;
     const int x = (x0 + xx - 1) & (g.nx - 1), y = (y0 + yy - 1) & (g.ny - 1);
     cp_async16(sm + i, ul + (size_t)j * g.N + ((size_t)y << g.lognx) + x);
   }
@@ -369,6 +375,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
                                                                   double2 *__restrict__ X, int R, int T,
                                                                   int j_off) {
   extern __shared__ double2 sm[];  // [nq][T]
+  const int lT = 31 - __clz(T);
   const int N = g.N;
   const int nq = N / R;
   const int lognq = g.logN - j_off;
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
   double2 *xl = X + (size_t)line * N;
   const int items = nq * T;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int tt = it % T, q = it / T;
+    const int tt = it & (T - 1), q = it >> lT;
     sm[it] = xl[(size_t)q * R + r0 + tt];
   }
   __syncthreads();
@@ -393,7 +400,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
     for (int k = 0; k < kPcrIPT; ++k) {
       const int it = threadIdx.x + k * kPcrThreads;
       if (it < items) {
-        const int tt = it % T, q = it / T;
+        const int tt = it & (T - 1), q = it >> lT;
         const double2 yc = sm[it];
         const double2 yp = sm[((q + h) & (nq - 1)) * T + tt];
         double2 v = csub(yc, cmul(pair ? pj : qj, yp));
@@ -411,7 +418,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
   }
   const double2 ie = __ldg(at.inv_e + line);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int tt = it % T, q = it / T;
+    const int tt = it & (T - 1), q = it >> lT;
     xl[(size_t)q * R + r0 + tt] = cmul(sm[it], ie);
   }
 }
@@ -470,7 +477,7 @@ constexpr int kFftThreads = 256;
 // Inverse: x-DIT inverse FFT, then y = G_p^{-1} S_p x2.  All threads of a CTA share p, so the
 // M x M table loads are warp-uniform (broadcast).
 template <int M, bool INV>
-__global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
+__global__ void __launch_bounds__(kFftThreads, kSpaceMinBlocks)
     fft2d_rows_kernel(const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X, int YG) {
   extern __shared__ double2 sm[];  // [YG][M][nx], swizzled
   const int nx = g.nx;
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
   double2 *xp = X + (size_t)p * plane;
   const int items = YG * M * nx;
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
-    const int x = i % nx, r = i / nx;
+    const int x = i & (nx - 1), r = i >> g.lognx;
     const int m = r % M, yy = r / M;
     cp_async16(sm + swz(i), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << g.lognx) + x);
   }
@@ -490,7 +497,7 @@ __global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
   const double2 *tab = (INV ? at.SG : at.Sinv) + (size_t)p * M * M;
   if (!INV) {
     for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
-      const int x = c % nx, yy = c / nx;
+      const int x = c & (nx - 1), yy = c >> g.lognx;
       double2 v[M];
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = sm[swz((yy * M + j) * nx + x)];
@@ -503,11 +510,11 @@ __global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
       }
     }
     __syncthreads();
-    fft_dif(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
+    fft_dif<4, true>(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
   } else {
-    fft_dit_inv(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
+    fft_dit_inv<4, true>(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
     for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
-      const int x = c % nx, yy = c / nx;
+      const int x = c & (nx - 1), yy = c >> g.lognx;
       double2 v[M];
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = sm[swz((yy * M + j) * nx + x)];
@@ -522,15 +529,18 @@ __global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
     __syncthreads();
   }
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
-    const int x = i % nx, r = i / nx;
+    const int x = i & (nx - 1), r = i >> g.lognx;
     const int m = r % M, yy = r / M;
     xp[(size_t)m * g.N + ((size_t)(y0 + yy) << g.lognx) + x] = sm[swz(i)];
   }
 }
 
-__global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
+constexpr int kColThreads = 512;
+
+__global__ void __launch_bounds__(kColThreads, 1)
     fft2d_cols_kernel(const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X, int T) {
-  extern __shared__ double2 sm[];  // [ny][T], swizzled
+  extern __shared__ double2 sm[];  // [ny][T] (T >= 8: contiguous quarter-warps, no swizzle)
+  const int lT = 31 - __clz(T);
   const int nx = g.nx, ny = g.ny;
   const int groups = nx / T;
   const int line = blockIdx.x / groups;           // line = p*M + m
@@ -538,30 +548,34 @@ __global__ void __launch_bounds__(kFftThreads, kTileMinBlocks)
   double2 *xl = X + (size_t)line * g.N;
   const int items = ny * T;
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
-    const int tt = i % T, y = i / T;
-    cp_async16(sm + swz(i), xl + (size_t)y * nx + kx0 + tt);
+    const int tt = i & (T - 1), y = i >> lT;
+    cp_async16(sm + sidx<false>(i), xl + (size_t)y * nx + kx0 + tt);
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_dif(sm, T, 1, T, ny, g.logny, st.twy);
+  const int blast = fft_dif_but_last<4, false>(sm, T, 1, T, g.logny, st.twy);
   const double2 s = __ldg(at.shift + line);
   const double inv_n = 1.0 / ((double)nx * (double)ny);
-  for (int i = threadIdx.x; i < items; i += blockDim.x) {
-    const int tt = i % T, py = i / T;
+  // x2 = x1 / (1 - s (lambda_x + lambda_y)) / (nx ny), applied in the fused middle groups
+  auto divide = [&](int tt, int py, double2 v) -> double2 {
     const int kx = brev(kx0 + tt, g.lognx), ky = brev(py, g.logny);
     const double2 lam = cadd(__ldg(st.lamx + kx), __ldg(st.lamy + ky));
-    // value * inv_n / (1 - s lam)
     const double2 sl = cmul(s, lam);
     const double dr = 1.0 - sl.x, di = -sl.y;
-    const double den = inv_n / (dr * dr + di * di);
-    const double2 v = sm[swz(i)];
-    sm[swz(i)] = make_double2((v.x * dr + v.y * di) * den, (v.y * dr - v.x * di) * den);
-  }
-  __syncthreads();
-  fft_dit_inv(sm, T, 1, T, ny, g.logny, st.twy);
+    const double q = dr * dr + di * di;             // > 0 (Re s > 0, Re lambda <= 0)
+    double rq = __drcp_rn(q);                        // reciprocal + one Newton step
+    rq = fma(rq, fma(-q, rq, 1.0), rq);
+    const double den = inv_n * rq;
+    return make_double2((v.x * dr + v.y * di) * den, (v.y * dr - v.x * di) * den);
+  };
+  if (blast == 1) fused_middle<1, false>(sm, T, 1, T, g.logny, divide);
+  else if (blast == 2) fused_middle<2, false>(sm, T, 1, T, g.logny, divide);
+  else if (blast == 3) fused_middle<3, false>(sm, T, 1, T, g.logny, divide);
+  else fused_middle<4, false>(sm, T, 1, T, g.logny, divide);
+  fft_dit_inv_from<4, false>(sm, T, 1, T, g.logny, st.twy, 1);
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
-    const int tt = i % T, y = i / T;
-    xl[(size_t)y * nx + kx0 + tt] = sm[swz(i)];
+    const int tt = i & (T - 1), y = i >> lT;
+    xl[(size_t)y * nx + kx0 + tt] = sm[sidx<false>(i)];
   }
 }
 
@@ -789,13 +803,13 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     rec(s);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    int T = 4096 / g.ny;
+    int T = 8192 / g.ny;                 // 128 KB tile, one 512-thread CTA per SM
     if (T < 1) T = 1;
     if (T > g.nx) T = g.nx;
     if (T > 16) T = 16;
     size_t smc = (size_t)g.ny * T * sizeof(double2);
     if ((e = set_smem((const void *)fft2d_cols_kernel, smc)) != cudaSuccess) return e;
-    fft2d_cols_kernel<<<lines * (g.nx / T), kFftThreads, smc, s>>>(g, st, at, b.X, T);
+    fft2d_cols_kernel<<<lines * (g.nx / T), kColThreads, smc, s>>>(g, st, at, b.X, T);
     rec(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     PINT_DISPATCH_M(g.M, { fft2d_rows_kernel<MM, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG); });
