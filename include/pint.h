@@ -77,9 +77,17 @@ typedef struct {
   int32_t M;       /* Radau IIA nodes, 1 <= M <= PINT_MAX_M                                   */
 } pint_problem;
 
+/* Time sharding (north star "partitioned by time steps"): with nranks = P > 1 rank
+ * g owns the global steps l = g + P j, j < L/P (cyclic distribution).  The time DFT becomes a
+ * four-step FFT: local L/P-point FFT + twiddle, one all-to-all, P-point DFT across ranks (and the
+ * same backwards); the H-term of the residual needs the last node of step l-1, i.e. a ring halo
+ * from rank g-1.  Requires (L/P) % P == 0 and M*P <= 32. */
 typedef struct {
-  int32_t rank, nranks;          /* nranks == 1 in this build (multi-GPU: DESIGN.md §7)       */
-  const void *nccl_unique_id;    /* reserved (NULL)                                            */
+  int32_t rank, nranks;          /* nranks in {1, 2, 4, 8}, 0 <= rank < nranks                  */
+  const void *nccl_unique_id;    /* nranks > 1: 128-byte ncclUniqueId (pint_nccl_unique_id on rank
+                                    0, broadcast by the caller) -> NCCL over NVLink; NULL -> a
+                                    "virtual rank" of a single-process loopback group driven by
+                                    pint_group_iterate (all ranks on one device; tests)          */
   int32_t device;                /* CUDA device ordinal                                        */
   void *stream;                  /* cudaStream_t on which all work is enqueued (NULL = legacy) */
 } pint_dist;
@@ -89,8 +97,9 @@ typedef struct {
  * per-alpha factor tables for up to PINT_MAX_SCHEDULE alphas and reduction scratch. */
 size_t pint_workspace_bytes(const pint_problem *p, const pint_dist *d);
 
-/* Creates a context.  u_dev: caller-owned device buffer of L*M*N complex128 (16-byte aligned),
- * set here to u^(0) = u0 replicated over all (l, m).  work_dev/work_bytes: caller-owned
+/* Creates a context.  u_dev: caller-owned device buffer of (L/nranks)*M*N complex128 (16-byte
+ * aligned; local steps j hold global steps rank + nranks*j), set here to u^(0) = u0 replicated
+ * over all (l, m).  work_dev/work_bytes: caller-owned
  * device scratch (256-byte aligned, >= pint_workspace_bytes).  u0_host: 2N doubles (re, im),
  * copied.  forcing_host must be NULL (b == 0; forcing is not supported in this build).
  * Errors: PINT_ERR_INVALID (sizes, alignment, NULL), PINT_ERR_CUDA. */
@@ -118,21 +127,38 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
  * P:421) and the call synchronises the stream.  PINT_ERR_SCHEDULE if the schedule would run out. */
 pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf);
 
-/* ||w - C u||_2 and ||w - C u||_inf of the current iterate (synchronises). PINT_ERR_NUMERIC if
- * non-finite. */
+/* ||w - C u||_2 and ||w - C u||_inf of the current (global) iterate (synchronises; with NCCL ranks
+ * it exchanges the halo and all-reduces).  PINT_ERR_NUMERIC if non-finite. */
 pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf);
 
 /* D2H of the whole local iterate (2*L*M*N doubles) — parity checks (synchronises). */
 pint_status pint_get_iterate(pint_ctx *c, double *u_host);
 
-/* D2H of the last node of the last step, u_{L-1, M-1, :} = the solution at T (2N doubles). */
+/* D2H of the last node of the last LOCAL step (2N doubles); on rank nranks-1 (and with one rank)
+ * that is u_{L-1, M-1, :}, the solution at T. */
 pint_status pint_get_final_value(pint_ctx *c, double *u_host);
 
 /* Replaces u0 (H2D copy of 2N doubles, changes w) and, if reset_iterate != 0, resets the iterate
  * to u0 replicated.  Used by the end-to-end benchmark. */
 pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t reset_iterate);
 
-/* Frees context-owned host state; never caller buffers. */
+/* nranks > 1: a fresh 128-byte NCCL unique id for pint_dist.nccl_unique_id (call on rank 0 and
+ * broadcast).  PINT_ERR_NCCL on failure. */
+pint_status pint_nccl_unique_id(void *out128);
+
+/* The global steps the local iterate holds: first, first + stride, ..., count of them. */
+pint_status pint_local_steps(pint_ctx *c, int32_t *first, int32_t *stride, int32_t *count);
+
+/* Single-process loopback group: ctxs[r] is rank r of a P-rank group created with
+ * nccl_unique_id == NULL on ONE device and ONE stream.  Runs n_iter iterations of the sharded
+ * algorithm phase by phase, moving the halo / all-to-all chunks with device-to-device copies
+ * (no kernel ever waits on another rank).  last_step_diff_inf as in pint_iterate (nullable). */
+pint_status pint_group_iterate(pint_ctx *const *ctxs, int32_t P, int32_t n_iter, double *last_step_diff_inf);
+
+/* Global residual norms of a loopback group. */
+pint_status pint_group_residual_norm(pint_ctx *const *ctxs, int32_t P, double *l2, double *linf);
+
+/* Frees context-owned host state and the NCCL communicator; never caller buffers. */
 pint_status pint_destroy(pint_ctx *c);
 
 /* Thread-local message of the last non-OK status. */

@@ -11,6 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpint.so")
 SOURCES = ["kernels.cu", "pint_abi.cpp", "host_numerics.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+LIBS = ["-lnccl"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
@@ -21,7 +22,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                    os.path.join(ROOT, "include", "pint.h")]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
-    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB, *srcs, "-I", os.path.join(ROOT, "include")]
+    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB, *srcs, "-I", os.path.join(ROOT, "include"), *LIBS]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

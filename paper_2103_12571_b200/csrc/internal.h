@@ -28,12 +28,24 @@ struct Geometry {
 };
 
 struct StaticTables {
-  const double2 *twL;         // [L]  e^{-2 pi i q / L}
+  const double2 *twL;         // [L]  e^{-2 pi i q / L}   (L = local step count L/P)
   const double2 *twx;         // [nx] e^{-2 pi i q / nx}
   const double2 *twy;         // [ny] e^{-2 pi i q / ny}
   const double2 *lamx;        // [nx] per-axis symbol, natural kx
   const double2 *lamy;        // [ny]
   const double2 *u0;          // [N]
+  // H-term source of the residual: the last node of the previous global step of local step l is
+  // prev_base[(l - prev_shift) * prev_stride + n]; l - prev_shift < 0 means global step 0 (w = u0).
+  //   1 rank:  prev_base = u + (M-1) N, prev_stride = M N, prev_shift = 1
+  //   P ranks: prev_base = received ring halo [L/P][N], prev_stride = N, prev_shift = (rank == 0)
+  const double2 *prev_base;
+  long long prev_stride;
+  int prev_shift;
+  // four-step time FFT across P ranks (P > 1 only, else null): twr[p] = e^{-2 pi i rank kappa / L},
+  // kappa = bitrev_{L/P}(p); twP[q] = e^{-2 pi i q / P}
+  const double2 *twr;
+  const double2 *twP;
+  int P, rank;
 };
 
 struct Buffers {
@@ -59,6 +71,9 @@ size_t fwd_smem_bytes(const Geometry &g, int T);
 
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                            const AlphaTables &at, const Buffers &b, cudaStream_t s);
+// spatial solves on the lines of `in` (which must be b.X): result in *out (b.X or b.Y).
+// node = true applies S^{-1} / G^{-1}S inside the solve passes where the design puts them
+// (2-D row passes); with P > 1 they live in launch_xdft instead.
 cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                          const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out);
 cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
@@ -68,6 +83,15 @@ cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, cons
                                  double *out2, cudaStream_t s);
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,
                                 cudaStream_t s);
+cudaError_t launch_square_first(const double *in, double *out, cudaStream_t s);
+cudaError_t launch_sqrt_into(const double *in, double *out, cudaStream_t s);
+// P > 1: pack the last-node planes u[l][M-1][:] of all local steps into hsend[l][:]
+cudaError_t launch_halo_pack(const Geometry &g, const Buffers &b, double2 *hsend, cudaStream_t s);
+// P > 1: cross-rank P-point DFT (+ S^{-1}) from the all-to-all receive buffer Yin[src][pl][m][n]
+// into slot order Xout[q*(L/P^2... see kernels.cu)], and its inverse (G^{-1} S, inverse DFT) into
+// send chunks by destination.
+cudaError_t launch_xdft(const Geometry &g, const StaticTables &st, const AlphaTables &at,
+                        const double2 *in, double2 *out, bool inverse, cudaStream_t s);
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc);
 const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i);
 

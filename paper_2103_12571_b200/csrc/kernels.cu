@@ -25,10 +25,15 @@ namespace pint {
 // residual of one (l, n) for all nodes: r_m = w_m - u_m + dT sum_j Q_mj (A u_j) + u_{l-1, M-1}
 // (C = I_L (x) C_coll + E (x) H; w_0 = u0 replicated, w_{l>0} = 0 since b == 0)
 
+// H-term source (last node of the previous global step) of local step l at point n
+__device__ __forceinline__ double2 prev_value(const StaticTables &st, int l, int n) {
+  const int jj = l - st.prev_shift;
+  return jj < 0 ? __ldg(st.u0 + n) : __ldg(st.prev_base + (long long)jj * st.prev_stride + n);
+}
+
 template <int M>
-__device__ __forceinline__ void residual_point(const Geometry &g, const double2 *__restrict__ u,
-                                               const double2 *__restrict__ u0, int l, int n,
-                                               double2 r[M]) {
+__device__ __forceinline__ void residual_point(const Geometry &g, const StaticTables &st,
+                                               const double2 *__restrict__ u, int l, int n, double2 r[M]) {
   const size_t plane = (size_t)M * g.N;
   const double2 *ul = u + (size_t)l * plane;
   const int x = n & (g.nx - 1);
@@ -53,9 +58,7 @@ __device__ __forceinline__ void residual_point(const Geometry &g, const double2 
     }
     Au[j] = s;
   }
-  double2 base = make_double2(0.0, 0.0);
-  if (l == 0) base = __ldg(u0 + n);
-  else base = __ldg(u + (size_t)(l - 1) * plane + (size_t)(M - 1) * g.N + n);
+  const double2 base = prev_value(st, l, n);   // w (global l = 0) or the H-term u_{l-1, M-1}
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     double2 acc = csub(base, uc[m]);
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
       const int t = it & (T - 1), l = it >> lT;
       double2 r[M];
-      residual_point<M>(g, u, st.u0, l, n0 + t, r);
+      residual_point<M>(g, st, u, l, n0 + t, r);
       const double sc = __ldg(at.scale_fwd + l);
 #pragma unroll
       for (int m = 0; m < M; ++m) sm[sidx<false>((l * M + m) * T + t)] = cscale(r[m], sc);
@@ -130,9 +133,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       }
     }
   } else {
+    // (P > 1: the node transform runs after the cross-rank DFT) four-step twiddle e^{-2 pi i rank kappa/L}
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
       const int t = idx & (T - 1), row = idx >> lT;
-      X[(size_t)row * g.N + n0 + t] = sm[sidx<false>(idx)];
+      double2 v = sm[sidx<false>(idx)];
+      if (st.twr) v = cmul(v, __ldg(st.twr + row / M));
+      X[(size_t)row * g.N + n0 + t] = v;
     }
   }
 }
@@ -158,6 +164,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
   cp_async_wait_all();
   __syncthreads();
+  if (!NODE && st.twr) {  // P > 1: inverse four-step twiddle e^{+2 pi i rank kappa/L}
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x)
+      sm[sidx<false>(idx)] = cmulc(sm[sidx<false>(idx)], __ldg(st.twr + (idx >> lT) / M));
+    __syncthreads();
+  }
   if (NODE) {
     // (v-a) y = G_p^{-1} S_p x2 in place, one (p, t) per work item
     const int items = L * T;
@@ -241,7 +252,9 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   fft_dif<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
     const int t = idx & (T - 1), p = idx >> lT;
-    base[(size_t)p * lstride + t] = sm[sidx<false>(idx)];
+    double2 v = sm[sidx<false>(idx)];
+    if (st.twr) v = cmul(v, __ldg(st.twr + p));   // P > 1: four-step twiddle
+    base[(size_t)p * lstride + t] = v;
   }
 }
 
@@ -264,6 +277,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   }
   cp_async_wait_all();
   __syncthreads();
+  if (st.twr) {  // P > 1: inverse four-step twiddle
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x)
+      sm[sidx<false>(idx)] = cmulc(sm[sidx<false>(idx)], __ldg(st.twr + (idx >> lT)));
+    __syncthreads();
+  }
   fft_dit_inv<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
   double dmax = 0.0;
   constexpr int kB = 4;
@@ -333,7 +351,7 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
   if (ty >= BY) return;
   const int n = ((y0 + ty) << g.lognx) + x0 + tx;
-  double2 base = (l == 0) ? __ldg(st.u0 + n) : __ldg(u + (size_t)(l - 1) * plane + (size_t)(M - 1) * g.N + n);
+  const double2 base = prev_value(st, l, n);
   double2 uc[M], Au[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) {
@@ -476,7 +494,7 @@ constexpr int kFftThreads = 256;
 // holding the M rows (p, m, y) of every y of the group.  Forward: x1 = S_p^{-1} x, then x-DIF FFT.
 // Inverse: x-DIT inverse FFT, then y = G_p^{-1} S_p x2.  All threads of a CTA share p, so the
 // M x M table loads are warp-uniform (broadcast).
-template <int M, bool INV>
+template <int M, bool INV, bool NODE>
 __global__ void __launch_bounds__(kFftThreads, kSpaceMinBlocks)
     fft2d_rows_kernel(const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X, int YG) {
   extern __shared__ double2 sm[];  // [YG][M][nx], swizzled
@@ -496,7 +514,7 @@ __global__ void __launch_bounds__(kFftThreads, kSpaceMinBlocks)
   __syncthreads();
   const double2 *tab = (INV ? at.SG : at.Sinv) + (size_t)p * M * M;
   if (!INV) {
-    for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
+    if (NODE) for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
       const int x = c & (nx - 1), yy = c >> g.lognx;
       double2 v[M];
 #pragma unroll
@@ -513,7 +531,7 @@ __global__ void __launch_bounds__(kFftThreads, kSpaceMinBlocks)
     fft_dif<4, true>(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
   } else {
     fft_dit_inv<4, true>(sm, YG * M, nx, 1, nx, g.lognx, st.twx);
-    for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
+    if (NODE) for (int c = threadIdx.x; c < YG * nx; c += blockDim.x) {
       const int x = c & (nx - 1), yy = c >> g.lognx;
       double2 v[M];
 #pragma unroll
@@ -580,6 +598,93 @@ __global__ void __launch_bounds__(kColThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// Multi-rank pieces (time-sharded cyclic distribution, four-step time FFT).
+// Rank g owns global steps l = g + P j (j < Ll = L/P).  After the local Ll-point DIF FFT (slot p,
+// kappa = bitrev_Ll(p)) and the twiddle e^{-2 pi i g kappa / L}, chunk d (p in [d Lc, (d+1) Lc),
+// Lc = Ll/P) goes to rank d.  Rank d then holds, for its local positions pl < Lc, the P values
+// y_g (g = source rank) and forms x_{kappa + Ll q} = sum_g e^{-2 pi i g q/P} y_g (q < P), stored at
+// slot sigma = q Lc + pl of the local frequency order (its factor tables are built for that order).
+
+__global__ void halo_pack_kernel(Geometry g, const double2 *__restrict__ u, double2 *__restrict__ hsend) {
+  const long long total = (long long)g.L * g.N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long l = i / g.N, n = i - l * g.N;
+    hsend[i] = __ldg(u + (l * g.M + (g.M - 1)) * (long long)g.N + n);
+  }
+}
+
+// forward: in = receive buffer [src g][pl][m][n] -> out[sigma][m][n] with S_sigma^{-1} applied
+// inverse: in[sigma][m][n] -> G_sigma^{-1} S_sigma, inverse P-point DFT -> out = send buffer
+//          [dst g][pl][m][n]
+template <int M, int P, bool INV>
+__global__ void __launch_bounds__(256) xdft_kernel(Geometry g, StaticTables st, AlphaTables at,
+                                                   const double2 *__restrict__ in, double2 *__restrict__ out) {
+  const int Lc = g.L / P;
+  const long long total = (long long)Lc * g.N;
+  const long long chunk = (long long)Lc * M * g.N;       // elements per peer chunk
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int pl = (int)(i / g.N);
+    const long long n = i - (long long)pl * g.N;
+    double2 x[P][M];
+    if (!INV) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double2 v[P];
+#pragma unroll
+        for (int gg = 0; gg < P; ++gg) v[gg] = __ldg(in + gg * chunk + ((long long)pl * M + m) * g.N + n);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          double2 acc = v[0];
+#pragma unroll
+          for (int gg = 1; gg < P; ++gg) acc = cfma(v[gg], __ldg(st.twP + (gg * q) % P), acc);
+          x[q][m] = acc;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const int sig = q * Lc + pl;
+        const double2 *S = at.Sinv + (size_t)sig * M * M;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int j = 0; j < M; ++j) acc = cfma(__ldg(S + m * M + j), x[q][j], acc);
+          out[((long long)sig * M + m) * g.N + n] = acc;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const int sig = q * Lc + pl;
+        double2 v[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) v[j] = __ldg(in + ((long long)sig * M + j) * g.N + n);
+        const double2 *S = at.SG + (size_t)sig * M * M;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int j = 0; j < M; ++j) acc = cfma(__ldg(S + m * M + j), v[j], acc);
+          x[q][m] = acc;
+        }
+      }
+#pragma unroll
+      for (int gg = 0; gg < P; ++gg) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          double2 acc = x[0][m];
+#pragma unroll
+          for (int q = 1; q < P; ++q) acc = cfma(x[q][m], cmulc(make_double2(1.0, 0.0), __ldg(st.twP + (gg * q) % P)), acc);
+          out[gg * chunk + ((long long)pl * M + m) * g.N + n] = acc;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // residual norms and initialisation
 
 template <int M>
@@ -592,7 +697,7 @@ __global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables s
        i += (long long)gridDim.x * blockDim.x) {
     const int l = (int)(i / g.N), n = (int)(i - (long long)l * g.N);
     double2 r[M];
-    residual_point<M>(g, u, st.u0, l, n, r);
+    residual_point<M>(g, st, u, l, n, r);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const double a2 = r[m].x * r[m].x + r[m].y * r[m].y;
@@ -734,8 +839,13 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
   cudaError_t e = cudaSuccess;
   if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
-      e = set_smem((const void *)fwd_kernel<MM, true, true>, smem);
-      if (e == cudaSuccess) fwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+      if (st.P == 1) {
+        e = set_smem((const void *)fwd_kernel<MM, true, true>, smem);
+        if (e == cudaSuccess) fwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+      } else {
+        e = set_smem((const void *)fwd_kernel<MM, true, false>, smem);
+        if (e == cudaSuccess) fwd_kernel<MM, true, false><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+      }
     });
     rec(s);
   } else {
@@ -796,9 +906,15 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     const size_t smem = (size_t)YG * g.M * g.nx * sizeof(double2);
     const unsigned rgrid = (unsigned)(g.L * (g.ny / YG));
     PINT_DISPATCH_M(g.M, {
-      e = set_smem((const void *)fft2d_rows_kernel<MM, false>, smem);
-      if (e == cudaSuccess) e = set_smem((const void *)fft2d_rows_kernel<MM, true>, smem);
-      if (e == cudaSuccess) fft2d_rows_kernel<MM, false><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+      if (st.P == 1) {
+        e = set_smem((const void *)fft2d_rows_kernel<MM, false, true>, smem);
+        if (e == cudaSuccess) e = set_smem((const void *)fft2d_rows_kernel<MM, true, true>, smem);
+        if (e == cudaSuccess) fft2d_rows_kernel<MM, false, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+      } else {
+        e = set_smem((const void *)fft2d_rows_kernel<MM, false, false>, smem);
+        if (e == cudaSuccess) e = set_smem((const void *)fft2d_rows_kernel<MM, true, false>, smem);
+        if (e == cudaSuccess) fft2d_rows_kernel<MM, false, false><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+      }
     });
     rec(s);
     if (e != cudaSuccess) return e;
@@ -812,7 +928,10 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     fft2d_cols_kernel<<<lines * (g.nx / T), kColThreads, smc, s>>>(g, st, at, b.X, T);
     rec(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    PINT_DISPATCH_M(g.M, { fft2d_rows_kernel<MM, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG); });
+    PINT_DISPATCH_M(g.M, {
+      if (st.P == 1) fft2d_rows_kernel<MM, true, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+      else fft2d_rows_kernel<MM, true, false><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+    });
     rec(s);
     *out = b.X;
   }
@@ -828,9 +947,15 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   cudaError_t e = cudaSuccess;
   if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
-      e = set_smem((const void *)bwd_kernel<MM, true>, smem);
-      if (e == cudaSuccess)
-        bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+      if (st.P == 1) {
+        e = set_smem((const void *)bwd_kernel<MM, true>, smem);
+        if (e == cudaSuccess)
+          bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+      } else {
+        e = set_smem((const void *)bwd_kernel<MM, false>, smem);
+        if (e == cudaSuccess)
+          bwd_kernel<MM, false><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+      }
     });
   } else {
     const int T2 = lc.tfft_T;
@@ -855,6 +980,50 @@ cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, cons
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   reduce_partials_kernel<<<1, 32, 0, s>>>(b.red, blocks, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pack(const Geometry &g, const Buffers &b, double2 *hsend, cudaStream_t s) {
+  const long long total = (long long)g.L * g.N;
+  long long blocks = (total + 255) / 256;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  halo_pack_kernel<<<(int)blocks, 256, 0, s>>>(g, b.u, hsend);
+  rec(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xdft(const Geometry &g, const StaticTables &st, const AlphaTables &at,
+                        const double2 *in, double2 *out, bool inverse, cudaStream_t s) {
+  const long long total = (long long)(g.L / st.P) * g.N;
+  long long blocks = (total + 255) / 256;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  cudaError_t e = cudaErrorInvalidValue;
+#define PINT_XDFT(PP)                                                                          \
+  if (st.P == PP) {                                                                            \
+    PINT_DISPATCH_M(g.M, {                                                                     \
+      if constexpr (MM * PP <= 32) {                                                           \
+        if (inverse) xdft_kernel<MM, PP, true><<<(int)blocks, 256, 0, s>>>(g, st, at, in, out);  \
+        else xdft_kernel<MM, PP, false><<<(int)blocks, 256, 0, s>>>(g, st, at, in, out);         \
+        e = cudaGetLastError();                                                                \
+      }                                                                                        \
+    });                                                                                        \
+  }
+  PINT_XDFT(2)
+  PINT_XDFT(4)
+  PINT_XDFT(8)
+#undef PINT_XDFT
+  rec(s);
+  return e;
+}
+
+__global__ void square_first_kernel(const double *in, double *out) { out[0] = in[0] * in[0]; }
+__global__ void sqrt_into_kernel(const double *in, double *out) { out[0] = sqrt(in[0]); }
+cudaError_t launch_square_first(const double *in, double *out, cudaStream_t s) {
+  square_first_kernel<<<1, 1, 0, s>>>(in, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_sqrt_into(const double *in, double *out, cudaStream_t s) {
+  sqrt_into_kernel<<<1, 1, 0, s>>>(in, out);
   return cudaGetLastError();
 }
 

@@ -2,6 +2,7 @@
 // carving and the stream-ordered iteration driver.  Every step of the iteration runs in the
 // kernels of kernels.cu; this file only builds tables and enqueues launches.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
@@ -27,8 +28,9 @@ pint_status fail(pint_status s, const std::string &msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t vec_bytes;      // one L*M*N complex128 vector
+  size_t vec_bytes;      // one local (L/P)*M*N complex128 vector
   size_t off_X, off_Y;
+  size_t off_hsend, off_hrecv, halo_bytes;   // P > 1: ring halo buffers [L/P][N]
   size_t off_static, static_bytes;
   size_t off_alpha, alpha_bytes_each;
   size_t off_red, red_bytes;
@@ -41,6 +43,9 @@ struct Layout {
 struct pint_ctx {
   pint_problem prob;
   pint_dist dist;
+  int P = 1, rank = 0;
+  ncclComm_t comm = nullptr;       // P > 1 with an NCCL unique id
+  bool loopback = false;           // P > 1 without an id: driven by pint_group_iterate
   Geometry g;
   LaunchCfg lc;
   Layout lay;
@@ -74,26 +79,32 @@ static pint_status validate(const pint_problem *p, const pint_dist *d) {
   if (!std::isfinite(p->nu) || !std::isfinite(p->cx) || !std::isfinite(p->cy))
     return fail(PINT_ERR_INVALID, "non-finite coefficient");
   if (d) {
-    if (d->nranks != 1 || d->rank != 0)
-      return fail(PINT_ERR_INVALID, "this build runs one rank per problem (nranks == 1)");
+    const int P = d->nranks;
+    if (P != 1 && P != 2 && P != 4 && P != 8) return fail(PINT_ERR_INVALID, "nranks must be 1, 2, 4 or 8");
+    if (d->rank < 0 || d->rank >= P) return fail(PINT_ERR_INVALID, "rank out of range");
+    if (P > 1) {
+      if ((p->L / P) % P != 0 || p->L < P * P)
+        return fail(PINT_ERR_INVALID, "time sharding needs (L/nranks) % nranks == 0 (four-step FFT, L >= nranks^2)");
+      if (p->M * P > 32) return fail(PINT_ERR_INVALID, "time sharding needs M * nranks <= 32");
+    }
   }
   return PINT_OK;
 }
 
-static Geometry make_geometry(const pint_problem *p) {
+static Geometry make_geometry(const pint_problem *p, int P) {
   Geometry g{};
   g.dim = p->dim;
   g.nx = p->nx;
   g.ny = p->dim == 2 ? p->ny : 1;
   g.N = g.nx * g.ny;
-  g.L = p->L;
+  g.L = p->L / P;          // local step count (cyclic distribution l = rank + P j)
   g.M = p->M;
   g.op = p->op;
   g.logL = ilog2(g.L);
   g.logN = ilog2(g.N);
   g.lognx = ilog2(g.nx);
   g.logny = ilog2(g.ny);
-  g.dT = p->T / p->L;
+  g.dT = p->T / p->L;      // global step size
   const double nx = g.nx, ny = g.ny;
   if (p->op == PINT_OP_HEAT) {
     g.cxm = g.cxp = p->nu * nx * nx;
@@ -114,17 +125,22 @@ static Geometry make_geometry(const pint_problem *p) {
   return g;
 }
 
-static Layout make_layout(const Geometry &g, const LaunchCfg &lc) {
+static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   Layout L{};
   L.vec_bytes = (size_t)g.L * g.M * g.N * sizeof(double2);
-  L.two_vectors = (g.dim == 1 && lc.pcr_mode == 1);
+  L.two_vectors = (g.dim == 1 && lc.pcr_mode == 1) || P > 1;
   size_t off = 0;
   L.off_X = off;
   off = align_up(off + L.vec_bytes, 256);
   L.off_Y = L.two_vectors ? off : L.off_X;
   if (L.two_vectors) off = align_up(off + L.vec_bytes, 256);
+  L.halo_bytes = P > 1 ? (size_t)g.L * g.N * sizeof(double2) : 0;
+  L.off_hsend = off;
+  off = align_up(off + L.halo_bytes, 256);
+  L.off_hrecv = off;
+  off = align_up(off + L.halo_bytes, 256);
   L.off_static = off;
-  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N) * sizeof(double2);
+  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8) * sizeof(double2);
   off = align_up(off + L.static_bytes, 256);
   L.off_alpha = off;
   const size_t LM = (size_t)g.L * g.M;
@@ -159,8 +175,9 @@ const char *pint_last_error(void) { return g_err.c_str(); }
 
 size_t pint_workspace_bytes(const pint_problem *p, const pint_dist *d) {
   if (validate(p, d) != PINT_OK) return 0;
-  Geometry g = make_geometry(p);
-  return make_layout(g, choose_launch(g)).total;
+  const int P = d ? d->nranks : 1;
+  Geometry g = make_geometry(p, P);
+  return make_layout(g, choose_launch(g), P).total;
 }
 
 pint_status pint_tableau(int32_t M, double *t, double *Q) {
@@ -195,14 +212,17 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   if (forcing_host) return fail(PINT_ERR_INVALID, "forcing b != 0 is not supported in this build");
   if (((uintptr_t)u_dev) % 16) return fail(PINT_ERR_INVALID, "u_dev must be 16-byte aligned");
   if (((uintptr_t)work_dev) % 256) return fail(PINT_ERR_INVALID, "work_dev must be 256-byte aligned");
-  Geometry g = make_geometry(p);
+  const int P = d->nranks, rank = d->rank;
+  Geometry g = make_geometry(p, P);
   LaunchCfg lc = choose_launch(g);
-  Layout lay = make_layout(g, lc);
+  Layout lay = make_layout(g, lc, P);
   if (work_bytes < lay.total) return fail(PINT_ERR_INVALID, "work_bytes < pint_workspace_bytes");
 
   pint_ctx *c = new pint_ctx();
   c->prob = *p;
   c->dist = *d;
+  c->P = P;
+  c->rank = rank;
   c->g = g;
   c->lc = lc;
   c->lay = lay;
@@ -248,6 +268,17 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   size_t o_u0 = o;
   c->u0.assign(u0_host, u0_host + 2 * (size_t)g.N);
   for (int n = 0; n < g.N; ++n) host[o++] = make_double2(u0_host[2 * n], u0_host[2 * n + 1]);
+  // four-step tables (P > 1): twr[p] = e^{-2 pi i rank bitrev_Ll(p) / L}, twP[q] = e^{-2 pi i q / P}
+  size_t o_twr = o;
+  for (int q = 0; q < g.L; ++q) {
+    cld w = unit_root((long long)rank * bitrev(q, g.logL), p->L, -1);
+    host[o++] = make_double2((double)w.real(), (double)w.imag());
+  }
+  size_t o_twP = o;
+  for (int q = 0; q < 8; ++q) {
+    cld w = unit_root(q % P, P, -1);
+    host[o++] = make_double2((double)w.real(), (double)w.imag());
+  }
   double2 *sbase = (double2 *)(c->work + lay.off_static);
   CUDA_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
   c->st.twL = sbase + o_twL;
@@ -256,6 +287,32 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   c->st.lamx = sbase + o_lx;
   c->st.lamy = sbase + o_ly;
   c->st.u0 = sbase + o_u0;
+  c->st.P = P;
+  c->st.rank = rank;
+  if (P == 1) {
+    c->st.prev_base = c->u + (size_t)(g.M - 1) * g.N;
+    c->st.prev_stride = (long long)g.M * g.N;
+    c->st.prev_shift = 1;
+    c->st.twr = nullptr;
+    c->st.twP = nullptr;
+  } else {
+    c->st.prev_base = (const double2 *)(c->work + lay.off_hrecv);
+    c->st.prev_stride = g.N;
+    c->st.prev_shift = rank == 0 ? 1 : 0;
+    c->st.twr = sbase + o_twr;
+    c->st.twP = sbase + o_twP;
+    if (d->nccl_unique_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, d->nccl_unique_id, sizeof id);
+      ncclResult_t r = ncclCommInitRank(&c->comm, P, id, rank);
+      if (r != ncclSuccess) {
+        delete c;
+        return fail(PINT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      }
+    } else {
+      c->loopback = true;
+    }
+  }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
             (double *)(c->work + lay.off_red)};
   CUDA_TRY(c, launch_init_iterate(c->g, c->st, b, c->stream));
@@ -285,8 +342,9 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
   for (int a = 0; a < K; ++a)
     if (!(alpha[a] > 0.0 && alpha[a] < 1.0)) return fail(PINT_ERR_SCHEDULE, "alpha must be in (0, 1)");
   const Geometry &g = c->g;
-  const int L = g.L, M = g.M;
-  const ld dT = (ld)c->prob.T / L;
+  const int L = g.L, M = g.M;            // L: local step / frequency-slot count
+  const int Lg = c->prob.L, P = c->P, rank = c->rank;
+  const ld dT = (ld)c->prob.T / Lg;
   // A's stencil as (sub, diag, super) for the 1-D PCR coefficients
   ld aA, bA, cA;
   if (c->prob.op == PINT_OP_HEAT) {
@@ -314,18 +372,27 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
       off_inv = off;
       inv_e = (double2 *)(blob.data() + off); off += (size_t)L * M * sizeof(double2);
     }
-    for (int l = 0; l < L; ++l) {
-      sf[l] = (double)powl(al, (ld)l / L);               // alpha^{l/L}
-      sb[l] = (double)(powl(al, -(ld)l / L) / L);        // alpha^{-l/L} / L
+    for (int j = 0; j < L; ++j) {
+      const ld lgl = (ld)(rank + (long long)P * j);      // global step of local step j
+      sf[j] = (double)powl(al, lgl / Lg);                // alpha^{l/L}
+      sb[j] = (double)(powl(al, -lgl / Lg) / Lg);        // alpha^{-l/L} / L
     }
-    hS[a].resize((size_t)L * M * M);
-    hSi[a].resize((size_t)L * M * M);
-    hD[a].resize((size_t)L * M);
-    hdk[a].resize(L);
-    const ld aroot = powl(al, 1.0L / L);
-    for (int k = 0; k < L; ++k) {
-      const int p = bitrev(k, g.logL);
-      const cld dk = -aroot * unit_root(k, L, -1);        // d_k = -alpha^{1/L} e^{-2 pi i k/L}
+    hS[a].assign((size_t)Lg * M * M, cld(0));
+    hSi[a].assign((size_t)Lg * M * M, cld(0));
+    hD[a].assign((size_t)Lg * M, cld(0));
+    hdk[a].assign(Lg, cld(0));
+    const ld aroot = powl(al, 1.0L / Lg);
+    for (int p = 0; p < L; ++p) {
+      // frequency of local slot p: 1 rank: bit-reversed order; P ranks: slot q*Lc + pl holds
+      // kappa + Ll q with kappa = bitrev_Ll(rank*Lc + pl)  (four-step order, kernels.cu)
+      int k;
+      if (P == 1) {
+        k = bitrev(p, g.logL);
+      } else {
+        const int Lc = L / P, q = p / Lc, pl = p % Lc;
+        k = bitrev(rank * Lc + pl, g.logL) + L * q;
+      }
+      const cld dk = -aroot * unit_root(k, Lg, -1);       // d_k = -alpha^{1/L} e^{-2 pi i k/L}
       const cld rk = dk / (1.0L + dk);                     // r_k = d_k / (1 + d_k)
       hdk[a][k] = dk;
       std::vector<cld> B((size_t)M * M);
@@ -398,20 +465,107 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
   return PINT_OK;
 }
 
-static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
+static double2 *hsend(pint_ctx *c) { return (double2 *)(c->work + c->lay.off_hsend); }
+static double2 *hrecv(pint_ctx *c) { return (double2 *)(c->work + c->lay.off_hrecv); }
+static size_t chunk_elems(pint_ctx *c) { return (size_t)(c->g.L / c->P) * c->g.M * c->g.N; }
+
+// ---- phases of one iteration.  1 rank: forward -> solve -> backward on one GPU.  P ranks
+// (DESIGN.md §7): [pack halo] -> ring exchange -> forward (residual with the received halo,
+// local FFT, four-step twiddle) -> all-to-all -> cross-rank DFT + S^{-1} -> solves ->
+// G^{-1}S + inverse cross-rank DFT -> all-to-all -> backward.
+enum Phase { PH_PRE, PH_FWD, PH_MID, PH_BWD };
+
+struct IterState {
+  double2 *solved = nullptr;     // buffer holding the solve output (P > 1: then the A2A-back target)
+  double2 *send_back = nullptr;  // P > 1: inverse cross-rank DFT output (send chunks)
+};
+
+static pint_status run_phase(pint_ctx *c, Phase ph, int a, double *diff_slot, IterState &is) {
   Buffers b = buffers(c);
   const AlphaTables &at = c->at[a];
-  CUDA_TRY(c, launch_forward(c->g, c->lc, c->st, at, b, c->stream));
-  double2 *x2 = nullptr;
-  CUDA_TRY(c, launch_solve(c->g, c->lc, c->st, at, b, c->stream, &x2));
-  CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, diff_slot, c->stream));
+  switch (ph) {
+    case PH_PRE:
+      if (c->P > 1) CUDA_TRY(c, launch_halo_pack(c->g, b, hsend(c), c->stream));
+      break;
+    case PH_FWD:
+      CUDA_TRY(c, launch_forward(c->g, c->lc, c->st, at, b, c->stream));
+      break;
+    case PH_MID: {
+      if (c->P > 1) CUDA_TRY(c, launch_xdft(c->g, c->st, at, b.Y, b.X, false, c->stream));
+      double2 *x2 = nullptr;
+      CUDA_TRY(c, launch_solve(c->g, c->lc, c->st, at, b, c->stream, &x2));
+      if (c->P > 1) {
+        double2 *other = (x2 == b.X) ? b.Y : b.X;
+        CUDA_TRY(c, launch_xdft(c->g, c->st, at, x2, other, true, c->stream));
+        is.send_back = other;
+        is.solved = x2;        // A2A back lands here (its contents are no longer needed)
+      } else {
+        is.solved = x2;
+      }
+      break;
+    }
+    case PH_BWD:
+      CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, is.solved, diff_slot, c->stream));
+      break;
+  }
   return PINT_OK;
+}
+
+// NCCL exchanges of one rank (all on the context stream)
+static pint_status nccl_halo(pint_ctx *c) {
+  const size_t cnt = (size_t)c->g.L * c->g.N * 2;
+  const int next = (c->rank + 1) % c->P, prev = (c->rank + c->P - 1) % c->P;
+  ncclResult_t r = ncclGroupStart();
+  if (r == ncclSuccess) r = ncclSend(hsend(c), cnt, ncclDouble, next, c->comm, c->stream);
+  if (r == ncclSuccess) r = ncclRecv(hrecv(c), cnt, ncclDouble, prev, c->comm, c->stream);
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    c->poisoned = true;
+    return fail(PINT_ERR_NCCL, std::string("halo exchange: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+  }
+  return PINT_OK;
+}
+
+static pint_status nccl_alltoall(pint_ctx *c, const double2 *send, double2 *recv) {
+  const size_t ce = chunk_elems(c);
+  ncclResult_t r = ncclGroupStart();
+  for (int d = 0; d < c->P && r == ncclSuccess; ++d) {
+    r = ncclSend(send + d * ce, ce * 2, ncclDouble, d, c->comm, c->stream);
+    if (r == ncclSuccess) r = ncclRecv(recv + d * ce, ce * 2, ncclDouble, d, c->comm, c->stream);
+  }
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    c->poisoned = true;
+    return fail(PINT_ERR_NCCL, std::string("all-to-all: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+  }
+  return PINT_OK;
+}
+
+static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
+  IterState is;
+  pint_status st;
+  if (c->P == 1) {
+    if ((st = run_phase(c, PH_FWD, a, nullptr, is)) != PINT_OK) return st;
+    if ((st = run_phase(c, PH_MID, a, nullptr, is)) != PINT_OK) return st;
+    return run_phase(c, PH_BWD, a, diff_slot, is);
+  }
+  if (!c->comm) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: use pint_group_iterate");
+  Buffers b = buffers(c);
+  if ((st = run_phase(c, PH_PRE, a, nullptr, is)) != PINT_OK) return st;
+  if ((st = nccl_halo(c)) != PINT_OK) return st;
+  if ((st = run_phase(c, PH_FWD, a, nullptr, is)) != PINT_OK) return st;
+  if ((st = nccl_alltoall(c, b.X, b.Y)) != PINT_OK) return st;
+  if ((st = run_phase(c, PH_MID, a, nullptr, is)) != PINT_OK) return st;
+  if ((st = nccl_alltoall(c, is.send_back, is.solved)) != PINT_OK) return st;
+  // last-step diff: only the rank holding global step L-1 (rank P-1) reports it
+  return run_phase(c, PH_BWD, a, c->rank == c->P - 1 ? diff_slot : nullptr, is);
 }
 
 pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (n_iter < 0) return fail(PINT_ERR_INVALID, "n_iter < 0");
+  if (c->loopback) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: use pint_group_iterate");
   if (c->k + n_iter > (int)c->alphas.size())
     return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
   double *slots = nullptr;
@@ -426,9 +580,117 @@ pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf
     c->k++;
   }
   if (slots) {
+    if (c->P > 1) {  // only rank P-1 wrote its slots; max over ranks gives everyone the value
+      ncclResult_t r = ncclAllReduce(slots, slots, n_iter, ncclDouble, ncclMax, c->comm, c->stream);
+      if (r != ncclSuccess) { c->poisoned = true; return fail(PINT_ERR_NCCL, ncclGetErrorString(r)); }
+    }
     CUDA_TRY(c, cudaMemcpyAsync(last_step_diff_inf, slots, n_iter * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   }
+  return PINT_OK;
+}
+
+pint_status pint_nccl_unique_id(void *out128) {
+  if (!out128) return fail(PINT_ERR_INVALID, "NULL argument");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(PINT_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof id);
+  return PINT_OK;
+}
+
+pint_status pint_local_steps(pint_ctx *c, int32_t *first, int32_t *stride, int32_t *count) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (first) *first = c->rank;
+  if (stride) *stride = c->P;
+  if (count) *count = c->g.L;
+  return PINT_OK;
+}
+
+pint_status pint_group_iterate(pint_ctx *const *ctxs, int32_t P, int32_t n_iter, double *last_step_diff_inf) {
+  if (!ctxs || P < 2) return fail(PINT_ERR_INVALID, "need the P >= 2 contexts of one virtual group");
+  for (int r = 0; r < P; ++r) {
+    pint_ctx *c = ctxs[r];
+    if (!c || !c->loopback || c->P != P || c->rank != r)
+      return fail(PINT_ERR_INVALID, "ctxs[r] must be the loopback context of rank r of a P-rank group");
+    if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+    if (c->stream != ctxs[0]->stream || c->dist.device != ctxs[0]->dist.device)
+      return fail(PINT_ERR_INVALID, "virtual ranks must share one device and one stream");
+    if (c->k != ctxs[0]->k || c->alphas.size() != ctxs[0]->alphas.size())
+      return fail(PINT_ERR_STATE, "virtual ranks out of step");
+    if (c->k + n_iter > (int)c->alphas.size())
+      return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
+  }
+  if (n_iter < 0) return fail(PINT_ERR_INVALID, "n_iter < 0");
+  cudaStream_t s = ctxs[0]->stream;
+  const size_t ce = chunk_elems(ctxs[0]) * sizeof(double2);
+  const size_t hb = ctxs[0]->lay.halo_bytes;
+  double *slots = nullptr;
+  pint_ctx *last = ctxs[P - 1];
+  if (last_step_diff_inf && n_iter > 0) {
+    if (n_iter > PINT_MAX_SCHEDULE) return fail(PINT_ERR_INVALID, "n_iter too large");
+    slots = (double *)(last->work + last->lay.off_red) + 148 * 8 * 2 + 64;
+    CUDA_TRY(last, cudaMemsetAsync(slots, 0, n_iter * sizeof(double), s));
+  }
+  for (int it = 0; it < n_iter; ++it) {
+    std::vector<IterState> is(P);
+    const int a = ctxs[0]->k;
+    pint_status st;
+    for (int r = 0; r < P; ++r)
+      if ((st = run_phase(ctxs[r], PH_PRE, a, nullptr, is[r])) != PINT_OK) return st;
+    for (int r = 0; r < P; ++r)  // ring: rank r -> rank r+1
+      CUDA_TRY(ctxs[r], cudaMemcpyAsync(hrecv(ctxs[(r + 1) % P]), hsend(ctxs[r]), hb, cudaMemcpyDeviceToDevice, s));
+    for (int r = 0; r < P; ++r)
+      if ((st = run_phase(ctxs[r], PH_FWD, a, nullptr, is[r])) != PINT_OK) return st;
+    for (int src = 0; src < P; ++src)
+      for (int dst = 0; dst < P; ++dst)
+        CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)buffers(ctxs[dst]).Y + src * ce,
+                                            (const char *)buffers(ctxs[src]).X + dst * ce, ce,
+                                            cudaMemcpyDeviceToDevice, s));
+    for (int r = 0; r < P; ++r)
+      if ((st = run_phase(ctxs[r], PH_MID, a, nullptr, is[r])) != PINT_OK) return st;
+    for (int src = 0; src < P; ++src)
+      for (int dst = 0; dst < P; ++dst)
+        CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)is[dst].solved + src * ce,
+                                            (const char *)is[src].send_back + dst * ce, ce,
+                                            cudaMemcpyDeviceToDevice, s));
+    for (int r = 0; r < P; ++r)
+      if ((st = run_phase(ctxs[r], PH_BWD, a, (r == P - 1 && slots) ? slots + it : nullptr, is[r])) != PINT_OK)
+        return st;
+    for (int r = 0; r < P; ++r) ctxs[r]->k++;
+  }
+  if (slots) {
+    CUDA_TRY(last, cudaMemcpyAsync(last_step_diff_inf, slots, n_iter * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(last, cudaStreamSynchronize(s));
+  }
+  return PINT_OK;
+}
+
+pint_status pint_group_residual_norm(pint_ctx *const *ctxs, int32_t P, double *l2, double *linf) {
+  if (!ctxs || P < 2) return fail(PINT_ERR_INVALID, "need the P >= 2 contexts of one virtual group");
+  for (int r = 0; r < P; ++r)
+    if (!ctxs[r] || !ctxs[r]->loopback || ctxs[r]->P != P || ctxs[r]->rank != r)
+      return fail(PINT_ERR_INVALID, "ctxs[r] must be the loopback context of rank r of a P-rank group");
+  cudaStream_t s = ctxs[0]->stream;
+  const size_t hb = ctxs[0]->lay.halo_bytes;
+  for (int r = 0; r < P; ++r) CUDA_TRY(ctxs[r], launch_halo_pack(ctxs[r]->g, buffers(ctxs[r]), hsend(ctxs[r]), s));
+  for (int r = 0; r < P; ++r)
+    CUDA_TRY(ctxs[r], cudaMemcpyAsync(hrecv(ctxs[(r + 1) % P]), hsend(ctxs[r]), hb, cudaMemcpyDeviceToDevice, s));
+  double sum2 = 0.0, mx = 0.0;
+  for (int r = 0; r < P; ++r) {
+    pint_ctx *c = ctxs[r];
+    double *out2 = (double *)(c->work + c->lay.off_red) + 148 * 8 * 2;
+    CUDA_TRY(c, launch_residual_norm(c->g, c->st, buffers(c), out2, s));
+    double h[2];
+    CUDA_TRY(c, cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    sum2 += h[0] * h[0];
+    mx = std::fmax(mx, h[1]);
+  }
+  if (l2) *l2 = std::sqrt(sum2);
+  if (linf) *linf = mx;
+  if (!std::isfinite(sum2) || !std::isfinite(mx)) return fail(PINT_ERR_NUMERIC, "non-finite residual");
   return PINT_OK;
 }
 
@@ -437,7 +699,23 @@ pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf) {
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   Buffers b = buffers(c);
   double *out2 = (double *)(c->work + c->lay.off_red) + 148 * 8 * 2;
+  if (c->P > 1) {
+    if (c->loopback) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: use pint_group_residual_norm");
+    CUDA_TRY(c, launch_halo_pack(c->g, b, hsend(c), c->stream));
+    pint_status st = nccl_halo(c);
+    if (st != PINT_OK) return st;
+  }
   CUDA_TRY(c, launch_residual_norm(c->g, c->st, b, out2, c->stream));
+  if (c->P > 1) {  // global: sum of squares and max over ranks
+    double *sq = out2 + 2;
+    CUDA_TRY(c, launch_square_first(out2, sq, c->stream));
+    ncclResult_t r = ncclGroupStart();
+    if (r == ncclSuccess) r = ncclAllReduce(sq, sq, 1, ncclDouble, ncclSum, c->comm, c->stream);
+    if (r == ncclSuccess) r = ncclAllReduce(out2 + 1, out2 + 1, 1, ncclDouble, ncclMax, c->comm, c->stream);
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) { c->poisoned = true; return fail(PINT_ERR_NCCL, "residual allreduce"); }
+    CUDA_TRY(c, launch_sqrt_into(sq, out2, c->stream));
+  }
   double h[2];
   CUDA_TRY(c, cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -477,12 +755,14 @@ pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t r
 }
 
 pint_status pint_destroy(pint_ctx *c) {
+  if (c && c->comm) ncclCommDestroy(c->comm);
   delete c;
   return PINT_OK;
 }
 
 pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms) {
   if (!c || !kernel_ms) return fail(PINT_ERR_INVALID, "NULL argument");
+  if (c->P > 1) return fail(PINT_ERR_INVALID, "per-launch profiling is single-rank only");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (c->k + n_iter > (int)c->alphas.size())
     return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
@@ -524,7 +804,7 @@ int32_t pint_launches_per_iteration(pint_ctx *c) {
 
 pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, double *S, double *Sinv,
                              double *d_km) {
-  if (!c || a < 0 || a >= (int)c->h_S.size() || k < 0 || k >= c->g.L)
+  if (!c || a < 0 || a >= (int)c->h_S.size() || k < 0 || k >= c->prob.L)
     return fail(PINT_ERR_INVALID, "bad schedule entry / frequency");
   const int M = c->g.M;
   if (d_k) { d_k[0] = (double)c->h_dk[a][k].real(); d_k[1] = (double)c->h_dk[a][k].imag(); }
@@ -539,6 +819,7 @@ pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, dou
 
 pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s) {
   if (!c || a < 0 || a >= (int)c->at.size()) return fail(PINT_ERR_INVALID, "bad schedule entry");
+  if (c->P > 1) return fail(PINT_ERR_INVALID, "debug stages are single-rank only");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   Buffers b = buffers(c);
   const AlphaTables &at = c->at[a];

@@ -26,7 +26,8 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_set_alpha_schedule", "pint_iterate", "pint_residual_norm", "pint_get_iterate",
            "pint_get_final_value", "pint_set_initial_value", "pint_destroy", "pint_last_error",
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
-           "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name"]
+           "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
+           "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm"]
 
 
 class PintError(RuntimeError):
@@ -82,6 +83,10 @@ def load_library(path: str = LIB_PATH):
         "pint_debug_get_work": (i32, [vp, i32, dp]),
         "pint_iterate_profiled": (i32, [vp, i32, dp]),
         "pint_kernel_name": (ctypes.c_char_p, [vp, i32]),
+        "pint_nccl_unique_id": (i32, [vp]),
+        "pint_local_steps": (i32, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "pint_group_iterate": (i32, [ctypes.POINTER(vp), i32, i32, dp]),
+        "pint_group_residual_norm": (i32, [ctypes.POINTER(vp), i32, dp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -123,10 +128,23 @@ def adaptive_schedule(L: int, w_inf: float, m0: float, K: int, eps: float = 2.0 
     return a[:K].copy(), m
 
 
-class Solver:
-    """One Paralpha context on one GPU.  Device buffers are torch tensors (complex128)."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.pint_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
 
-    def __init__(self, problem, u0: np.ndarray, device: int = 0, stream=None):
+
+class Solver:
+    """One Paralpha context on one GPU (one rank).  Device buffers are torch tensors (complex128).
+
+    nranks > 1 shards the time steps cyclically (rank r owns global steps r + nranks*j); with an
+    nccl_id the ranks exchange over NCCL, without one the context is a virtual rank of a
+    single-process loopback Group."""
+
+    def __init__(self, problem, u0: np.ndarray, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("pint needs a CUDA device (no CPU fallback)")
@@ -135,11 +153,14 @@ class Solver:
         self.cp = make_problem(problem)
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.dist = Dist(0, 1, None, device, ctypes.c_void_p(self.stream.cuda_stream))
+        self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self.dist = Dist(rank, nranks, ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None,
+                         device, ctypes.c_void_p(self.stream.cuda_stream))
+        self.rank, self.nranks = rank, nranks
         nbytes = self.lib.pint_workspace_bytes(ctypes.byref(self.cp), ctypes.byref(self.dist))
         if nbytes == 0:
             raise PintError(1, self.lib.pint_last_error().decode())
-        self.L, self.M, self.N = problem.L, problem.M, problem.nx * (problem.ny if problem.dim == 2 else 1)
+        self.L, self.M, self.N = problem.L // nranks, problem.M, problem.nx * (problem.ny if problem.dim == 2 else 1)
         self.u = torch.empty((self.L, self.M, self.N), dtype=torch.complex128, device=self.device)
         self.work = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         u0h = np.ascontiguousarray(np.asarray(u0, dtype=np.complex128)).view(np.float64)
@@ -218,6 +239,11 @@ class Solver:
         _check(self.lib.pint_debug_get_work(self.ctx, which, _dp(out.view(np.float64))))
         return out
 
+    def local_steps(self):
+        a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(self.lib.pint_local_steps(self.ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
     def close(self):
         if getattr(self, "ctx", None):
             self.lib.pint_destroy(self.ctx)
@@ -228,3 +254,45 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+class Group:
+    """Single-process loopback group of P virtual ranks on one GPU (tests of the sharded path):
+    the same kernels and phase sequence as the NCCL ranks, chunks moved by device copies."""
+
+    def __init__(self, problem, u0: np.ndarray, P: int, device: int = 0):
+        import torch
+        self.P = P
+        self.problem = problem
+        stream = torch.cuda.current_stream(torch.device("cuda", device))
+        self.ranks = [Solver(problem, u0, device=device, stream=stream, rank=r, nranks=P) for r in range(P)]
+        self.lib = self.ranks[0].lib
+        self._ctxs = (ctypes.c_void_p * P)(*[s.ctx.value for s in self.ranks])
+
+    def set_alpha_schedule(self, alphas):
+        for s in self.ranks:
+            s.set_alpha_schedule(alphas)
+
+    def iterate(self, n: int = 1, want_diff: bool = False):
+        d = np.zeros(n) if want_diff else None
+        _check(self.lib.pint_group_iterate(self._ctxs, self.P, n, _dp(d)))
+        return d
+
+    def residual_norm(self):
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(self.lib.pint_group_residual_norm(self._ctxs, self.P, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def get_iterate(self) -> np.ndarray:
+        """Global iterate u[l][m][n] gathered from the ranks (rank r holds l = r + P j)."""
+        p = self.problem
+        N = p.nx * (p.ny if p.dim == 2 else 1)
+        out = np.empty((p.L, p.M, N), dtype=np.complex128)
+        for s in self.ranks:
+            first, stride, count = s.local_steps()
+            out[first::stride] = s.get_iterate()
+        return out
+
+    def close(self):
+        for s in self.ranks:
+            s.close()

@@ -92,14 +92,22 @@ def test_workspace_and_validation():
         assert n == 0 and msg in err, (bad, err)
 
 
-def test_create_rejects_null_and_nranks():
+def test_create_rejects_null_and_bad_sharding():
     lib = P.load_library()
 
     class Pr:
         dim, nx, ny, op, nu, cx, cy, T, L, M = 1, 64, 1, "heat", 1.0, 0.0, 0.0, 0.1, 4, 2
 
     cp = P.make_problem(Pr)
-    d = P.pint.Dist(0, 2, None, 0, None)
     ctx = ctypes.c_void_p()
-    st = lib.pint_create(ctypes.byref(cp), ctypes.byref(d), None, None, 0, None, None, ctypes.byref(ctx))
-    assert st == 1 and "nranks" in lib.pint_last_error().decode()
+    for nranks, rank, msg in [(3, 0, "nranks must be"), (4, 0, "time sharding"), (2, 2, "rank out of range"),
+                              (2, 0, "NULL buffer")]:
+        d = P.pint.Dist(rank, nranks, None, 0, None)
+        st = lib.pint_create(ctypes.byref(cp), ctypes.byref(d), None, None, 0, None, None, ctypes.byref(ctx))
+        assert st == 1 and msg in lib.pint_last_error().decode(), (nranks, lib.pint_last_error())
+    # M * nranks <= 32
+    Pr.M, Pr.L = 8, 64
+    cp = P.make_problem(Pr)
+    d = P.pint.Dist(0, 8, None, 0, None)
+    assert lib.pint_workspace_bytes(ctypes.byref(cp), ctypes.byref(d)) == 0
+    assert "M * nranks" in lib.pint_last_error().decode()
