@@ -220,7 +220,12 @@ def main():
         return float(t.item())
 
     u0 = p.u0()
-    s = P.Solver(p, u0, device=local)
+    if world > 1:
+        # time-sharded across the ranks (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)
+        from paper_2103_12571_b200.distributed import sharded_solver
+        s = sharded_solver(p, u0, device=local)
+    else:
+        s = P.Solver(p, u0, device=local)
     stream = s.stream
     w_inf = s.w_inf()
     nlaunch = s.launches_per_iteration()
@@ -245,18 +250,31 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
-    value = world * p.U / (ms * 1e-3)
+    value = p.U / (ms * 1e-3)          # the whole problem (all ranks together) per iteration
 
-    # ---- per-kernel device times (same kernels, events after every launch) ---------------------
-    nprof = max(3, min(args.steps, 10))
-    s.set_alpha_schedule(schedule_for(p, w_inf, nprof + 1))
-    s.iterate(1)
-    kms = s.iterate_profiled(nprof)
+    # ---- per-kernel device times (same kernels, events after every launch; 1 rank only) -------
     peak, peak_src = measured_peaks()
-    top = int(np.argmax(kms))
+    if world == 1:
+        nprof = max(3, min(args.steps, 10))
+        s.set_alpha_schedule(schedule_for(p, w_inf, nprof + 1))
+        s.iterate(1)
+        kms = s.iterate_profiled(nprof)
+    else:
+        kms = None
+    model_bytes = sum(ALGO_BYTES.get(n_, 32) for n_ in names)
+    iteration_roof = {"model_bytes_per_unknown": model_bytes,
+                      "achieved_gbs": model_bytes * p.U / world / (ms * 1e-3) / 1e9,
+                      "frac": model_bytes * p.U / world / (ms * 1e-3) / 1e9 / peak,
+                      "floor96_frac": 96 * p.U / world / (ms * 1e-3) / 1e9 / peak,
+                      "note": "per GPU (local share of the HBM model bytes)"}
+    if kms is None:
+        roofline = {"bound": "hbm", "kernel": None, "achieved": iteration_roof["achieved_gbs"], "peak": peak,
+                    "unit": "GB/s", "frac": iteration_roof["frac"], "traffic": None, "peak_source": peak_src,
+                    "iteration": iteration_roof, "note": "multi-rank: per-launch profiling is single-rank only"}
+    top = int(np.argmax(kms)) if kms is not None else 0
     top_name = names[top]
     algo = ALGO_BYTES.get(top_name, 32) * p.U
-    achieved = algo / (kms[top] * 1e-3) / 1e9
+    achieved = algo / (kms[top] * 1e-3) / 1e9 if kms is not None else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -264,16 +282,13 @@ def main():
             traffic = json.load(open(tpath)).get(p.name, {}).get(top_name)
         except Exception:
             traffic = None
-    model_bytes = sum(ALGO_BYTES.get(n_, 32) for n_ in names)
-    roofline = {"bound": "hbm", "kernel": top_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "algo_bytes_per_launch": algo,
-                "kernel_share_of_step": float(kms[top] / kms.sum()),
-                "per_kernel_ms": {n_: float(v) for n_, v in zip(names, kms)},
-                "iteration": {"model_bytes_per_unknown": model_bytes,
-                              "achieved_gbs": model_bytes * p.U / (ms * 1e-3) / 1e9,
-                              "frac": model_bytes * p.U / (ms * 1e-3) / 1e9 / peak,
-                              "floor96_frac": 96 * p.U / (ms * 1e-3) / 1e9 / peak}}
+    if kms is not None:
+        roofline = {"bound": "hbm", "kernel": top_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "algo_bytes_per_launch": algo,
+                    "kernel_share_of_step": float(kms[top] / kms.sum()),
+                    "per_kernel_ms": {n_: float(v) for n_, v in zip(names, kms)},
+                    "iteration": iteration_roof}
 
     # ---- end to end through the public API with host buffers -----------------------------------
     e2e = None
@@ -303,7 +318,7 @@ def main():
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         ems = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3)) / ke
-        e2e = {"value": world * p.U / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * p.N,
+        e2e = {"value": p.U / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * p.N * world,
                "d2h_bytes_per_step": 16 * p.N, "ms_per_step": ems,
                "what": "per step: H2D u0 (pinned) -> pint_iterate(1) -> D2H u_{L-1,M-1} (solution at T)"}
 
@@ -314,15 +329,17 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak",
                 "vs_baseline": None, "dtype": "c128 (fp64)",
                 "data": "synthetic (workloads.py seeded generators; BASELINE.json config recipe)",
                 "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
                            "unknowns": p.U, "bytes_per_vector": 16 * p.U,
                            "l2": "inputs larger than L2 (no flush)" if 16 * p.U > 126e6 else "L2-resident",
-                           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+                           "parallelism": "single GPU" if world == 1 else
+                           f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": nlaunch * args.steps, "clocks": clk.summary()}
+                "gpu_launches": (nlaunch if world == 1 else nlaunch + 3) * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     s.close()
     if dist is not None:
