@@ -441,6 +441,113 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
   }
 }
 
+// one block-arrangement PCR level with compile-time stride H (< E: only the 2H edge values move
+// between lanes; >= E: whole neighbours H/E lanes away)
+template <int E, int H>
+__device__ __forceinline__ void pcr_block_level(double2 (&y)[E], int b, int S, double2 pj, double2 qj) {
+  double2 nv[E];
+  if constexpr (H < E) {
+    const int left = (b + S - 1) & (S - 1), right = (b + 1) & (S - 1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      double2 lv, rv;
+      if (e >= H) {
+        lv = y[e - H];
+      } else {
+        lv.x = __shfl_sync(0xffffffffu, y[e - H + E].x, left, S);
+        lv.y = __shfl_sync(0xffffffffu, y[e - H + E].y, left, S);
+      }
+      if (e + H < E) {
+        rv = y[e + H];
+      } else {
+        rv.x = __shfl_sync(0xffffffffu, y[e + H - E].x, right, S);
+        rv.y = __shfl_sync(0xffffffffu, y[e + H - E].y, right, S);
+      }
+      nv[e] = cfms(qj, rv, cfms(pj, lv, y[e]));
+    }
+  } else {
+    constexpr int d = H / E;
+    const int bl = (b + S - d) & (S - 1), br = (b + d) & (S - 1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      double2 lv, rv;
+      lv.x = __shfl_sync(0xffffffffu, y[e].x, bl, S);
+      lv.y = __shfl_sync(0xffffffffu, y[e].y, bl, S);
+      rv.x = __shfl_sync(0xffffffffu, y[e].x, br, S);
+      rv.y = __shfl_sync(0xffffffffu, y[e].y, br, S);
+      nv[e] = cfms(qj, rv, cfms(pj, lv, y[e]));
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) y[e] = nv[e];
+}
+
+// Register-resident variant of the class pass (two-pass scheme, nq = N/R <= 32*E): E class
+// elements per thread.  Levels with stride h' < S = nq/E run in a BLOCK arrangement (thread holds
+// q in [b E, (b+1) E) of one column; neighbours across the block edge come from lanes b-1/b+1 by
+// warp shuffle); then one shared-memory transposition to a CLASS arrangement (thread holds
+// q = c + S k), where every stride h' >= S is closed in registers (cyclic in k).  Large strides
+// are applied last, so the 1/e scaling and the store happen from the class arrangement
+// (coalesced over the T columns).  Level operators commute (circulant), so the order is free.
+template <int E>
+__global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, AlphaTables at, double2 *__restrict__ X,
+                                                         int R, int T, int j_off) {
+  extern __shared__ double2 sm[];  // [nq][T], swizzled
+  const int N = g.N;
+  const int nq = N / R;
+  const int lognq = g.logN - j_off;
+  const int S = nq / E;                 // lanes per column in the block arrangement
+  const int logS = 31 - __clz(S);
+  const int lT = 31 - __clz(T);
+  const int groups = R / T;
+  const int line = blockIdx.x / groups;
+  const int r0 = (blockIdx.x - line * groups) * T;
+  double2 *xl = X + (size_t)line * N;
+  const int items = nq * T;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int tt = it & (T - 1), q = it >> lT;
+    cp_async16(sm + swz(it), xl + (size_t)q * R + r0 + tt);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
+  double2 y[E];
+  {  // block arrangement: thread -> (column, block b); the S lanes of a column are consecutive
+    const int b = threadIdx.x & (S - 1), col = threadIdx.x >> logS;
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = sm[swz(((b * E + e) << lT) + col)];
+    const double2 *cb = coef + 2 * j_off;
+#define PINT_BLK(H, JJ) \
+    if ((H) < S) pcr_block_level<E, H>(y, b, S, __ldg(cb + 2 * (JJ)), __ldg(cb + 2 * (JJ) + 1));
+    PINT_BLK(1, 0) PINT_BLK(2, 1) PINT_BLK(4, 2) PINT_BLK(8, 3) PINT_BLK(16, 4)
+#undef PINT_BLK
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[swz(((b * E + e) << lT) + col)] = y[e];
+  }
+  __syncthreads();
+  // class arrangement: thread -> (column fastest, class c); holds q = c + S k
+  const int col = threadIdx.x & (T - 1), c = threadIdx.x >> lT;
+#pragma unroll
+  for (int k = 0; k < E; ++k) y[k] = sm[swz(((c + (k << logS)) << lT) + col)];
+  for (int jj = logS; jj < lognq; ++jj) {   // strides h' = S 2^i, i.e. 2^i in k (cyclic over E)
+    const int hk = 1 << (jj - logS);
+    const double2 pj = __ldg(coef + 2 * (j_off + jj)), qj = __ldg(coef + 2 * (j_off + jj) + 1);
+    const bool pair = (jj == lognq - 1);
+    double2 nv[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const double2 rv = y[(k + hk) & (E - 1)];
+      if (pair) nv[k] = cfms(pj, rv, y[k]);
+      else nv[k] = cfms(qj, rv, cfms(pj, y[(k - hk) & (E - 1)], y[k]));
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) y[k] = nv[k];
+  }
+  const double2 ie = __ldg(at.inv_e + line);
+#pragma unroll
+  for (int k = 0; k < E; ++k) xl[(size_t)(c + (k << logS)) * R + r0 + col] = cmul(y[k], ie);
+}
+
 // Small-stride levels 0..jA-1 on contiguous chunks of C with halos of H >= 2^jA - 1 (redundant
 // halo computation, out of place X -> Y).
 constexpr int kChunkThreads = 512;
@@ -886,8 +993,16 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       const int jOff = __builtin_ctz((unsigned)R);
       const int nq = g.N / R;
       size_t smem = (size_t)nq * T * sizeof(double2);
-      if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-      pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff);
+      constexpr int E = 8;
+      const int Sr = nq / E, Tr = Sr > 0 ? 256 / Sr : 0;
+      if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
+        const size_t smr = (size_t)nq * Tr * sizeof(double2);
+        if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
+        pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff);
+      } else {
+        if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
+        pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff);
+      }
       rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       const int C = lc.pcr_chunk, H = R;
