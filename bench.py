@@ -32,6 +32,10 @@ UNIT = "unknowns/s"
 ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32, "fft2d_rows_kernel<fwd>": 32,
               "fft2d_cols_kernel": 32, "fft2d_rows_kernel<inv>": 32, "bwd_kernel": 48, "residual2d_kernel": 32,
               "tfft_fwd_kernel": 32, "tfft_bwd_kernel": 48}
+# direct form (u = C_a^{-1}((C_a - C)u + w)): no read of u, input synthesized from one N-vector
+ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
+                     "cols_direct_kernel": 16, "fft2d_rows_kernel<inv>": 32, "tfft_bwd_kernel": 32,
+                     "pcr_classes_kernel": 16, "pcr_chunk_kernel": 32, "bwd_kernel": 32}
 
 
 def env_rank():
@@ -187,6 +191,8 @@ def main():
     ap.add_argument("--cpu-target-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
     ap.add_argument("--grid", type=int, default=0, help="profiling only: override nx (and ny in 2-D)")
+    ap.add_argument("--form", default="correction", choices=["correction", "direct"],
+                    help="iteration form: correction (north star, default) or direct (Alg. 1 as printed)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     p = W.CONFIGS[args.config]
@@ -226,6 +232,8 @@ def main():
         s = sharded_solver(p, u0, device=local)
     else:
         s = P.Solver(p, u0, device=local)
+    if args.form != "correction":
+        s.set_form(args.form)
     stream = s.stream
     w_inf = s.w_inf()
     nlaunch = s.launches_per_iteration()
@@ -261,7 +269,8 @@ def main():
         kms = s.iterate_profiled(nprof)
     else:
         kms = None
-    model_bytes = sum(ALGO_BYTES.get(n_, 32) for n_ in names)
+    algo_tab = ALGO_BYTES_DIRECT if args.form == "direct" else ALGO_BYTES
+    model_bytes = sum(algo_tab.get(n_, 32) for n_ in names)
     iteration_roof = {"model_bytes_per_unknown": model_bytes,
                       "achieved_gbs": model_bytes * p.U / world / (ms * 1e-3) / 1e9,
                       "frac": model_bytes * p.U / world / (ms * 1e-3) / 1e9 / peak,
@@ -273,7 +282,7 @@ def main():
                     "iteration": iteration_roof, "note": "multi-rank: per-launch profiling is single-rank only"}
     top = int(np.argmax(kms)) if kms is not None else 0
     top_name = names[top]
-    algo = ALGO_BYTES.get(top_name, 32) * p.U
+    algo = algo_tab.get(top_name, 32) * p.U
     achieved = algo / (kms[top] * 1e-3) / 1e9 if kms is not None else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -334,7 +343,7 @@ def main():
                 "vs_baseline": None, "dtype": "c128 (fp64)",
                 "data": "synthetic (workloads.py seeded generators; BASELINE.json config recipe)",
                 "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
-                           "unknowns": p.U, "bytes_per_vector": 16 * p.U,
+                           "unknowns": p.U, "bytes_per_vector": 16 * p.U, "form": args.form,
                            "l2": "inputs larger than L2 (no flush)" if 16 * p.U > 126e6 else "L2-resident",
                            "parallelism": "single GPU" if world == 1 else
                            f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},

@@ -122,6 +122,15 @@ pint_status pint_w_inf(pint_ctx *c, double *w_inf);
  * PINT_ERR_INVALID (K > PINT_MAX_SCHEDULE), PINT_ERR_CUDA. */
 pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K);
 
+/* Iteration form.  PINT_FORM_CORRECTION (default; north star, reading R1):
+ * u <- u + C_a^{-1}(w - C u).  PINT_FORM_DIRECT (Alg. 1 as printed, eq. Riteration
+ * P:159): u <- C_a^{-1}((C_a - C) u + w); (C_a - C) u + w = w - alpha e_1 (x) H u_L has a
+ * single non-zero block r0 = u0 - alpha u_{L-1,M-1}, so the residual pass and the forward time
+ * transform collapse to one N-vector.  Direct form: nranks == 1 only. */
+#define PINT_FORM_CORRECTION 0
+#define PINT_FORM_DIRECT 1
+pint_status pint_set_form(pint_ctx *c, int32_t form);
+
 /* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:
  * nullable; if given, n_iter doubles receive ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf (Alg. 2 line 7,
  * P:421) and the call synchronises the stream.  PINT_ERR_SCHEDULE if the schedule would run out. */

@@ -166,6 +166,16 @@ class Oracle:
         c = np.einsum("lk,kmn->lmn", V_matrix(p.L, alpha), y)               # (v)   eq. s3
         return u + c
 
+    def iterate_direct(self, u: np.ndarray, alpha: float) -> np.ndarray:
+        """Alg. 1 as printed (eq. Riteration): u^{k+1} = C_a^{-1} ((C_a - C) u + w).
+        (C_a - C) u + w = w - alpha e_1 (x) H u_L: only block 0 is non-zero."""
+        p = self.p
+        r = w_vector(p, self.u0)
+        r[0, :, :] -= alpha * u[p.L - 1, p.M - 1, :][None, :]
+        x = np.einsum("kl,lmn->kmn", V_inverse(p.L, alpha), r)
+        y = self.solver.solve(alpha, x)
+        return np.einsum("lk,kmn->lmn", V_matrix(p.L, alpha), y)
+
     def residual_norms(self, u: np.ndarray):
         r = residual(self.p, self.tab, u, self.u0)
         return float(np.linalg.norm(r.ravel())), float(np.abs(r).max())
@@ -211,6 +221,24 @@ class ModeOracle:
         Cu[1:] -= uh[:-1, p.M - 1, :][:, None, :]
         return w - Cu
 
+    def iterate_direct(self, uh: np.ndarray, alpha: float) -> np.ndarray:
+        """Direct form for the sampled modes: uh^{k+1} = C_a(lam)^{-1} (w - alpha e_1 (x) H uh_L)."""
+        p = self.p
+        r = np.zeros_like(uh)
+        r[0] = self.u0hat[None, :] - alpha * uh[p.L - 1, p.M - 1, :][None, :]
+        return self._solve_ca(r, alpha)
+
+    def _solve_ca(self, r: np.ndarray, alpha: float) -> np.ndarray:
+        p, tab = self.p, self.tab
+        x = np.einsum("kl,lmj->kmj", V_inverse(p.L, alpha), r)
+        d = d_values(p.L, alpha)
+        y = np.empty_like(x)
+        for k in range(p.L):
+            G = np.eye(p.M) + d[k] * tab.H
+            B = G[None, :, :] - p.dT * self.lam[:, None, None] * tab.Q[None, :, :]
+            y[k] = np.linalg.solve(B, x[k].T[:, :, None])[:, :, 0].T
+        return np.einsum("lk,kmj->lmj", V_matrix(p.L, alpha), y)
+
     def iterate(self, uh: np.ndarray, alpha: float) -> np.ndarray:
         p, tab = self.p, self.tab
         r = self.residual(uh)
@@ -234,6 +262,14 @@ def assemble_C(p, tab: Tableau, alpha: float | None = None) -> np.ndarray:
     Ccoll = np.eye(p.M * p.N) - p.dT * np.kron(tab.Q, A)
     H = np.kron(tab.H, np.eye(p.N))
     return np.kron(np.eye(p.L), Ccoll) + np.kron(E_matrix(p.L, alpha), H)
+
+
+def brute_force_iterate_direct(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, alpha: float) -> np.ndarray:
+    """u^{k+1} = solve(C_a, (C_a - C) u + w) with C, C_a assembled densely (eq. Riteration)."""
+    C = assemble_C(p, tab)
+    Ca = assemble_C(p, tab, alpha)
+    w = w_vector(p, u0).reshape(-1)
+    return np.linalg.solve(Ca, (Ca - C) @ u.reshape(-1) + w).reshape(u.shape)
 
 
 def brute_force_iterate(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, alpha: float) -> np.ndarray:

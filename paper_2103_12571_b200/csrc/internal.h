@@ -16,6 +16,8 @@ struct AlphaTables {
   const double2 *shift;       // [L][M]    s_km = d_km dT
   const double2 *pcr;         // [L][M][nlev] (p_j, q_j) pairs: 2 double2 per level  (1-D only)
   const double2 *inv_e;       // [L][M]    1 / e_final of the row-sum-carrying PCR   (1-D only)
+  const double2 *sig;         // [L][M]    row sums of S_k^{-1} (direct form: S^{-1} (1 (x) r0))
+  double alpha;
 };
 
 struct Geometry {
@@ -78,7 +80,17 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
                          const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out);
 cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                             const AlphaTables &at, const Buffers &b, const double2 *x2,
-                            double *diff_slot, cudaStream_t s);
+                            double *diff_slot, cudaStream_t s, int overwrite);
+// Direct form (Alg. 1 as printed, 1 rank): r0 = u0 - alpha u_{L-1,M-1}; its time transform is
+// constant over frequencies, so x1_{k,m} = sig_km r0.  front: r0 (+ 2-D: one-plane forward FFT
+// and the synthesized column pass into b.X); solve: 1-D PCR reading sig*r0 / 2-D inverse row
+// pass; then launch_backward(..., overwrite = 1).
+cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s);
+cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
+                                double2 **out);
+int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc);
 cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
                                  double *out2, cudaStream_t s);
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,

@@ -148,7 +148,7 @@ __device__ __forceinline__ unsigned long long dbl_bits(double v) { return (unsig
 template <int M, bool NODE>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
-               double2 *__restrict__ u, int T, unsigned long long *diff_slot) {
+               double2 *__restrict__ u, int T, unsigned long long *diff_slot, int overwrite) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
   const int lT = 31 - __clz(T);
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     const int t = idx & (T - 1), row = idx >> lT;
     cp_async16(sm + sidx<false>(idx), X2 + (size_t)row * g.N + n0 + t);
   }
-  for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
+  if (!overwrite)
+    for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
   cp_async_wait_all();
   __syncthreads();
   if (!NODE && st.twr) {  // P > 1: inverse four-step twiddle e^{+2 pi i rank kappa/L}
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       const int idx = base + k * blockDim.x;
       if (idx < all) {
         const int t = idx & (T - 1), row = idx >> lT;
-        uo[k] = u[(size_t)row * g.N + n0 + t];
+        const bool need_old = !overwrite || (diff_slot && row / M == L - 1);
+        uo[k] = need_old ? u[(size_t)row * g.N + n0 + t] : make_double2(0.0, 0.0);
         sc[k] = __ldg(at.scale_bwd + row / M);
       }
     }
@@ -211,8 +213,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), row = idx >> lT;
         const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
-        u[(size_t)row * g.N + n0 + t] = cadd(uo[k], c);
-        if (row / M == L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
+        u[(size_t)row * g.N + n0 + t] = overwrite ? c : cadd(uo[k], c);   // direct form: u = C_a^{-1} r
+        if (row / M == L - 1) {
+          const double2 dd = overwrite ? csub(c, uo[k]) : c;
+          dmax = fmax(dmax, hypot(dd.x, dd.y));
+        }
       }
     }
   }
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tfft_bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
-                    double2 *__restrict__ u, int T, unsigned long long *diff_slot) {
+                    double2 *__restrict__ u, int T, unsigned long long *diff_slot, int overwrite) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
   const int lT = 31 - __clz(T);
@@ -293,7 +298,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       const int idx = b0 + k * blockDim.x;
       if (idx < all) {
         const int t = idx & (T - 1), l = idx >> lT;
-        uo[k] = ub[(size_t)l * lstride + t];
+        const bool need_old = !overwrite || (diff_slot && l == g.L - 1);
+        uo[k] = need_old ? ub[(size_t)l * lstride + t] : make_double2(0.0, 0.0);
         sc[k] = __ldg(at.scale_bwd + l);
       }
     }
@@ -303,8 +309,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), l = idx >> lT;
         const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
-        ub[(size_t)l * lstride + t] = cadd(uo[k], c);
-        if (l == g.L - 1) dmax = fmax(dmax, hypot(c.x, c.y));
+        ub[(size_t)l * lstride + t] = overwrite ? c : cadd(uo[k], c);
+        if (l == g.L - 1) {
+          const double2 dd = overwrite ? csub(c, uo[k]) : c;
+          dmax = fmax(dmax, hypot(dd.x, dd.y));
+        }
       }
     }
   }
@@ -391,7 +400,7 @@ constexpr int kPcrIPT = 16;   // items per thread held in registers per level
 // Applies coefficient levels j_off .. nlev-1 (the last is the pair level) and multiplies by 1/e.
 __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry g, AlphaTables at,
                                                                   double2 *__restrict__ X, int R, int T,
-                                                                  int j_off) {
+                                                                  int j_off, const double2 *__restrict__ r0) {
   extern __shared__ double2 sm[];  // [nq][T]
   const int lT = 31 - __clz(T);
   const int N = g.N;
@@ -399,12 +408,12 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
   const int lognq = g.logN - j_off;
   const int groups = R / T;
   const int line = blockIdx.x / groups;
-  const int r0 = (blockIdx.x - line * groups) * T;
+  const int rr = (blockIdx.x - line * groups) * T;
   double2 *xl = X + (size_t)line * N;
   const int items = nq * T;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it & (T - 1), q = it >> lT;
-    sm[it] = xl[(size_t)q * R + r0 + tt];
+    sm[it] = r0 ? cmul(__ldg(at.sig + line), __ldg(r0 + (size_t)q * R + rr + tt)) : xl[(size_t)q * R + rr + tt];
   }
   __syncthreads();
   const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
@@ -437,7 +446,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
   const double2 ie = __ldg(at.inv_e + line);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it & (T - 1), q = it >> lT;
-    xl[(size_t)q * R + r0 + tt] = cmul(sm[it], ie);
+    xl[(size_t)q * R + rr + tt] = cmul(sm[it], ie);
   }
 }
 
@@ -491,7 +500,7 @@ __device__ __forceinline__ void pcr_block_level(double2 (&y)[E], int b, int S, d
 // (coalesced over the T columns).  Level operators commute (circulant), so the order is free.
 template <int E>
 __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, AlphaTables at, double2 *__restrict__ X,
-                                                         int R, int T, int j_off) {
+                                                         int R, int T, int j_off, const double2 *__restrict__ r0) {
   extern __shared__ double2 sm[];  // [nq][T], swizzled
   const int N = g.N;
   const int nq = N / R;
@@ -501,12 +510,13 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
   const int lT = 31 - __clz(T);
   const int groups = R / T;
   const int line = blockIdx.x / groups;
-  const int r0 = (blockIdx.x - line * groups) * T;
+  const int rr = (blockIdx.x - line * groups) * T;
   double2 *xl = X + (size_t)line * N;
   const int items = nq * T;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it & (T - 1), q = it >> lT;
-    cp_async16(sm + swz(it), xl + (size_t)q * R + r0 + tt);
+    if (r0) sm[swz(it)] = cmul(__ldg(at.sig + line), __ldg(r0 + (size_t)q * R + rr + tt));  // direct form
+    else cp_async16(sm + swz(it), xl + (size_t)q * R + rr + tt);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -545,7 +555,7 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
   }
   const double2 ie = __ldg(at.inv_e + line);
 #pragma unroll
-  for (int k = 0; k < E; ++k) xl[(size_t)(c + (k << logS)) * R + r0 + col] = cmul(y[k], ie);
+  for (int k = 0; k < E; ++k) xl[(size_t)(c + (k << logS)) * R + rr + col] = cmul(y[k], ie);
 }
 
 // Small-stride levels 0..jA-1 on contiguous chunks of C with halos of H >= 2^jA - 1 (redundant
@@ -701,6 +711,89 @@ __global__ void __launch_bounds__(kColThreads, 1)
   for (int i = threadIdx.x; i < items; i += blockDim.x) {
     const int tt = i & (T - 1), y = i >> lT;
     xl[(size_t)y * nx + kx0 + tt] = sm[sidx<false>(i)];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Direct form (Alg. 1 as printed): r = (C_a - C) u + w = w - alpha e_1 (x) H u_L
+// has one non-zero block, r0 = u0 - alpha u_{L-1,M-1} replicated over the nodes; its
+// scaled time DFT is r0 at every frequency, so the forward transform costs one N-vector.
+
+__global__ void direct_r0_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ u,
+                                 double2 *__restrict__ r0) {
+  const double2 *ul = u + ((size_t)(g.L - 1) * g.M + (g.M - 1)) * g.N;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x) {
+    const double2 a = __ldg(st.u0 + n), b = __ldg(ul + n);
+    r0[n] = make_double2(a.x - at.alpha * b.x, a.y - at.alpha * b.y);
+  }
+}
+
+// one plane: x-DIF of YG rows per CTA (in place, bit-reversed kx positions)
+__global__ void __launch_bounds__(kFftThreads) plane_rows_dif_kernel(const Geometry g, StaticTables st,
+                                                                     double2 *__restrict__ P, int YG) {
+  extern __shared__ double2 sm[];
+  const int nx = g.nx;
+  double2 *base = P + (size_t)blockIdx.x * YG * nx;
+  const int items = YG * nx;
+  for (int i = threadIdx.x; i < items; i += blockDim.x) cp_async16(sm + swz(i), base + i);
+  cp_async_wait_all();
+  __syncthreads();
+  fft_dif<4, true>(sm, YG, nx, 1, nx, g.lognx, st.twx);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) base[i] = sm[swz(i)];
+}
+
+// one plane: y-DIF of T columns per CTA (in place, bit-reversed ky positions)
+__global__ void __launch_bounds__(kFftThreads) plane_cols_dif_kernel(const Geometry g, StaticTables st,
+                                                                     double2 *__restrict__ P, int T) {
+  extern __shared__ double2 sm[];
+  const int lT = 31 - __clz(T);
+  const int kx0 = blockIdx.x * T;
+  const int items = g.ny * T;
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i & (T - 1), y = i >> lT;
+    cp_async16(sm + swz(i), P + (size_t)y * g.nx + kx0 + tt);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  fft_dif<4, true>(sm, T, 1, T, g.ny, g.logny, st.twy);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i & (T - 1), y = i >> lT;
+    P[(size_t)y * g.nx + kx0 + tt] = sm[swz(i)];
+  }
+}
+
+// synthesized column pass: x2_{km} spectrum = sig_km r0hat / (1 - s_km lambda) / (nx ny), then the
+// y-DIT inverse; writes the (line, all y, T columns) tile of X (no read of X)
+__global__ void __launch_bounds__(kColThreads, 1)
+    cols_direct_kernel(const Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ spec,
+                       double2 *__restrict__ X, int T) {
+  extern __shared__ double2 sm[];  // [ny][T]
+  const int lT = 31 - __clz(T);
+  const int nx = g.nx, ny = g.ny;
+  const int groups = nx / T;
+  const int line = blockIdx.x / groups;
+  const int kx0 = (blockIdx.x - line * groups) * T;
+  double2 *xl = X + (size_t)line * g.N;
+  const int items = ny * T;
+  const double2 s = __ldg(at.shift + line);
+  const double2 sg = cscale(__ldg(at.sig + line), 1.0 / ((double)nx * (double)ny));
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i & (T - 1), py = i >> lT;
+    const int kx = brev(kx0 + tt, g.lognx), ky = brev(py, g.logny);
+    const double2 lam = cadd(__ldg(st.lamx + kx), __ldg(st.lamy + ky));
+    const double2 sl = cmul(s, lam);
+    const double dr = 1.0 - sl.x, di = -sl.y;
+    const double q = dr * dr + di * di;
+    double rq = __drcp_rn(q);
+    rq = fma(rq, fma(-q, rq, 1.0), rq);
+    const double2 v = cmul(sg, __ldg(spec + (size_t)py * nx + kx0 + tt));
+    sm[i] = make_double2((v.x * dr + v.y * di) * rq, (v.y * dr - v.x * di) * rq);
+  }
+  __syncthreads();
+  fft_dit_inv<4, false>(sm, T, 1, T, ny, g.logny, st.twy);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int tt = i & (T - 1), y = i >> lT;
+    xl[(size_t)y * nx + kx0 + tt] = sm[i];
   }
 }
 
@@ -985,7 +1078,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     if (lc.pcr_mode == 0) {
       const size_t smem = (size_t)g.N * sizeof(double2);
       if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-      pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0);
+      pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, nullptr);
       rec(s);
       *out = b.X;
     } else {
@@ -998,10 +1091,10 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
         const size_t smr = (size_t)nq * Tr * sizeof(double2);
         if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
-        pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff);
+        pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, nullptr);
       } else {
         if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-        pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff);
+        pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, nullptr);
       }
       rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1055,7 +1148,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
 
 cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                             const AlphaTables &at, const Buffers &b, const double2 *x2,
-                            double *diff_slot, cudaStream_t s) {
+                            double *diff_slot, cudaStream_t s, int overwrite) {
   const int T = lc.fwd_T;
   const size_t smem = fwd_smem_bytes(g, T);
   const int grid = g.N / T;
@@ -1065,11 +1158,11 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
       if (st.P == 1) {
         e = set_smem((const void *)bwd_kernel<MM, true>, smem);
         if (e == cudaSuccess)
-          bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+          bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
       } else {
         e = set_smem((const void *)bwd_kernel<MM, false>, smem);
         if (e == cudaSuccess)
-          bwd_kernel<MM, false><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot);
+          bwd_kernel<MM, false><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
       }
     });
   } else {
@@ -1078,10 +1171,102 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
     e = set_smem((const void *)tfft_bwd_kernel, sm2);
     if (e == cudaSuccess)
       tfft_bwd_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
-                                                                    (unsigned long long *)diff_slot);
+                                                                    (unsigned long long *)diff_slot, overwrite);
   }
   rec(s);
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc) {
+  if (g.dim == 2) return 6;               // r0, plane rows, plane cols, synthesized cols, rows<inv>, bwd
+  return lc.pcr_mode == 0 ? 3 : 4;        // r0, pcr (1 or 2), bwd
+}
+
+cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s) {
+  (void)lc;
+  int blocks = (g.N + 255) / 256;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  direct_r0_kernel<<<blocks, 256, 0, s>>>(g, st, at, b.u, r0);
+  rec(s);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || g.dim == 1) return e;
+  int YG = 4096 / g.nx;
+  if (YG < 1) YG = 1;
+  if (YG > g.ny) YG = g.ny;
+  size_t smr = (size_t)YG * g.nx * sizeof(double2);
+  if ((e = set_smem((const void *)plane_rows_dif_kernel, smr)) != cudaSuccess) return e;
+  plane_rows_dif_kernel<<<g.ny / YG, kFftThreads, smr, s>>>(g, st, r0, YG);
+  rec(s);
+  int Tp = 4096 / g.ny;
+  if (Tp < 1) Tp = 1;
+  if (Tp > g.nx) Tp = g.nx;
+  size_t smc = (size_t)g.ny * Tp * sizeof(double2);
+  if ((e = set_smem((const void *)plane_cols_dif_kernel, smc)) != cudaSuccess) return e;
+  plane_cols_dif_kernel<<<g.nx / Tp, kFftThreads, smc, s>>>(g, st, r0, Tp);
+  rec(s);
+  int T = 8192 / g.ny;
+  if (T < 1) T = 1;
+  if (T > g.nx) T = g.nx;
+  if (T > 16) T = 16;
+  size_t smd = (size_t)g.ny * T * sizeof(double2);
+  if ((e = set_smem((const void *)cols_direct_kernel, smd)) != cudaSuccess) return e;
+  cols_direct_kernel<<<g.L * g.M * (g.nx / T), kColThreads, smd, s>>>(g, st, at, r0, b.X, T);
+  rec(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
+                                double2 **out) {
+  cudaError_t e = cudaSuccess;
+  const int lines = g.L * g.M;
+  if (g.dim == 2) {
+    int YG = 4096 / (g.M * g.nx);
+    if (YG < 1) YG = 1;
+    if (YG > g.ny) YG = g.ny;
+    while (g.ny % YG) YG >>= 1;
+    const size_t smem = (size_t)YG * g.M * g.nx * sizeof(double2);
+    const unsigned rgrid = (unsigned)(g.L * (g.ny / YG));
+    PINT_DISPATCH_M(g.M, {
+      e = set_smem((const void *)fft2d_rows_kernel<MM, true, true>, smem);
+      if (e == cudaSuccess) fft2d_rows_kernel<MM, true, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+    });
+    rec(s);
+    *out = b.X;
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
+  if (lc.pcr_mode == 0) {
+    const size_t smem = (size_t)g.N * sizeof(double2);
+    if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
+    pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, r0);
+    rec(s);
+    *out = b.X;
+    return cudaGetLastError();
+  }
+  const int R = lc.pcr_R, T = lc.pcr_T;
+  const int jOff = __builtin_ctz((unsigned)R);
+  const int nq = g.N / R;
+  constexpr int E = 8;
+  const int Sr = nq / E, Tr = Sr > 0 ? 256 / Sr : 0;
+  if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
+    const size_t smr = (size_t)nq * Tr * sizeof(double2);
+    if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
+    pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, r0);
+  } else {
+    const size_t smem = (size_t)nq * T * sizeof(double2);
+    if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
+    pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, r0);
+  }
+  rec(s);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int C = lc.pcr_chunk, H = R;
+  const size_t smc = (size_t)(C + 2 * H) * sizeof(double2);
+  if ((e = set_smem((const void *)pcr_chunk_kernel, smc)) != cudaSuccess) return e;
+  pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smc, s>>>(g, at, b.X, b.Y, C, H, jOff);
+  rec(s);
+  *out = b.Y;
   return cudaGetLastError();
 }
 

@@ -31,6 +31,7 @@ struct Layout {
   size_t vec_bytes;      // one local (L/P)*M*N complex128 vector
   size_t off_X, off_Y;
   size_t off_hsend, off_hrecv, halo_bytes;   // P > 1: ring halo buffers [L/P][N]
+  size_t off_r0;                              // direct form: r0 / its 2-D spectrum [N]
   size_t off_static, static_bytes;
   size_t off_alpha, alpha_bytes_each;
   size_t off_red, red_bytes;
@@ -56,6 +57,7 @@ struct pint_ctx {
   std::vector<AlphaTables> at;
   std::vector<double> alphas;
   int k = 0;
+  int form = PINT_FORM_CORRECTION;
   bool poisoned = false;
   std::vector<ld> t, Q;
   std::vector<double> u0;          // host copy (2N)
@@ -139,6 +141,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   off = align_up(off + L.halo_bytes, 256);
   L.off_hrecv = off;
   off = align_up(off + L.halo_bytes, 256);
+  L.off_r0 = off;
+  off = align_up(off + (size_t)g.N * sizeof(double2), 256);
   L.off_static = off;
   L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8) * sizeof(double2);
   off = align_up(off + L.static_bytes, 256);
@@ -148,6 +152,7 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   per = align_up(per, 16);
   per += 2 * LM * g.M * sizeof(double2);                                   // Sinv, SG
   per += LM * sizeof(double2);                                             // shift
+  per += LM * sizeof(double2);                                             // sig (row sums of S^{-1})
   if (g.dim == 1) per += LM * g.logN * 2 * sizeof(double2) + LM * sizeof(double2);  // pcr, inv_e
   L.alpha_bytes_each = align_up(per, 256);
   off += L.alpha_bytes_each * PINT_MAX_SCHEDULE;
@@ -364,6 +369,7 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
     double2 *Sinv = (double2 *)(blob.data() + off); off += (size_t)L * M * M * sizeof(double2);
     double2 *SG = (double2 *)(blob.data() + off); off += (size_t)L * M * M * sizeof(double2);
     double2 *shift = (double2 *)(blob.data() + off); off += (size_t)L * M * sizeof(double2);
+    double2 *sig = (double2 *)(blob.data() + off); off += (size_t)L * M * sizeof(double2);
     double2 *pcr = nullptr, *inv_e = nullptr;
     size_t off_pcr = 0, off_inv = 0;
     if (g.dim == 1) {
@@ -409,6 +415,11 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
       }
       for (int i = 0; i < M * M; ++i) { hS[a][(size_t)k * M * M + i] = S[i]; hSi[a][(size_t)k * M * M + i] = Si[i]; }
       for (int m = 0; m < M; ++m) hD[a][(size_t)k * M + m] = lam[m];
+      for (int m = 0; m < M; ++m) {
+        cld rs = 0;
+        for (int j = 0; j < M; ++j) rs += Si[(size_t)m * M + j];
+        sig[(size_t)p * M + m] = make_double2((double)rs.real(), (double)rs.imag());
+      }
       for (int m = 0; m < M; ++m)
         for (int j = 0; j < M; ++j) {
           cld v = Si[(size_t)m * M + j];
@@ -452,6 +463,8 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
     t.Sinv = (const double2 *)(dst + o2); o2 += (size_t)L * M * M * sizeof(double2);
     t.SG = (const double2 *)(dst + o2); o2 += (size_t)L * M * M * sizeof(double2);
     t.shift = (const double2 *)(dst + o2); o2 += (size_t)L * M * sizeof(double2);
+    t.sig = (const double2 *)(dst + o2); o2 += (size_t)L * M * sizeof(double2);
+    t.alpha = (double)al;
     t.pcr = g.dim == 1 ? (const double2 *)(dst + off_pcr) : nullptr;
     t.inv_e = g.dim == 1 ? (const double2 *)(dst + off_inv) : nullptr;
   }
@@ -505,7 +518,7 @@ static pint_status run_phase(pint_ctx *c, Phase ph, int a, double *diff_slot, It
       break;
     }
     case PH_BWD:
-      CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, is.solved, diff_slot, c->stream));
+      CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, is.solved, diff_slot, c->stream, 0));
       break;
   }
   return PINT_OK;
@@ -544,6 +557,16 @@ static pint_status nccl_alltoall(pint_ctx *c, const double2 *send, double2 *recv
 static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
   IterState is;
   pint_status st;
+  if (c->form == PINT_FORM_DIRECT) {  // Alg. 1 as printed: u = C_a^{-1}((C_a - C) u + w), 1 rank
+    Buffers b = buffers(c);
+    const AlphaTables &at = c->at[a];
+    double2 *r0 = (double2 *)(c->work + c->lay.off_r0);
+    CUDA_TRY(c, launch_direct_front(c->g, c->lc, c->st, at, b, r0, c->stream));
+    double2 *x2 = nullptr;
+    CUDA_TRY(c, launch_direct_solve(c->g, c->lc, c->st, at, b, r0, c->stream, &x2));
+    CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, diff_slot, c->stream, 1));
+    return PINT_OK;
+  }
   if (c->P == 1) {
     if ((st = run_phase(c, PH_FWD, a, nullptr, is)) != PINT_OK) return st;
     if ((st = run_phase(c, PH_MID, a, nullptr, is)) != PINT_OK) return st;
@@ -794,12 +817,31 @@ pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms
 
 const char *pint_kernel_name(pint_ctx *c, int32_t i) {
   if (!c) return "";
+  if (c->form == PINT_FORM_DIRECT) {
+    static const char *k1a[] = {"direct_r0_kernel", "pcr_classes_kernel", "bwd_kernel"};
+    static const char *k1b[] = {"direct_r0_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
+    static const char *k2[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel",
+                               "cols_direct_kernel", "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
+    const int n = launches_per_iteration_direct(c->g, c->lc);
+    if (i < 0 || i >= n) return "";
+    if (c->g.dim == 2) return k2[i];
+    return c->lc.pcr_mode == 0 ? k1a[i] : k1b[i];
+  }
   return kernel_name(c->g, c->lc, i);
 }
 
 int32_t pint_launches_per_iteration(pint_ctx *c) {
   if (!c) return -1;
+  if (c->form == PINT_FORM_DIRECT) return launches_per_iteration_direct(c->g, c->lc);
   return launches_per_iteration(c->g, c->lc);
+}
+
+pint_status pint_set_form(pint_ctx *c, int32_t form) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (form != PINT_FORM_CORRECTION && form != PINT_FORM_DIRECT) return fail(PINT_ERR_INVALID, "unknown form");
+  if (form == PINT_FORM_DIRECT && c->P > 1) return fail(PINT_ERR_INVALID, "the direct form is single-rank only");
+  c->form = form;
+  return PINT_OK;
 }
 
 pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, double *S, double *Sinv,
@@ -827,7 +869,7 @@ pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s) {
   else if (s == 1) { double2 *x2; CUDA_TRY(c, launch_solve(c->g, c->lc, c->st, at, b, c->stream, &x2)); }
   else if (s == 2) {
     double2 *x2 = (c->g.dim == 1 && c->lc.pcr_mode == 1) ? b.Y : b.X;
-    CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, nullptr, c->stream));
+    CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, nullptr, c->stream, 0));
   } else return fail(PINT_ERR_INVALID, "stage must be 0, 1 or 2");
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PINT_OK;

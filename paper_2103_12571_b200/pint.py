@@ -27,7 +27,9 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_get_final_value", "pint_set_initial_value", "pint_destroy", "pint_last_error",
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
-           "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm"]
+           "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
+           "pint_set_form"]
+FORMS = {"correction": 0, "direct": 1}
 
 
 class PintError(RuntimeError):
@@ -87,6 +89,7 @@ def load_library(path: str = LIB_PATH):
         "pint_local_steps": (i32, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "pint_group_iterate": (i32, [ctypes.POINTER(vp), i32, i32, dp]),
         "pint_group_residual_norm": (i32, [ctypes.POINTER(vp), i32, dp, dp]),
+        "pint_set_form": (i32, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -179,6 +182,10 @@ class Solver:
     def set_alpha_schedule(self, alphas: Sequence[float]):
         a = np.ascontiguousarray(np.asarray(alphas, dtype=np.float64))
         _check(self.lib.pint_set_alpha_schedule(self.ctx, _dp(a), len(a)))
+
+    def set_form(self, form: str):
+        """"correction" (default, u += C_a^{-1}(w - C u)) or "direct" (Alg. 1: u = C_a^{-1}((C_a - C)u + w))."""
+        _check(self.lib.pint_set_form(self.ctx, FORMS[form]))
 
     # -- iteration
     def iterate(self, n: int = 1, want_diff: bool = False):

@@ -1,0 +1,75 @@
+"""GPU parity of the direct form (Alg. 1 as printed, PINT_FORM_DIRECT) against the oracle's
+direct-form iteration (itself pinned to a dense C_a solve, tests/test_oracle_iteration.py)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle.paralpha import ModeOracle, Oracle, mode_coefficients, relative_l2
+from oracle.schedule import adaptive_schedule as oracle_schedule
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def _alphas(p, u0):
+    if p.alpha_mode == "fixed":
+        return [p.alpha_fixed] * p.iters
+    return list(oracle_schedule(p.L, float(np.abs(u0).max()), p.m0, p.iters, p.eps, p.tau)[0])
+
+
+CASES = [W.CONFIGS[1], W.CONFIGS[2], W.reduced(3), W.reduced(4), W.reduced(5),
+         W.CONFIGS[3].replace(name="twopass_N16384_L8", nx=16384, L=8, iters=4)] + W.edge_cases()
+
+
+@pytest.mark.parametrize("p", CASES, ids=lambda p: p.name)
+def test_direct_form_parity(p):
+    import paper_2103_12571_b200 as PB
+    u0 = p.u0()
+    a = _alphas(p, u0)
+    s = PB.Solver(p, u0)
+    s.set_form("direct")
+    s.set_alpha_schedule(a)
+    o = Oracle(p, u0, "dense" if p.M * p.N <= 2048 else "fourier")
+    u = o.initial()
+    for k in range(min(p.iters, 5)):
+        un = o.iterate_direct(u, a[k])
+        d = s.iterate(1, want_diff=True)[0]
+        e = relative_l2(s.get_iterate(), un)
+        assert e <= TOL, (k, e)
+        ref = float(np.abs(un[-1] - u[-1]).max())
+        assert abs(d - ref) <= 1e-4 * ref + 1e-10 * np.abs(un).max()
+        u = un
+    s.close()
+
+
+def test_direct_form_full_size_config5_sampled():
+    import paper_2103_12571_b200 as PB
+    p = W.CONFIGS[5]
+    u0 = p.u0()
+    a = _alphas(p, u0)
+    s = PB.Solver(p, u0)
+    s.set_form("direct")
+    s.set_alpha_schedule(a)
+    rng = np.random.default_rng(5)
+    kx = np.concatenate([np.arange(0, 5).repeat(5), rng.integers(0, p.nx, 8)])
+    ky = np.concatenate([np.tile(np.arange(0, 5), 5), rng.integers(0, p.ny, 8)])
+    mo = ModeOracle(p, mode_coefficients(p, u0, kx, ky), kx, ky)
+    uh = mo.initial()
+    from test_gpu_parity import _gpu_project
+    for k in range(4):
+        uh = mo.iterate_direct(uh, a[k])
+        s.iterate(1)
+        g = _gpu_project(s, p, kx, ky)
+        e = float(np.linalg.norm((g - uh).ravel()) / np.linalg.norm(uh.ravel()))
+        assert e <= TOL, (k, e)
+    s.close()
+
+
+def test_direct_form_refused_when_sharded():
+    import paper_2103_12571_b200 as PB
+    p = W.CONFIGS[2].replace(L=16)
+    grp = PB.Group(p, p.u0(), 2)
+    with pytest.raises(PB.PintError) as e:
+        grp.ranks[0].set_form("direct")
+    assert e.value.status == 1
+    grp.close()

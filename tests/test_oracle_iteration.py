@@ -9,6 +9,7 @@ import pytest
 import workloads as W
 from oracle.collocation import Tableau
 from oracle.paralpha import (E_matrix, ModeOracle, Oracle, V_inverse, V_matrix, brute_force_iterate,
+                             brute_force_iterate_direct,
                              d_values, mode_coefficients, relative_l2, residual, sequential_solution,
                              single_mode_solution, w_vector)
 
@@ -173,3 +174,35 @@ def test_w_vector_layout():
     p = W.CONFIGS[1]
     w = w_vector(p, p.u0())
     assert np.all(w[1:] == 0) and np.all(w[0, 1] == p.u0())
+
+
+@pytest.mark.parametrize("p", TINY, ids=lambda p: p.name)
+def test_direct_form_brute_force_and_equivalence(p):
+    """Alg. 1 as printed (direct form): equals the dense C_a solve of (C_a - C)u + w,
+    and agrees with the correction form (reading R1) up to roundoff."""
+    u0 = p.u0()
+    o = Oracle(p, u0, "dense")
+    u = o.initial()
+    uc = u.copy()
+    for k in range(3):
+        a = p.alpha_fixed * (1 + k)
+        un = o.iterate_direct(u, a)
+        ub = brute_force_iterate_direct(p, o.tab, u, u0, a)
+        assert relative_l2(un, ub) < 1e-11
+        uc = o.iterate(uc, a)
+        assert relative_l2(un, uc) < 1e-9
+        u = un
+
+
+def test_direct_form_mode_tier():
+    p = W.reduced(5).replace(L=8)
+    u0 = p.u0()
+    o = Oracle(p, u0, "fourier")
+    kx = np.array([0, 1, 3, 5])
+    ky = np.array([0, 2, 1, 7])
+    mo = ModeOracle(p, mode_coefficients(p, u0, kx, ky), kx, ky)
+    u, uh = o.initial(), mo.initial()
+    for a in (1e-3, 1e-2):
+        u, uh = o.iterate_direct(u, a), mo.iterate_direct(uh, a)
+        proj = mode_coefficients(p, u, kx, ky)
+        assert np.abs(proj - uh).max() <= 1e-10 * np.abs(uh).max()
