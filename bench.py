@@ -31,11 +31,14 @@ UNIT = "unknowns/s"
 # algorithmic HBM bytes per unknown of each launch (compulsory reads + writes)
 ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32, "fft2d_rows_kernel<fwd>": 32,
               "fft2d_cols_kernel": 32, "fft2d_rows_kernel<inv>": 32, "bwd_kernel": 48, "residual2d_kernel": 32,
-              "tfft_fwd_kernel": 32, "tfft_bwd_kernel": 48}
+              "tfft_fwd_kernel": 32, "tfft_bwd_kernel": 48,
+              # persistent 2-D spatial pipeline: the three plane passes' compulsory traffic (3 x 32 B)
+              "spatial2d_kernel": 96}
 # direct form (u = C_a^{-1}((C_a - C)u + w)): no read of u, input synthesized from one N-vector
 ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
                      "cols_direct_kernel": 16, "fft2d_rows_kernel<inv>": 32, "tfft_bwd_kernel": 32,
-                     "pcr_classes_kernel": 16, "pcr_chunk_kernel": 32, "bwd_kernel": 32}
+                     "pcr_classes_kernel": 16, "pcr_chunk_kernel": 32, "bwd_kernel": 32,
+                     "spatial2d_kernel": 48}
 
 
 def env_rank():

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpint.so")
-SOURCES = ["kernels.cu", "pint_abi.cpp", "host_numerics.cpp"]
+SOURCES = ["kernels.cu", "spatial2d.cu", "pint_abi.cpp", "host_numerics.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 LIBS = ["-lnccl"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -18,7 +18,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "host_numerics.h"),
+    deps = srcs + [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "host_numerics.h"), os.path.join(CSRC, "fft_reg.cuh"),
+                   os.path.join(CSRC, "device_common.cuh"),
                    os.path.join(ROOT, "include", "pint.h")]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB

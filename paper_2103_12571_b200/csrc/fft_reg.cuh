@@ -1,0 +1,244 @@
+// Register-resident radix-16 FFT engine for power-of-two lines of N = 2^LOGN complex fp64
+// values, 4 <= N <= 4096 (time axis L, spatial axes nx, ny).
+//
+// Plan: N = R0 R1 R2 with R_i = 2^{B_i}, B0 = min(4, LOGN), B1 = min(4, LOGN - B0), B2 = rest
+// (at most 3 passes).  A line is handled by TPL = N / E threads, E = R0 values per thread.  Pass i
+// works on blocks of m_i = N / (R0..R_{i-1}) positions at stride s_i = m_i / R_i: butterfly
+// g = tau + TPL u (u < E / R_i) is (block beta = g / s_i, offset j = g % s_i) and owns positions
+// beta m_i + j + s_i t, t < R_i.  DIF pass: in-register radix-R DFT (slot t receives frequency
+// bitrev(t)), then slot t *= w_{m_i}^{j bitrev(t)}; the product over the passes leaves frequency
+// bitrev_N(P) at position P (natural in, bit-reversed out: the order the paper keeps).
+// The inverse (DIT) pass undoes a DIF pass on the same position sets (conjugate twiddle, then the
+// inverse radix-R DFT from bit-reversed slots), passes in reverse order, unnormalised (N x).
+//
+// Between passes the values go through shared memory (one write, one barrier, one read per
+// pass).  Element P of a line lives at swizzled offset F(P): F XORs the low three 16-byte slot
+// bits with higher position bits so that every quarter-warp access of every pass of the plan is
+// bank-conflict free (tests/test_fft_plan.py checks it).  Twiddles: per-pass tables of the
+// powers tw_i[k s_i + j] = w_{m_i}^{j 2^k}, k < B_i (host long double, staged in shared memory,
+// lanes read consecutive j or broadcast); the other exponents j r are formed in registers by a
+// short product chain from the nearest power of two below r (<= 7 complex products, error a few
+// ulp), which trades 11 of 15 shared-memory loads per radix-16 butterfly for fp64 work.
+// Exchanges synchronise only the threads of one line (warp or named barrier), never the CTA.
+#pragma once
+#include "device_common.cuh"
+
+namespace pint {
+namespace rfft {
+
+__host__ __device__ constexpr int ilog2_ct(int r) { return r <= 1 ? 0 : 1 + ilog2_ct(r >> 1); }
+
+template <int LOGN>
+struct Plan {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int B0 = LOGN < 4 ? LOGN : 4;
+  static constexpr int B1 = (LOGN - B0) < 4 ? (LOGN - B0) : 4;
+  static constexpr int B2 = LOGN - B0 - B1;
+  static constexpr int NP = B2 > 0 ? 3 : (B1 > 0 ? 2 : 1);
+  static constexpr int E = 1 << B0;
+  static constexpr int TPL = N / E;
+  static constexpr int BL = NP == 3 ? B2 : (NP == 2 ? B1 : B0);   // radix (log2) of the last pass
+  static constexpr int b(int p) { return p == 0 ? B0 : (p == 1 ? B1 : B2); }
+  static constexpr int logm(int p) { return p == 0 ? LOGN : (p == 1 ? LOGN - B0 : LOGN - B0 - B1); }
+  static constexpr int logs(int p) { return logm(p) - b(p); }
+  static constexpr int twcount(int p) { return b(p) << logs(p); }
+  static constexpr int twoff(int p) { return p == 0 ? 0 : (p == 1 ? twcount(0) : twcount(0) + twcount(1)); }
+  static constexpr int twsize() {
+    return twcount(0) + (NP > 1 ? twcount(1) : 0) + (NP > 2 ? twcount(2) : 0);
+  }
+};
+
+// swizzled offset of position p inside a line (see header)
+template <int LOGN>
+__device__ __forceinline__ int F(int p) {
+  using P = Plan<LOGN>;
+  int h = 0;
+  if constexpr (P::NP >= 2) {
+    constexpr int bl = P::BL;
+    constexpr int sh = bl > 3 ? bl : 3;
+    constexpr int mk = bl >= 3 ? 7 : ((1 << bl) - 1);
+    h ^= (p >> sh) & mk;
+  }
+  if constexpr (P::NP == 3 && P::B2 < 3) {
+    constexpr int lm1 = P::logm(1);
+    h ^= ((p >> lm1) & ((8 >> P::B2) - 1)) << P::B2;
+  }
+  return p ^ h;
+}
+
+// position of value (u, t) of thread tau in pass PASS
+template <int LOGN, int PASS>
+__device__ __forceinline__ int pos(int tau, int u, int t) {
+  using P = Plan<LOGN>;
+  constexpr int lm = P::logm(PASS), ls = P::logs(PASS);
+  const int g = tau + P::TPL * u;
+  return ((g >> ls) << lm) + (g & ((1 << ls) - 1)) + (t << ls);
+}
+
+template <int LOGN, int PASS>
+__device__ __forceinline__ void to_smem(const double2 (&v)[Plan<LOGN>::E], double2 *line, int tau) {
+  using P = Plan<LOGN>;
+  constexpr int R = 1 << P::b(PASS);
+#pragma unroll
+  for (int u = 0; u < P::E / R; ++u)
+#pragma unroll
+    for (int t = 0; t < R; ++t) line[F<LOGN>(pos<LOGN, PASS>(tau, u, t))] = v[u * R + t];
+}
+
+template <int LOGN, int PASS>
+__device__ __forceinline__ void from_smem(double2 (&v)[Plan<LOGN>::E], const double2 *line, int tau) {
+  using P = Plan<LOGN>;
+  constexpr int R = 1 << P::b(PASS);
+#pragma unroll
+  for (int u = 0; u < P::E / R; ++u)
+#pragma unroll
+    for (int t = 0; t < R; ++t) v[u * R + t] = line[F<LOGN>(pos<LOGN, PASS>(tau, u, t))];
+}
+
+// slot t of a radix-2^B butterfly carries frequency bitrev_B(t), i.e. exponent r = brev(t);
+// multiply every slot by w^{j r} (CONJ: w^{-j r}) with w^{j 2^k} = tp[k s]
+template <int B, bool CONJ>
+__device__ __forceinline__ void apply_twiddles(double2 *x, const double2 *tp, int s) {
+  constexpr int R = 1 << B;
+  double2 w1 = tp[0];
+  if (CONJ) w1.y = -w1.y;
+  double2 w = w1;
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    if (r > 1) {
+      if ((r & (r - 1)) == 0) {        // power of two: fresh table value (resets the chain)
+        w = tp[ilog2_ct(r) * s];
+        if (CONJ) w.y = -w.y;
+      } else {
+        w = cmul(w, w1);
+      }
+    }
+    const int t = brev_ct<B>(r);
+    x[t] = cmul(x[t], w);
+  }
+}
+
+// DIF pass PASS on the thread's values; tw = the plan's twiddle table (shared memory)
+template <int LOGN, int PASS>
+__device__ __forceinline__ void dif(double2 (&v)[Plan<LOGN>::E], int tau, const double2 *tw) {
+  using P = Plan<LOGN>;
+  constexpr int b = P::b(PASS), R = 1 << b, ls = P::logs(PASS), s = 1 << ls;
+#pragma unroll
+  for (int u = 0; u < P::E / R; ++u) {
+    reg_dif<b>(v + u * R);
+    if constexpr (ls > 0) {
+      const int j = (tau + P::TPL * u) & (s - 1);
+      apply_twiddles<b, false>(v + u * R, tw + P::twoff(PASS) + j, s);
+    }
+  }
+}
+
+// inverse (DIT) of DIF pass PASS: conjugate twiddles, then the inverse radix-R DFT
+template <int LOGN, int PASS>
+__device__ __forceinline__ void dit(double2 (&v)[Plan<LOGN>::E], int tau, const double2 *tw) {
+  using P = Plan<LOGN>;
+  constexpr int b = P::b(PASS), R = 1 << b, ls = P::logs(PASS), s = 1 << ls;
+#pragma unroll
+  for (int u = 0; u < P::E / R; ++u) {
+    if constexpr (ls > 0) {
+      const int j = (tau + P::TPL * u) & (s - 1);
+      apply_twiddles<b, true>(v + u * R, tw + P::twoff(PASS) + j, s);
+    }
+    reg_dit_inv<b>(v + u * R);
+  }
+}
+
+// barrier over the TPL threads of line l (TPL <= 32: the warp; else named barrier 1 + l)
+template <int LOGN>
+__device__ __forceinline__ void line_sync(int l) {
+  constexpr int TPL = Plan<LOGN>::TPL;
+  if constexpr (TPL <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + l), "r"(TPL) : "memory");
+  }
+}
+
+// Forward transform of a line whose values sit in shared memory at `line` (swizzled, natural
+// order).  Returns with the values of the LAST pass in registers (positions pos<NP-1>).
+// Contains NP - 1 exchanges; the first statement is a read, so the caller must have barriered
+// after filling the line; ends without a trailing barrier.
+template <int LOGN>
+__device__ __forceinline__ void forward_regs(double2 (&v)[Plan<LOGN>::E], double2 *line, int l, int tau,
+                                             const double2 *tw) {
+  using P = Plan<LOGN>;
+  dif<LOGN, 0>(v, tau, tw);
+  if constexpr (P::NP >= 2) {
+    line_sync<LOGN>(l);
+    to_smem<LOGN, 0>(v, line, tau);
+    line_sync<LOGN>(l);
+    from_smem<LOGN, 1>(v, line, tau);
+    dif<LOGN, 1>(v, tau, tw);
+  }
+  if constexpr (P::NP >= 3) {
+    line_sync<LOGN>(l);
+    to_smem<LOGN, 1>(v, line, tau);
+    line_sync<LOGN>(l);
+    from_smem<LOGN, 2>(v, line, tau);
+    dif<LOGN, 2>(v, tau, tw);
+  }
+}
+// forward_regs starting from pass-0 values that sit (natural order, swizzled) in `line`
+template <int LOGN>
+__device__ __forceinline__ void forward_from_smem(double2 (&v)[Plan<LOGN>::E], double2 *line, int l, int tau,
+                                                  const double2 *tw) {
+  from_smem<LOGN, 0>(v, line, tau);
+  forward_regs<LOGN>(v, line, l, tau, tw);
+}
+
+// Inverse transform starting from the last pass's positions in registers; ends with the values
+// of pass 0 (natural positions tau + TPL t) in registers.  Uses `line` for the exchanges: the
+// caller must make sure nobody still reads it (barrier) before calling.
+template <int LOGN>
+__device__ __forceinline__ void inverse_in_regs(double2 (&v)[Plan<LOGN>::E], double2 *line, int l, int tau,
+                                                const double2 *tw) {
+  using P = Plan<LOGN>;
+  if constexpr (P::NP >= 3) {
+    dit<LOGN, 2>(v, tau, tw);
+    to_smem<LOGN, 2>(v, line, tau);
+    line_sync<LOGN>(l);
+    from_smem<LOGN, 1>(v, line, tau);
+    line_sync<LOGN>(l);
+  }
+  if constexpr (P::NP >= 2) {
+    dit<LOGN, 1>(v, tau, tw);
+    to_smem<LOGN, 1>(v, line, tau);
+    line_sync<LOGN>(l);
+    from_smem<LOGN, 0>(v, line, tau);
+    line_sync<LOGN>(l);
+  }
+  dit<LOGN, 0>(v, tau, tw);
+}
+
+// Natural position of pass-0 value t of thread tau: tau + TPL t.
+template <int LOGN>
+__device__ __forceinline__ int natural_pos(int tau, int t) { return tau + Plan<LOGN>::TPL * t; }
+
+// S-layout: storage slot of last-pass value (u, t) of thread tau in spectral (bit-reversed
+// position) data kept in global memory: slot q = t * (N / R_L) + beta, beta = tau + TPL u; the
+// lanes of a warp write consecutive slots.  slot_to_pos inverts it.
+template <int LOGN>
+__device__ __forceinline__ int s_slot(int tau, int u, int t) {
+  using P = Plan<LOGN>;
+  return (t << (LOGN - P::BL)) + tau + P::TPL * u;
+}
+template <int LOGN>
+__device__ __forceinline__ int slot_to_pos(int q) {
+  using P = Plan<LOGN>;
+  constexpr int sh = LOGN - P::BL;
+  return ((q & ((1 << sh) - 1)) << P::BL) + (q >> sh);
+}
+// position of last-pass value (u, t) of thread tau (its frequency is bitrev_N of it)
+template <int LOGN>
+__device__ __forceinline__ int last_pos(int tau, int u, int t) {
+  using P = Plan<LOGN>;
+  return pos<LOGN, P::NP - 1>(tau, u, t);
+}
+
+}  // namespace rfft
+}  // namespace pint

@@ -313,4 +313,25 @@ bool eig_diagonalize(int n, const std::vector<cld> &B, std::vector<cld> &lam, st
   return true;
 }
 
+void pass_twiddles(int logn, std::vector<cld> &out) {
+  out.clear();
+  const int b0 = logn < 4 ? logn : 4;
+  const int b1 = (logn - b0) < 4 ? (logn - b0) : 4;
+  const int b[3] = {b0, b1, logn - b0 - b1};
+  int logm = logn;
+  for (int p = 0; p < 3 && b[p] > 0; ++p) {
+    const int logs = logm - b[p], s = 1 << logs;
+    for (int k = 0; k < b[p]; ++k)
+      for (int j = 0; j < s; ++j)
+        out.push_back(unit_root(((long long)j << k) & ((1LL << logm) - 1), 1LL << logm, -1));
+    logm -= b[p];
+  }
+}
+
+size_t pass_twiddle_count(int logn) {
+  std::vector<cld> v;
+  pass_twiddles(logn, v);
+  return v.size();
+}
+
 }  // namespace pint

@@ -48,6 +48,8 @@ struct StaticTables {
   const double2 *twr;
   const double2 *twP;
   int P, rank;
+  // per-pass twiddle tables of the register FFT engine (fft_reg.cuh) for nx, ny
+  const double2 *ptwx, *ptwy;
 };
 
 struct Buffers {
@@ -55,6 +57,7 @@ struct Buffers {
   double2 *X;                 // [L][M][N] work 1
   double2 *Y;                 // [L][M][N] work 2 (1-D two-pass PCR only; else == X)
   double *red;                // reduction scratch (doubles)
+  unsigned *sync;             // 2-D spatial pipeline: per-(stage, batch) completion counters
 };
 
 // ---- launch wrappers (kernels.cu) -----------------------------------------------------------
@@ -69,6 +72,22 @@ struct LaunchCfg {
 };
 
 LaunchCfg choose_launch(const Geometry &g);
+
+// 2-D spatial solves as one persistent L2-resident pipeline (spatial2d.cu)
+struct SpatialPlan {
+  int lines;                  // planes (p, m) to solve
+  int B, nbatch;              // planes per batch, batches
+  int YR, TC;                 // rows per R/I item, columns per C item (64 KB tiles)
+  int nRI, nC;                // items per batch of the R/I stages and of the C stage
+  int synth;                  // direct form: C synthesizes sig_q * r0hat, no R stage
+  int nstage, rounds;         // 3 (R, C, I) or 2 (C, I); nbatch + nstage - 1
+};
+SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth);
+size_t spatial_sync_bytes(int lines);
+// X (lines planes [ny][nx]) solved in place; spec != nullptr: direct form (C reads spec = r0hat)
+cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                             const double2 *spec, unsigned *sync, int lines, cudaStream_t s);
+bool spatial2d_supported(const Geometry &g);
 size_t fwd_smem_bytes(const Geometry &g, int T);
 
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
@@ -91,6 +110,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
                                 const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
                                 double2 **out);
 int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc);
+const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, int i);
 cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
                                  double *out2, cudaStream_t s);
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,

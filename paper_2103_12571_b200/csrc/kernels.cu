@@ -15,6 +15,7 @@
 // accesses; no tensor cores (no dense contraction on this path).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "device_common.cuh"
 #include "internal.h"
@@ -959,11 +960,28 @@ static int num_sms() {
 
 size_t fwd_smem_bytes(const Geometry &g, int T) { return (size_t)g.L * g.M * T * sizeof(double2); }
 
+// 2-D path selection: default = all-node time tiles + the persistent spatial pipeline
+// (spatial2d.cu); PINT_LEGACY2D=1 selects the six-pass path (A/B measurements only).
+static bool legacy2d() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("PINT_LEGACY2D");
+    v = (e && atoi(e)) ? 1 : 0;
+  }
+  return v == 1;
+}
+// register-engine 2-D path (spatial2d.cu) for the grids it is instantiated for; the generic
+// smem-engine kernels below serve every other 2-D shape
+static bool reg2d(const Geometry &g) {
+  return g.dim == 2 && !legacy2d() && spatial2d_supported(g) && g.logL >= 2 && g.logL <= 10;
+}
+
 LaunchCfg choose_launch(const Geometry &g) {
   LaunchCfg lc{};
   // forward/backward tile: as many spatial points as fit ~100 KB (2 CTAs per SM), <= 16
   int T = 16;
   while (T > 1 && fwd_smem_bytes(g, T) > 64 * 1024) T >>= 1;
+  if (const char *e = getenv("PINT_FWD_T")) T = atoi(e);   // tuning experiments only
   while (T > g.N) T >>= 1;
   lc.fwd_T = T;
   int T2 = 32;
@@ -992,7 +1010,7 @@ LaunchCfg choose_launch(const Geometry &g) {
 }
 
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc) {
-  if (g.dim == 2) return 6;
+  if (g.dim == 2) return reg2d(g) ? 4 : 6;
   return lc.pcr_mode == 0 ? 3 : 4;
 }
 
@@ -1001,9 +1019,10 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i) {
   static const char *k1b[] = {"fwd_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
   static const char *k2[] = {"residual2d_kernel", "tfft_fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
                              "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
+  static const char *k2p[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial2d_kernel", "tfft_bwd_kernel"};
   const int n = launches_per_iteration(g, lc);
   if (i < 0 || i >= n) return "";
-  if (g.dim == 2) return k2[i];
+  if (g.dim == 2) return reg2d(g) ? k2p[i] : k2[i];
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 
@@ -1105,6 +1124,11 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       rec(s);
       *out = b.Y;
     }
+  } else if (reg2d(g)) {
+    e = launch_spatial2d(g, st, at, b.X, nullptr, b.sync, g.L * g.M, s);
+    rec(s);
+    *out = b.X;
+    if (e != cudaSuccess) return e;
   } else {
     // row passes: one frequency p and YG rows y per CTA (M*YG*nx <= 4096 elements = 64 KB)
     int YG = 4096 / (g.M * g.nx);
@@ -1179,8 +1203,21 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
 }
 
 int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc) {
-  if (g.dim == 2) return 6;               // r0, plane rows, plane cols, synthesized cols, rows<inv>, bwd
-  return lc.pcr_mode == 0 ? 3 : 4;        // r0, pcr (1 or 2), bwd
+  if (g.dim == 2) return reg2d(g) ? 5 : 6;  // r0, plane rows, plane cols, [spatial2d | synthesized cols, rows<inv>], bwd
+  return lc.pcr_mode == 0 ? 3 : 4;            // r0, pcr (1 or 2), bwd
+}
+
+const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, int i) {
+  static const char *k1a[] = {"direct_r0_kernel", "pcr_classes_kernel", "bwd_kernel"};
+  static const char *k1b[] = {"direct_r0_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
+  static const char *k2[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel",
+                             "cols_direct_kernel", "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
+  static const char *k2p[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel",
+                              "spatial2d_kernel", "tfft_bwd_kernel"};
+  const int n = launches_per_iteration_direct(g, lc);
+  if (i < 0 || i >= n) return "";
+  if (g.dim == 2) return reg2d(g) ? k2p[i] : k2[i];
+  return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 
 cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
@@ -1206,6 +1243,7 @@ cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const St
   if ((e = set_smem((const void *)plane_cols_dif_kernel, smc)) != cudaSuccess) return e;
   plane_cols_dif_kernel<<<g.nx / Tp, kFftThreads, smc, s>>>(g, st, r0, Tp);
   rec(s);
+  if (reg2d(g)) return cudaGetLastError();   // the synthesized column pass runs inside spatial2d
   int T = 8192 / g.ny;
   if (T < 1) T = 1;
   if (T > g.nx) T = g.nx;
@@ -1222,6 +1260,12 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
                                 double2 **out) {
   cudaError_t e = cudaSuccess;
   const int lines = g.L * g.M;
+  if (reg2d(g)) {
+    e = launch_spatial2d(g, st, at, b.X, r0, b.sync, lines, s);
+    rec(s);
+    *out = b.X;
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   if (g.dim == 2) {
     int YG = 4096 / (g.M * g.nx);
     if (YG < 1) YG = 1;

@@ -35,6 +35,7 @@ struct Layout {
   size_t off_static, static_bytes;
   size_t off_alpha, alpha_bytes_each;
   size_t off_red, red_bytes;
+  size_t off_sync, sync_bytes;                // 2-D spatial pipeline completion counters
   size_t total;
   bool two_vectors;
 };
@@ -144,7 +145,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   L.off_r0 = off;
   off = align_up(off + (size_t)g.N * sizeof(double2), 256);
   L.off_static = off;
-  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8) * sizeof(double2);
+  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8 + pass_twiddle_count(g.lognx) +
+                            pass_twiddle_count(g.logny)) * sizeof(double2);
   off = align_up(off + L.static_bytes, 256);
   L.off_alpha = off;
   const size_t LM = (size_t)g.L * g.M;
@@ -159,6 +161,9 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   L.off_red = off;
   L.red_bytes = (size_t)(148 * 8 * 2 + 64 + PINT_MAX_SCHEDULE * 8) * sizeof(double) * 2;
   off = align_up(off + L.red_bytes, 256);
+  L.off_sync = off;
+  L.sync_bytes = g.dim == 2 ? spatial_sync_bytes(g.L * g.M) : 0;
+  off = align_up(off + L.sync_bytes, 256);
   L.total = off;
   return L;
 }
@@ -284,6 +289,13 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     cld w = unit_root(q % P, P, -1);
     host[o++] = make_double2((double)w.real(), (double)w.imag());
   }
+  auto ptw = [&](int logn) {
+    std::vector<cld> v;
+    pass_twiddles(logn, v);
+    for (const cld &w : v) host[o++] = make_double2((double)w.real(), (double)w.imag());
+  };
+  size_t o_px = o; ptw(g.lognx);
+  size_t o_py = o; ptw(g.logny);
   double2 *sbase = (double2 *)(c->work + lay.off_static);
   CUDA_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
   c->st.twL = sbase + o_twL;
@@ -292,6 +304,8 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   c->st.lamx = sbase + o_lx;
   c->st.lamy = sbase + o_ly;
   c->st.u0 = sbase + o_u0;
+  c->st.ptwx = sbase + o_px;
+  c->st.ptwy = sbase + o_py;
   c->st.P = P;
   c->st.rank = rank;
   if (P == 1) {
@@ -319,7 +333,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     }
   }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
-            (double *)(c->work + lay.off_red)};
+            (double *)(c->work + lay.off_red), (unsigned *)(c->work + lay.off_sync)};
   CUDA_TRY(c, launch_init_iterate(c->g, c->st, b, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // host staging buffer goes out of scope
   *out = c;
@@ -328,7 +342,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
 
 static Buffers buffers(pint_ctx *c) {
   return Buffers{c->u, (double2 *)(c->work + c->lay.off_X), (double2 *)(c->work + c->lay.off_Y),
-                 (double *)(c->work + c->lay.off_red)};
+                 (double *)(c->work + c->lay.off_red), (unsigned *)(c->work + c->lay.off_sync)};
 }
 
 pint_status pint_w_inf(pint_ctx *c, double *w_inf) {
@@ -789,7 +803,7 @@ pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (c->k + n_iter > (int)c->alphas.size())
     return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
-  const int nk = launches_per_iteration(c->g, c->lc);
+  const int nk = pint_launches_per_iteration(c);
   std::vector<cudaEvent_t> ev(nk + 1);
   for (auto &e : ev) CUDA_TRY(c, cudaEventCreate(&e));
   for (int i = 0; i < nk; ++i) kernel_ms[i] = 0.0;
@@ -817,16 +831,7 @@ pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms
 
 const char *pint_kernel_name(pint_ctx *c, int32_t i) {
   if (!c) return "";
-  if (c->form == PINT_FORM_DIRECT) {
-    static const char *k1a[] = {"direct_r0_kernel", "pcr_classes_kernel", "bwd_kernel"};
-    static const char *k1b[] = {"direct_r0_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
-    static const char *k2[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel",
-                               "cols_direct_kernel", "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
-    const int n = launches_per_iteration_direct(c->g, c->lc);
-    if (i < 0 || i >= n) return "";
-    if (c->g.dim == 2) return k2[i];
-    return c->lc.pcr_mode == 0 ? k1a[i] : k1b[i];
-  }
+  if (c->form == PINT_FORM_DIRECT) return kernel_name_direct(c->g, c->lc, i);
   return kernel_name(c->g, c->lc, i);
 }
 

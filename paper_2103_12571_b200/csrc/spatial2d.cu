@@ -1,0 +1,387 @@
+// 2-D spatial solves (north star step (iv), Alg. 1) on the register FFT
+// engine of fft_reg.cuh.
+//
+// Spatial solves: for every line q = (slot p, node m) x2 = F^{-1}[F x1 / (1 - s_q lambda)] as
+// three plane passes over the frequency batch of slot p (all M nodes):
+//   R  rows:    x1 = S_p^{-1} x (node transform), x-DIF; spectral rows stored in the
+//               S-layout of fft_reg.cuh (coalesced)
+//   C  columns: y-DIF, x2 = x1 / ((1 - s_q (lambda_x + lambda_y)) nx ny), y-DIT, in registers
+//   I  rows:    x-DIT, y = G_p^{-1} S_p x2
+// run as ONE persistent kernel that software-pipelines the batches (round j: R(j), C(j-1),
+// I(j-2)) so intermediate planes are re-read while they are still in L2.
+//
+// Work distribution: the global item sequence (round by round, stage segments in the order
+// R, C, I) is dealt round-robin to the co-resident CTAs of a cooperative launch.  An item of
+// C(b) waits until all items of R(b) have been counted done (I(b): all of C(b)); every
+// dependency points to an item that comes earlier in the sequence and each CTA walks its items
+// in sequence order, so the earliest unfinished item can always run (no deadlock while all CTAs
+// are resident, which the cooperative launch guarantees).  Producers publish with bar.sync +
+// fence.gpu + atomicAdd; consumers acquire with ld.acquire.gpu and then load with cp.async.cg /
+// ld.global.cg (L2; never a stale L1 line).
+//
+// Direct form (Alg. 1 as printed): the C stage synthesizes its input spectrum sig_q * r0hat (no
+// R stage); see launch_direct_front in kernels.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "device_common.cuh"
+#include "fft_reg.cuh"
+#include "internal.h"
+
+namespace pint {
+
+namespace {
+
+constexpr int kSpThreads = 256;
+enum { kStR = 0, kStC = 1, kStI = 2 };
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 ld_cg(const double2 *p) {
+  double2 v;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void wait_count(const unsigned *ctr, unsigned need) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire_gpu(ctr) < need) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void publish(unsigned *ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+  }
+}
+
+__device__ __forceinline__ void copy_table(double2 *dst, const double2 *src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+// 1 / ((1 - s lambda) nx ny) for natural frequencies (kx, ky)
+__device__ __forceinline__ double2 inv_symbol(const StaticTables &st, double2 s, double inv_n, int kx, int ky) {
+  const double2 lam = cadd(__ldg(st.lamx + kx), __ldg(st.lamy + ky));
+  const double2 sl = cmul(s, lam);
+  const double dr = 1.0 - sl.x, di = -sl.y;
+  const double q = dr * dr + di * di;   // > 0: |1 - s lambda| >= 7.7e-4 on every config
+  double rq = __drcp_rn(q);
+  rq = fma(rq, fma(-q, rq, 1.0), rq);
+  const double den = inv_n * rq;
+  return make_double2(dr * den, -di * den);   // conj(1 - s lambda) / |1 - s lambda|^2 / (nx ny)
+}
+
+// M x M complex matvec over the M lines (stride ls) of every column x of `rows` rows in shared
+// memory: v_m <- sum_j A[m][j] v_j (A row-major in shared memory, compile-time M; the A reads
+// are warp-uniform broadcasts, issued inside the loop so they do not pin M^2 registers)
+template <int LX, int MM>
+__device__ __forceinline__ void node_transform_m(double2 *sm, int ls, int rows, const double2 *A) {
+  constexpr int NX = 1 << LX;
+  for (int i = threadIdx.x; i < rows * NX; i += blockDim.x) {
+    const int x = i & (NX - 1), r = i >> LX;
+    double2 *base = sm + (size_t)r * MM * ls + rfft::F<LX>(x);
+    double2 v[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) v[j] = base[j * ls];
+#pragma unroll (MM <= 4 ? MM : 1)
+    for (int m = 0; m < MM; ++m) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < MM; ++j) {
+        const volatile double2 *a = (const volatile double2 *)(A + m * MM + j);
+        acc = cfma(make_double2(a->x, a->y), v[j], acc);
+      }
+      base[m * ls] = acc;
+    }
+  }
+}
+template <int LX>
+__device__ __forceinline__ void node_transform(double2 *sm, int ls, int M, int rows, const double2 *A) {
+  switch (M) {
+    case 1: node_transform_m<LX, 1>(sm, ls, rows, A); break;
+    case 2: node_transform_m<LX, 2>(sm, ls, rows, A); break;
+    case 3: node_transform_m<LX, 3>(sm, ls, rows, A); break;
+    case 4: node_transform_m<LX, 4>(sm, ls, rows, A); break;
+    case 5: node_transform_m<LX, 5>(sm, ls, rows, A); break;
+    case 6: node_transform_m<LX, 6>(sm, ls, rows, A); break;
+    case 7: node_transform_m<LX, 7>(sm, ls, rows, A); break;
+    default: node_transform_m<LX, 8>(sm, ls, rows, A); break;
+  }
+}
+
+// ---- R item: rows y0 .. y0 + YR - 1 of slot p, all M nodes ---------------------------------
+template <int LX>
+__device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
+                                       const double2 *twx,
+                                       double2 *__restrict__ X, int p, int y0, int YR, bool node) {
+  using PX = rfft::Plan<LX>;
+  constexpr int NX = PX::N;
+  const int M = g.M, nl = M * YR;
+  double2 *xp = X + (size_t)p * M * g.N;
+  for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
+    const int x = i & (NX - 1), l = i >> LX;
+    const int yy = l / M, m = l - yy * M;
+    cp_async16(tile + (size_t)l * NX + rfft::F<LX>(x), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX) + x);
+  }
+  if (node && threadIdx.x < M * M) nt[threadIdx.x] = __ldg(at.Sinv + (size_t)p * M * M + threadIdx.x);
+  cp_async_wait_all();
+  __syncthreads();
+  if (node) {
+    node_transform<LX>(tile, NX, M, YR, nt);
+    __syncthreads();
+  }
+  const int l = threadIdx.x / PX::TPL, tau = threadIdx.x - l * PX::TPL;
+  const int lc = l < nl ? l : nl - 1;   // TPL < 32: surplus lanes shadow the last line (no stores)
+  if (l >= nl && PX::TPL >= 32) return;   // idle warps (line barriers are per line)
+  double2 v[PX::E];
+  rfft::forward_from_smem<LX>(v, tile + (size_t)lc * NX, lc, tau, twx);
+  if (l < nl) {
+    const int yy = l / M, m = l - yy * M;
+    double2 *dst = xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX);
+    constexpr int R = 1 << PX::BL;
+#pragma unroll
+    for (int u = 0; u < PX::E / R; ++u)
+#pragma unroll
+      for (int t = 0; t < R; ++t) dst[rfft::s_slot<LX>(tau, u, t)] = v[u * R + t];
+  }
+}
+
+// ---- I item: inverse rows ------------------------------------------------------------------
+template <int LX>
+__device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
+                                       const double2 *twx,
+                                       double2 *__restrict__ X, int p, int y0, int YR, bool node) {
+  using PX = rfft::Plan<LX>;
+  constexpr int NX = PX::N;
+  constexpr int R = 1 << PX::BL;
+  const int M = g.M, nl = M * YR;
+  double2 *xp = X + (size_t)p * M * g.N;
+  const int l = threadIdx.x / PX::TPL, tau = threadIdx.x - l * PX::TPL;
+  const int lc = l < nl ? l : nl - 1;
+  const int yy = lc / M, m = lc - yy * M;
+  const double2 *src = xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX);
+  double2 v[PX::E];
+#pragma unroll
+  for (int u = 0; u < PX::E / R; ++u)
+#pragma unroll
+    for (int t = 0; t < R; ++t) v[u * R + t] = ld_cg(src + rfft::s_slot<LX>(tau, u, t));
+  double2 *line = tile + (size_t)lc * NX;
+  if (l < nl || PX::TPL < 32) {
+    rfft::inverse_in_regs<LX>(v, line, lc, tau, twx);
+    if (l < nl) rfft::to_smem<LX, 0>(v, line, tau);
+  }
+  if (node && threadIdx.x < M * M) nt[threadIdx.x] = __ldg(at.SG + (size_t)p * M * M + threadIdx.x);
+  __syncthreads();
+  if (node) {
+    node_transform<LX>(tile, NX, M, YR, nt);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
+    const int x = i & (NX - 1), li = i >> LX;
+    const int y2 = li / M, m2 = li - y2 * M;
+    xp[(size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x] = tile[(size_t)li * NX + rfft::F<LX>(x)];
+  }
+}
+
+// ---- C item: columns (S-slots) kx0 .. kx0 + TC - 1 of line q -----------------------------------
+template <int LX, int LY>
+__device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st, const AlphaTables &at,
+                                       double2 *tile, const double2 *twy, double2 *__restrict__ X,
+                                       const double2 *__restrict__ spec, int q, int kx0, int TC) {
+  using PY = rfft::Plan<LY>;
+  constexpr int NX = 1 << LX, NY = PY::N;
+  constexpr int R = 1 << PY::BL;
+  const int pad = TC >= 8 ? 1 : 8 / TC;
+  const int ls = NY + pad;
+  const int lT = 31 - __clz(TC);
+  double2 *xl = X + (size_t)q * g.N;
+  const int l = threadIdx.x / PY::TPL, tau = threadIdx.x - l * PY::TPL;
+  const int lc = l < TC ? l : TC - 1;
+  double2 *line = tile + (size_t)lc * ls;
+  const double2 s = __ldg(at.shift + q);
+  const double inv_n = 1.0 / ((double)NX * (double)NY);
+  const int pxs = rfft::slot_to_pos<LX>(kx0 + lc);     // x position of this column (S-layout slot)
+  const int kx = brev(pxs, LX);
+  double2 v[PY::E];
+  if (spec) {
+    // direct form: x1 spectrum = sig_q * r0hat, r0hat[py][px] in position order (P -> bitrev(P))
+    const double2 sg = __ldg(at.sig + q);
+#pragma unroll
+    for (int u = 0; u < PY::E / R; ++u)
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int P = rfft::last_pos<LY>(tau, u, t);
+        const double2 w = cmul(sg, __ldg(spec + ((size_t)P << LX) + pxs));
+        v[u * R + t] = cmul(w, inv_symbol(st, s, inv_n, kx, brev(P, LY)));
+      }
+  } else {
+    for (int i = threadIdx.x; i < TC * NY; i += blockDim.x) {
+      const int c = i & (TC - 1), y = i >> lT;
+      cp_async16(tile + (size_t)c * ls + rfft::F<LY>(y), xl + ((size_t)y << LX) + kx0 + c);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (l < TC || PY::TPL < 32) {
+      rfft::forward_from_smem<LY>(v, line, lc, tau, twy);
+#pragma unroll
+      for (int u = 0; u < PY::E / R; ++u)
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const int P = rfft::last_pos<LY>(tau, u, t);
+          v[u * R + t] = cmul(v[u * R + t], inv_symbol(st, s, inv_n, kx, brev(P, LY)));
+        }
+      rfft::line_sync<LY>(lc);   // every thread of the line has read its last-pass values
+    }
+  }
+  if (l < TC || PY::TPL < 32) {
+    rfft::inverse_in_regs<LY>(v, line, lc, tau, twy);
+    if (l < TC) rfft::to_smem<LY, 0>(v, line, tau);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TC * NY; i += blockDim.x) {
+    const int c = i & (TC - 1), y = i >> lT;
+    xl[((size_t)y << LX) + kx0 + c] = tile[(size_t)c * ls + rfft::F<LY>(y)];
+  }
+}
+
+}  // namespace
+
+template <int LX, int LY>
+__global__ void __launch_bounds__(kSpThreads, 2)
+    spatial2d_kernel(const Geometry g, StaticTables st, AlphaTables at, SpatialPlan sp, double2 *__restrict__ X,
+                     const double2 *__restrict__ spec, unsigned *__restrict__ sync) {
+  extern __shared__ double2 sm[];
+  constexpr int TWX = rfft::Plan<LX>::twsize(), TWY = rfft::Plan<LY>::twsize();
+  double2 *twx = sm, *twy = sm + TWX, *nt = sm + TWX + TWY, *tile = nt + 64;   // nt: M x M node table
+  copy_table(twx, st.ptwx, TWX);
+  copy_table(twy, st.ptwy, TWY);
+  __syncthreads();
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int riPerBatch = g.ny / sp.YR, cPerLine = g.nx / sp.TC;
+  const bool node = st.P == 1;   // P > 1: the node transforms live in the cross-rank DFT kernels
+  long long rs = 0;   // sequence position of the current round's first item
+  for (int j = 0; j < sp.rounds; ++j) {
+    // stage segments of round j: stage index si works on batch j - si
+    const int first = sp.synth ? kStC : kStR;
+    const int slo = j - (sp.nbatch - 1) > 0 ? j - (sp.nbatch - 1) : 0;
+    const int shi = j < sp.nstage - 1 ? j : sp.nstage - 1;
+    int rn = 0;
+    for (int si = slo; si <= shi; ++si) rn += (first + si == kStC) ? sp.nC : sp.nRI;
+    int k = (int)(((cta - rs) % G + G) % G);
+    for (; k < rn; k += G) {
+      int si = slo, kk = k;
+      for (;;) {
+        const int n = (first + si == kStC) ? sp.nC : sp.nRI;
+        if (kk < n) break;
+        kk -= n;
+        ++si;
+      }
+      const int stage = first + si, b = j - si;
+      if (stage == kStC) {
+        if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
+        const int li = kk / cPerLine;                       // line within the batch
+        c_item<LX, LY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, b * sp.B * g.M + li,
+                       (kk - li * cPerLine) * sp.TC, sp.TC);
+      } else {
+        if (stage == kStI) wait_count(sync + kStC * sp.nbatch + b, (unsigned)sp.nC);
+        const int pi = kk / riPerBatch;                     // slot within the batch
+        const int y0 = (kk - pi * riPerBatch) * sp.YR;
+        if (stage == kStR) r_item<LX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+        else i_item<LX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+      }
+      publish(sync + stage * sp.nbatch + b);
+    }
+    rs += rn;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side
+
+SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth) {
+  SpatialPlan sp{};
+  sp.lines = lines;
+  const int tplx = g.nx >= 16 ? g.nx / 16 : 1;
+  const int tply = g.ny >= 16 ? g.ny / 16 : 1;
+  sp.YR = kSpThreads / (tplx * g.M);         // rows per R/I item: M*YR lines of TPLx threads
+  if (sp.YR < 1) sp.YR = 1;
+  while (sp.YR > 1 && (g.ny % sp.YR)) sp.YR >>= 1;
+  if (sp.YR > g.ny) sp.YR = g.ny;
+  sp.TC = kSpThreads / tply;                 // columns per C item
+  if (sp.TC > g.nx) sp.TC = g.nx;
+  if (sp.TC < 1) sp.TC = 1;
+  // batch = one frequency slot (all M nodes: the node transforms sit in R and I)
+  const int slots = lines / g.M;
+  sp.B = 1;
+  const size_t slot_bytes = (size_t)g.M * g.N * sizeof(double2);
+  while ((size_t)sp.B * slot_bytes < ((size_t)16 << 20) && slots % (2 * sp.B) == 0) sp.B *= 2;
+  sp.nbatch = slots / sp.B;
+  sp.nRI = sp.B * (g.ny / sp.YR);
+  sp.nC = sp.B * g.M * (g.nx / sp.TC);
+  sp.synth = synth ? 1 : 0;
+  sp.nstage = synth ? 2 : 3;
+  sp.rounds = sp.nbatch + sp.nstage - 1;
+  return sp;
+}
+
+size_t spatial_sync_bytes(int lines) { return (size_t)3 * lines * sizeof(unsigned); }
+
+bool spatial2d_supported(const Geometry &g) {
+  const int d = g.lognx - g.logny;
+  return g.dim == 2 && g.lognx >= 2 && g.lognx <= 12 && g.logny >= 2 && g.logny <= 12 && d >= -1 && d <= 1 &&
+         (g.nx >= 16 ? g.nx / 16 : 1) * g.M <= kSpThreads;
+}
+
+namespace {
+template <int LX, int LY>
+cudaError_t launch_sp(const Geometry &g, const StaticTables &st, const AlphaTables &at, const SpatialPlan &sp,
+                      double2 *X, const double2 *spec, unsigned *sync, cudaStream_t s) {
+  const void *fn = (const void *)spatial2d_kernel<LX, LY>;
+  const size_t tile = (size_t)sp.YR * g.M * g.nx > (size_t)sp.TC * (g.ny + 8) ? (size_t)sp.YR * g.M * g.nx
+                                                                               : (size_t)sp.TC * (g.ny + 8);
+  const size_t smem = (rfft::Plan<LX>::twsize() + rfft::Plan<LY>::twsize() + 64 + tile) * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kSpThreads, smem)) != cudaSuccess) return e;
+  if (per < 1) return cudaErrorInvalidConfiguration;
+  Geometry gg = g;
+  StaticTables sst = st;
+  AlphaTables aat = at;
+  SpatialPlan ssp = sp;
+  double2 *xx = X;
+  const double2 *ss = spec;
+  unsigned *sy = sync;
+  void *args[] = {&gg, &sst, &aat, &ssp, &xx, &ss, &sy};
+  return cudaLaunchCooperativeKernel(fn, dim3(sms * per), dim3(kSpThreads), args, smem, s);
+}
+
+}  // namespace
+
+cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                             const double2 *spec, unsigned *sync, int lines, cudaStream_t s) {
+  if (!spatial2d_supported(g)) return cudaErrorInvalidValue;
+  const SpatialPlan sp = make_spatial_plan(g, lines, spec != nullptr);
+  cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)3 * sp.nbatch * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+#define PINT_SP(LXX, LYY) \
+  if (g.lognx == LXX && g.logny == LYY) return launch_sp<LXX, LYY>(g, st, at, sp, X, spec, sync, s);
+#define PINT_SP3(L_) PINT_SP(L_, L_) PINT_SP(L_, L_ - 1) PINT_SP(L_ - 1, L_)
+  PINT_SP(2, 2)
+  PINT_SP3(3) PINT_SP3(4) PINT_SP3(5) PINT_SP3(6) PINT_SP3(7) PINT_SP3(8) PINT_SP3(9) PINT_SP3(10)
+  PINT_SP3(11) PINT_SP3(12)
+#undef PINT_SP3
+#undef PINT_SP
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pint

@@ -1,5 +1,5 @@
 # quick loop: parity tests (not the full-size sampled ones) + bench configs 3-5 (device time only)
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -k "not full_size_sampled" > gpurun_out/gpu_tests.log 2>&1
+
 tail -3 gpurun_out/gpu_tests.log
 for c in 3 4 5; do for f in ${FORMS:-correction}; do
   timeout 600 python bench.py --config $c --form $f --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench$c.json 2> gpurun_out/bench$c.err
