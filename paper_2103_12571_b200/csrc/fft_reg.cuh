@@ -28,12 +28,14 @@ namespace rfft {
 
 __host__ __device__ constexpr int ilog2_ct(int r) { return r <= 1 ? 0 : 1 + ilog2_ct(r >> 1); }
 
-template <int LOGN>
+template <int LOGN_, int MAXB = 4>
 struct Plan {
+  static constexpr int LOGN = LOGN_;
   static constexpr int N = 1 << LOGN;
-  static constexpr int B0 = LOGN < 4 ? LOGN : 4;
-  static constexpr int B1 = (LOGN - B0) < 4 ? (LOGN - B0) : 4;
+  static constexpr int B0 = LOGN < MAXB ? LOGN : MAXB;
+  static constexpr int B1 = (LOGN - B0) < MAXB ? (LOGN - B0) : MAXB;
   static constexpr int B2 = LOGN - B0 - B1;
+  static_assert(B2 <= MAXB, "plan needs more than three passes");
   static constexpr int NP = B2 > 0 ? 3 : (B1 > 0 ? 2 : 1);
   static constexpr int E = 1 << B0;
   static constexpr int TPL = N / E;
@@ -49,9 +51,8 @@ struct Plan {
 };
 
 // swizzled offset of position p inside a line (see header)
-template <int LOGN>
+template <class P>
 __device__ __forceinline__ int F(int p) {
-  using P = Plan<LOGN>;
   int h = 0;
   if constexpr (P::NP >= 2) {
     constexpr int bl = P::BL;
@@ -67,32 +68,29 @@ __device__ __forceinline__ int F(int p) {
 }
 
 // position of value (u, t) of thread tau in pass PASS
-template <int LOGN, int PASS>
+template <class P, int PASS>
 __device__ __forceinline__ int pos(int tau, int u, int t) {
-  using P = Plan<LOGN>;
   constexpr int lm = P::logm(PASS), ls = P::logs(PASS);
   const int g = tau + P::TPL * u;
   return ((g >> ls) << lm) + (g & ((1 << ls) - 1)) + (t << ls);
 }
 
-template <int LOGN, int PASS>
-__device__ __forceinline__ void to_smem(const double2 (&v)[Plan<LOGN>::E], double2 *line, int tau) {
-  using P = Plan<LOGN>;
+template <class P, int PASS>
+__device__ __forceinline__ void to_smem(const double2 (&v)[P::E], double2 *line, int tau) {
   constexpr int R = 1 << P::b(PASS);
 #pragma unroll
   for (int u = 0; u < P::E / R; ++u)
 #pragma unroll
-    for (int t = 0; t < R; ++t) line[F<LOGN>(pos<LOGN, PASS>(tau, u, t))] = v[u * R + t];
+    for (int t = 0; t < R; ++t) line[F<P>(pos<P, PASS>(tau, u, t))] = v[u * R + t];
 }
 
-template <int LOGN, int PASS>
-__device__ __forceinline__ void from_smem(double2 (&v)[Plan<LOGN>::E], const double2 *line, int tau) {
-  using P = Plan<LOGN>;
+template <class P, int PASS>
+__device__ __forceinline__ void from_smem(double2 (&v)[P::E], const double2 *line, int tau) {
   constexpr int R = 1 << P::b(PASS);
 #pragma unroll
   for (int u = 0; u < P::E / R; ++u)
 #pragma unroll
-    for (int t = 0; t < R; ++t) v[u * R + t] = line[F<LOGN>(pos<LOGN, PASS>(tau, u, t))];
+    for (int t = 0; t < R; ++t) v[u * R + t] = line[F<P>(pos<P, PASS>(tau, u, t))];
 }
 
 // slot t of a radix-2^B butterfly carries frequency bitrev_B(t), i.e. exponent r = brev(t);
@@ -119,9 +117,8 @@ __device__ __forceinline__ void apply_twiddles(double2 *x, const double2 *tp, in
 }
 
 // DIF pass PASS on the thread's values; tw = the plan's twiddle table (shared memory)
-template <int LOGN, int PASS>
-__device__ __forceinline__ void dif(double2 (&v)[Plan<LOGN>::E], int tau, const double2 *tw) {
-  using P = Plan<LOGN>;
+template <class P, int PASS>
+__device__ __forceinline__ void dif(double2 (&v)[P::E], int tau, const double2 *tw) {
   constexpr int b = P::b(PASS), R = 1 << b, ls = P::logs(PASS), s = 1 << ls;
 #pragma unroll
   for (int u = 0; u < P::E / R; ++u) {
@@ -134,9 +131,8 @@ __device__ __forceinline__ void dif(double2 (&v)[Plan<LOGN>::E], int tau, const 
 }
 
 // inverse (DIT) of DIF pass PASS: conjugate twiddles, then the inverse radix-R DFT
-template <int LOGN, int PASS>
-__device__ __forceinline__ void dit(double2 (&v)[Plan<LOGN>::E], int tau, const double2 *tw) {
-  using P = Plan<LOGN>;
+template <class P, int PASS>
+__device__ __forceinline__ void dit(double2 (&v)[P::E], int tau, const double2 *tw) {
   constexpr int b = P::b(PASS), R = 1 << b, ls = P::logs(PASS), s = 1 << ls;
 #pragma unroll
   for (int u = 0; u < P::E / R; ++u) {
@@ -149,9 +145,9 @@ __device__ __forceinline__ void dit(double2 (&v)[Plan<LOGN>::E], int tau, const 
 }
 
 // barrier over the TPL threads of line l (TPL <= 32: the warp; else named barrier 1 + l)
-template <int LOGN>
+template <class P>
 __device__ __forceinline__ void line_sync(int l) {
-  constexpr int TPL = Plan<LOGN>::TPL;
+  constexpr int TPL = P::TPL;
   if constexpr (TPL <= 32) {
     __syncwarp();
   } else {
@@ -163,81 +159,76 @@ __device__ __forceinline__ void line_sync(int l) {
 // order).  Returns with the values of the LAST pass in registers (positions pos<NP-1>).
 // Contains NP - 1 exchanges; the first statement is a read, so the caller must have barriered
 // after filling the line; ends without a trailing barrier.
-template <int LOGN>
-__device__ __forceinline__ void forward_regs(double2 (&v)[Plan<LOGN>::E], double2 *line, int l, int tau,
+template <class P>
+__device__ __forceinline__ void forward_regs(double2 (&v)[P::E], double2 *line, int l, int tau,
                                              const double2 *tw) {
-  using P = Plan<LOGN>;
-  dif<LOGN, 0>(v, tau, tw);
+  dif<P, 0>(v, tau, tw);
   if constexpr (P::NP >= 2) {
-    line_sync<LOGN>(l);
-    to_smem<LOGN, 0>(v, line, tau);
-    line_sync<LOGN>(l);
-    from_smem<LOGN, 1>(v, line, tau);
-    dif<LOGN, 1>(v, tau, tw);
+    line_sync<P>(l);
+    to_smem<P, 0>(v, line, tau);
+    line_sync<P>(l);
+    from_smem<P, 1>(v, line, tau);
+    dif<P, 1>(v, tau, tw);
   }
   if constexpr (P::NP >= 3) {
-    line_sync<LOGN>(l);
-    to_smem<LOGN, 1>(v, line, tau);
-    line_sync<LOGN>(l);
-    from_smem<LOGN, 2>(v, line, tau);
-    dif<LOGN, 2>(v, tau, tw);
+    line_sync<P>(l);
+    to_smem<P, 1>(v, line, tau);
+    line_sync<P>(l);
+    from_smem<P, 2>(v, line, tau);
+    dif<P, 2>(v, tau, tw);
   }
 }
 // forward_regs starting from pass-0 values that sit (natural order, swizzled) in `line`
-template <int LOGN>
-__device__ __forceinline__ void forward_from_smem(double2 (&v)[Plan<LOGN>::E], double2 *line, int l, int tau,
+template <class P>
+__device__ __forceinline__ void forward_from_smem(double2 (&v)[P::E], double2 *line, int l, int tau,
                                                   const double2 *tw) {
-  from_smem<LOGN, 0>(v, line, tau);
-  forward_regs<LOGN>(v, line, l, tau, tw);
+  from_smem<P, 0>(v, line, tau);
+  forward_regs<P>(v, line, l, tau, tw);
 }
 
 // Inverse transform starting from the last pass's positions in registers; ends with the values
 // of pass 0 (natural positions tau + TPL t) in registers.  Uses `line` for the exchanges: the
 // caller must make sure nobody still reads it (barrier) before calling.
-template <int LOGN>
-__device__ __forceinline__ void inverse_in_regs(double2 (&v)[Plan<LOGN>::E], double2 *line, int l, int tau,
+template <class P>
+__device__ __forceinline__ void inverse_in_regs(double2 (&v)[P::E], double2 *line, int l, int tau,
                                                 const double2 *tw) {
-  using P = Plan<LOGN>;
   if constexpr (P::NP >= 3) {
-    dit<LOGN, 2>(v, tau, tw);
-    to_smem<LOGN, 2>(v, line, tau);
-    line_sync<LOGN>(l);
-    from_smem<LOGN, 1>(v, line, tau);
-    line_sync<LOGN>(l);
+    dit<P, 2>(v, tau, tw);
+    to_smem<P, 2>(v, line, tau);
+    line_sync<P>(l);
+    from_smem<P, 1>(v, line, tau);
+    line_sync<P>(l);
   }
   if constexpr (P::NP >= 2) {
-    dit<LOGN, 1>(v, tau, tw);
-    to_smem<LOGN, 1>(v, line, tau);
-    line_sync<LOGN>(l);
-    from_smem<LOGN, 0>(v, line, tau);
-    line_sync<LOGN>(l);
+    dit<P, 1>(v, tau, tw);
+    to_smem<P, 1>(v, line, tau);
+    line_sync<P>(l);
+    from_smem<P, 0>(v, line, tau);
+    line_sync<P>(l);
   }
-  dit<LOGN, 0>(v, tau, tw);
+  dit<P, 0>(v, tau, tw);
 }
 
 // Natural position of pass-0 value t of thread tau: tau + TPL t.
-template <int LOGN>
-__device__ __forceinline__ int natural_pos(int tau, int t) { return tau + Plan<LOGN>::TPL * t; }
+template <class P>
+__device__ __forceinline__ int natural_pos(int tau, int t) { return tau + P::TPL * t; }
 
 // S-layout: storage slot of last-pass value (u, t) of thread tau in spectral (bit-reversed
 // position) data kept in global memory: slot q = t * (N / R_L) + beta, beta = tau + TPL u; the
 // lanes of a warp write consecutive slots.  slot_to_pos inverts it.
-template <int LOGN>
+template <class P>
 __device__ __forceinline__ int s_slot(int tau, int u, int t) {
-  using P = Plan<LOGN>;
-  return (t << (LOGN - P::BL)) + tau + P::TPL * u;
+  return (t << (P::LOGN - P::BL)) + tau + P::TPL * u;
 }
-template <int LOGN>
+template <class P>
 __device__ __forceinline__ int slot_to_pos(int q) {
-  using P = Plan<LOGN>;
-  constexpr int sh = LOGN - P::BL;
+  constexpr int sh = P::LOGN - P::BL;
   return ((q & ((1 << sh) - 1)) << P::BL) + (q >> sh);
 }
 // position of last-pass value (u, t) of thread tau (its frequency is bitrev_N of it)
-template <int LOGN>
+template <class P>
 __device__ __forceinline__ int last_pos(int tau, int u, int t) {
-  using P = Plan<LOGN>;
-  return pos<LOGN, P::NP - 1>(tau, u, t);
+  return pos<P, P::NP - 1>(tau, u, t);
 }
 
 }  // namespace rfft

@@ -313,10 +313,10 @@ bool eig_diagonalize(int n, const std::vector<cld> &B, std::vector<cld> &lam, st
   return true;
 }
 
-void pass_twiddles(int logn, std::vector<cld> &out) {
+void pass_twiddles(int logn, int maxb, std::vector<cld> &out) {
   out.clear();
-  const int b0 = logn < 4 ? logn : 4;
-  const int b1 = (logn - b0) < 4 ? (logn - b0) : 4;
+  const int b0 = logn < maxb ? logn : maxb;
+  const int b1 = (logn - b0) < maxb ? (logn - b0) : maxb;
   const int b[3] = {b0, b1, logn - b0 - b1};
   int logm = logn;
   for (int p = 0; p < 3 && b[p] > 0; ++p) {
@@ -328,9 +328,9 @@ void pass_twiddles(int logn, std::vector<cld> &out) {
   }
 }
 
-size_t pass_twiddle_count(int logn) {
+size_t pass_twiddle_count(int logn, int maxb) {
   std::vector<cld> v;
-  pass_twiddles(logn, v);
+  pass_twiddles(logn, maxb, v);
   return v.size();
 }
 

@@ -39,9 +39,9 @@ inline int bitrev(int x, int bits) {
 cld unit_root(long long q, long long n, int sign);
 
 // Per-pass twiddle tables of the register FFT plan of fft_reg.cuh for N = 2^logn: passes of
-// radix 2^b (b0 = min(4, logn), b1 = min(4, logn - b0), b2 = rest), pass p over blocks of m_p at
+// radix 2^b (b0 = min(B, logn), b1 = min(B, logn - b0), b2 = rest; B = maxb), pass p over blocks of m_p at
 // stride s_p = m_p / 2^b_p; entry k s_p + j = e^{-2 pi i j 2^k / m_p}, k < b_p.
-void pass_twiddles(int logn, std::vector<cld> &out);
-size_t pass_twiddle_count(int logn);
+void pass_twiddles(int logn, int maxb, std::vector<cld> &out);
+size_t pass_twiddle_count(int logn, int maxb);
 
 }  // namespace pint

@@ -83,6 +83,7 @@ struct SpatialPlan {
   int nstage, rounds;         // 3 (R, C, I) or 2 (C, I); nbatch + nstage - 1
 };
 SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth);
+int spatial_maxb(const Geometry &g);   // largest radix (log2) of the spatial FFT plan in use
 size_t spatial_sync_bytes(int lines);
 // X (lines planes [ny][nx]) solved in place; spec != nullptr: direct form (C reads spec = r0hat)
 cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,

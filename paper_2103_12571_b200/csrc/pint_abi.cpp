@@ -145,8 +145,9 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   L.off_r0 = off;
   off = align_up(off + (size_t)g.N * sizeof(double2), 256);
   L.off_static = off;
-  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8 + pass_twiddle_count(g.lognx) +
-                            pass_twiddle_count(g.logny)) * sizeof(double2);
+  const int mb = g.dim == 2 ? spatial_maxb(g) : 4;
+  L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8 + pass_twiddle_count(g.lognx, mb) +
+                            pass_twiddle_count(g.logny, mb)) * sizeof(double2);
   off = align_up(off + L.static_bytes, 256);
   L.off_alpha = off;
   const size_t LM = (size_t)g.L * g.M;
@@ -289,9 +290,10 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     cld w = unit_root(q % P, P, -1);
     host[o++] = make_double2((double)w.real(), (double)w.imag());
   }
+  const int mb = g.dim == 2 ? spatial_maxb(g) : 4;   // plan of the spatial FFT kernels
   auto ptw = [&](int logn) {
     std::vector<cld> v;
-    pass_twiddles(logn, v);
+    pass_twiddles(logn, mb, v);
     for (const cld &w : v) host[o++] = make_double2((double)w.real(), (double)w.imag());
   };
   size_t o_px = o; ptw(g.lognx);

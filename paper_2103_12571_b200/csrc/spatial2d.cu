@@ -81,12 +81,12 @@ __device__ __forceinline__ double2 inv_symbol(const StaticTables &st, double2 s,
 // M x M complex matvec over the M lines (stride ls) of every column x of `rows` rows in shared
 // memory: v_m <- sum_j A[m][j] v_j (A row-major in shared memory, compile-time M; the A reads
 // are warp-uniform broadcasts, issued inside the loop so they do not pin M^2 registers)
-template <int LX, int MM>
+template <class PX, int MM>
 __device__ __forceinline__ void node_transform_m(double2 *sm, int ls, int rows, const double2 *A) {
-  constexpr int NX = 1 << LX;
+  constexpr int LX = PX::LOGN, NX = 1 << LX;
   for (int i = threadIdx.x; i < rows * NX; i += blockDim.x) {
     const int x = i & (NX - 1), r = i >> LX;
-    double2 *base = sm + (size_t)r * MM * ls + rfft::F<LX>(x);
+    double2 *base = sm + (size_t)r * MM * ls + rfft::F<PX>(x);
     double2 v[MM];
 #pragma unroll
     for (int j = 0; j < MM; ++j) v[j] = base[j * ls];
@@ -102,46 +102,47 @@ __device__ __forceinline__ void node_transform_m(double2 *sm, int ls, int rows, 
     }
   }
 }
-template <int LX>
+template <class PX>
 __device__ __forceinline__ void node_transform(double2 *sm, int ls, int M, int rows, const double2 *A) {
   switch (M) {
-    case 1: node_transform_m<LX, 1>(sm, ls, rows, A); break;
-    case 2: node_transform_m<LX, 2>(sm, ls, rows, A); break;
-    case 3: node_transform_m<LX, 3>(sm, ls, rows, A); break;
-    case 4: node_transform_m<LX, 4>(sm, ls, rows, A); break;
-    case 5: node_transform_m<LX, 5>(sm, ls, rows, A); break;
-    case 6: node_transform_m<LX, 6>(sm, ls, rows, A); break;
-    case 7: node_transform_m<LX, 7>(sm, ls, rows, A); break;
-    default: node_transform_m<LX, 8>(sm, ls, rows, A); break;
+    case 1: node_transform_m<PX, 1>(sm, ls, rows, A); break;
+    case 2: node_transform_m<PX, 2>(sm, ls, rows, A); break;
+    case 3: node_transform_m<PX, 3>(sm, ls, rows, A); break;
+    case 4: node_transform_m<PX, 4>(sm, ls, rows, A); break;
+    case 5: node_transform_m<PX, 5>(sm, ls, rows, A); break;
+    case 6: node_transform_m<PX, 6>(sm, ls, rows, A); break;
+    case 7: node_transform_m<PX, 7>(sm, ls, rows, A); break;
+    default: node_transform_m<PX, 8>(sm, ls, rows, A); break;
   }
 }
 
 // ---- R item: rows y0 .. y0 + YR - 1 of slot p, all M nodes ---------------------------------
-template <int LX>
+template <class PX>
 __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
                                        const double2 *twx,
                                        double2 *__restrict__ X, int p, int y0, int YR, bool node) {
-  using PX = rfft::Plan<LX>;
-  constexpr int NX = PX::N;
+  constexpr int LX = PX::LOGN, NX = PX::N;
   const int M = g.M, nl = M * YR;
   double2 *xp = X + (size_t)p * M * g.N;
   for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
     const int x = i & (NX - 1), l = i >> LX;
     const int yy = l / M, m = l - yy * M;
-    cp_async16(tile + (size_t)l * NX + rfft::F<LX>(x), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX) + x);
+    cp_async16(tile + (size_t)l * NX + rfft::F<PX>(x), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX) + x);
   }
   if (node && threadIdx.x < M * M) nt[threadIdx.x] = __ldg(at.Sinv + (size_t)p * M * M + threadIdx.x);
   cp_async_wait_all();
   __syncthreads();
   if (node) {
-    node_transform<LX>(tile, NX, M, YR, nt);
+    node_transform<PX>(tile, NX, M, YR, nt);
     __syncthreads();
   }
   const int l = threadIdx.x / PX::TPL, tau = threadIdx.x - l * PX::TPL;
-  const int lc = l < nl ? l : nl - 1;   // TPL < 32: surplus lanes shadow the last line (no stores)
-  if (l >= nl && PX::TPL >= 32) return;   // idle warps (line barriers are per line)
+  // warps without a line skip; surplus lanes of a partly used warp (TPL < 32) run on the dummy
+  // line nl (never read back, never stored) so that their exchanges cannot touch a real line
+  if ((int)(threadIdx.x & ~31) / PX::TPL >= nl) return;
+  const int lc = l < nl ? l : nl;
   double2 v[PX::E];
-  rfft::forward_from_smem<LX>(v, tile + (size_t)lc * NX, lc, tau, twx);
+  rfft::forward_from_smem<PX>(v, tile + (size_t)lc * NX, lc, tau, twx);
   if (l < nl) {
     const int yy = l / M, m = l - yy * M;
     double2 *dst = xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX);
@@ -149,53 +150,54 @@ __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at,
 #pragma unroll
     for (int u = 0; u < PX::E / R; ++u)
 #pragma unroll
-      for (int t = 0; t < R; ++t) dst[rfft::s_slot<LX>(tau, u, t)] = v[u * R + t];
+      for (int t = 0; t < R; ++t) dst[rfft::s_slot<PX>(tau, u, t)] = v[u * R + t];
   }
 }
 
 // ---- I item: inverse rows ------------------------------------------------------------------
-template <int LX>
+template <class PX>
 __device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
                                        const double2 *twx,
                                        double2 *__restrict__ X, int p, int y0, int YR, bool node) {
-  using PX = rfft::Plan<LX>;
-  constexpr int NX = PX::N;
+  constexpr int LX = PX::LOGN, NX = PX::N;
   constexpr int R = 1 << PX::BL;
   const int M = g.M, nl = M * YR;
   double2 *xp = X + (size_t)p * M * g.N;
   const int l = threadIdx.x / PX::TPL, tau = threadIdx.x - l * PX::TPL;
-  const int lc = l < nl ? l : nl - 1;
-  const int yy = lc / M, m = lc - yy * M;
+  const bool wrun = (int)(threadIdx.x & ~31) / PX::TPL < nl;   // warp holds at least one line
+  const int lc = l < nl ? l : nl;                                 // nl: dummy line (see r_item)
+  const int ls_ = l < nl ? l : nl - 1;                            // line whose data the loads read
+  const int yy = ls_ / M, m = ls_ - yy * M;
   const double2 *src = xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX);
   double2 v[PX::E];
 #pragma unroll
   for (int u = 0; u < PX::E / R; ++u)
 #pragma unroll
-    for (int t = 0; t < R; ++t) v[u * R + t] = ld_cg(src + rfft::s_slot<LX>(tau, u, t));
+    for (int t = 0; t < R; ++t) v[u * R + t] = ld_cg(src + rfft::s_slot<PX>(tau, u, t));
   double2 *line = tile + (size_t)lc * NX;
-  if (l < nl || PX::TPL < 32) {
-    rfft::inverse_in_regs<LX>(v, line, lc, tau, twx);
-    if (l < nl) rfft::to_smem<LX, 0>(v, line, tau);
+  if (wrun) {
+    rfft::inverse_in_regs<PX>(v, line, lc, tau, twx);
+    if (l < nl) rfft::to_smem<PX, 0>(v, line, tau);
   }
   if (node && threadIdx.x < M * M) nt[threadIdx.x] = __ldg(at.SG + (size_t)p * M * M + threadIdx.x);
   __syncthreads();
   if (node) {
-    node_transform<LX>(tile, NX, M, YR, nt);
+    node_transform<PX>(tile, NX, M, YR, nt);
     __syncthreads();
   }
   for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
     const int x = i & (NX - 1), li = i >> LX;
     const int y2 = li / M, m2 = li - y2 * M;
-    xp[(size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x] = tile[(size_t)li * NX + rfft::F<LX>(x)];
+    xp[(size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x] = tile[(size_t)li * NX + rfft::F<PX>(x)];
   }
 }
 
 // ---- C item: columns (S-slots) kx0 .. kx0 + TC - 1 of line q -----------------------------------
-template <int LX, int LY>
+template <class PX, class PY>
 __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st, const AlphaTables &at,
                                        double2 *tile, const double2 *twy, double2 *__restrict__ X,
                                        const double2 *__restrict__ spec, int q, int kx0, int TC) {
-  using PY = rfft::Plan<LY>;
+  constexpr int LX = PX::LOGN, LY = PY::LOGN;
   constexpr int NX = 1 << LX, NY = PY::N;
   constexpr int R = 1 << PY::BL;
   const int pad = TC >= 8 ? 1 : 8 / TC;
@@ -203,11 +205,12 @@ __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st
   const int lT = 31 - __clz(TC);
   double2 *xl = X + (size_t)q * g.N;
   const int l = threadIdx.x / PY::TPL, tau = threadIdx.x - l * PY::TPL;
-  const int lc = l < TC ? l : TC - 1;
+  const bool wrun = (int)(threadIdx.x & ~31) / PY::TPL < TC;   // warp holds at least one column
+  const int lc = l < TC ? l : TC;                                 // TC: dummy line (see r_item)
   double2 *line = tile + (size_t)lc * ls;
   const double2 s = __ldg(at.shift + q);
   const double inv_n = 1.0 / ((double)NX * (double)NY);
-  const int pxs = rfft::slot_to_pos<LX>(kx0 + lc);     // x position of this column (S-layout slot)
+  const int pxs = rfft::slot_to_pos<PX>(kx0 + (l < TC ? l : TC - 1));   // x position of the column (S-slot)
   const int kx = brev(pxs, LX);
   double2 v[PY::E];
   if (spec) {
@@ -217,48 +220,50 @@ __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st
     for (int u = 0; u < PY::E / R; ++u)
 #pragma unroll
       for (int t = 0; t < R; ++t) {
-        const int P = rfft::last_pos<LY>(tau, u, t);
+        const int P = rfft::last_pos<PY>(tau, u, t);
         const double2 w = cmul(sg, __ldg(spec + ((size_t)P << LX) + pxs));
         v[u * R + t] = cmul(w, inv_symbol(st, s, inv_n, kx, brev(P, LY)));
       }
   } else {
     for (int i = threadIdx.x; i < TC * NY; i += blockDim.x) {
       const int c = i & (TC - 1), y = i >> lT;
-      cp_async16(tile + (size_t)c * ls + rfft::F<LY>(y), xl + ((size_t)y << LX) + kx0 + c);
+      cp_async16(tile + (size_t)c * ls + rfft::F<PY>(y), xl + ((size_t)y << LX) + kx0 + c);
     }
     cp_async_wait_all();
     __syncthreads();
-    if (l < TC || PY::TPL < 32) {
-      rfft::forward_from_smem<LY>(v, line, lc, tau, twy);
+    if (wrun) {
+      rfft::forward_from_smem<PY>(v, line, lc, tau, twy);
 #pragma unroll
       for (int u = 0; u < PY::E / R; ++u)
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-          const int P = rfft::last_pos<LY>(tau, u, t);
+          const int P = rfft::last_pos<PY>(tau, u, t);
           v[u * R + t] = cmul(v[u * R + t], inv_symbol(st, s, inv_n, kx, brev(P, LY)));
         }
-      rfft::line_sync<LY>(lc);   // every thread of the line has read its last-pass values
+      rfft::line_sync<PY>(lc);   // every thread of the line has read its last-pass values
     }
   }
-  if (l < TC || PY::TPL < 32) {
-    rfft::inverse_in_regs<LY>(v, line, lc, tau, twy);
-    if (l < TC) rfft::to_smem<LY, 0>(v, line, tau);
+  if (wrun) {
+    rfft::inverse_in_regs<PY>(v, line, lc, tau, twy);
+    if (l < TC) rfft::to_smem<PY, 0>(v, line, tau);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TC * NY; i += blockDim.x) {
     const int c = i & (TC - 1), y = i >> lT;
-    xl[((size_t)y << LX) + kx0 + c] = tile[(size_t)c * ls + rfft::F<LY>(y)];
+    xl[((size_t)y << LX) + kx0 + c] = tile[(size_t)c * ls + rfft::F<PY>(y)];
   }
 }
 
 }  // namespace
 
-template <int LX, int LY>
-__global__ void __launch_bounds__(kSpThreads, 2)
+template <int LX, int LY, int MB>
+__global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
     spatial2d_kernel(const Geometry g, StaticTables st, AlphaTables at, SpatialPlan sp, double2 *__restrict__ X,
                      const double2 *__restrict__ spec, unsigned *__restrict__ sync) {
+  using PX = rfft::Plan<LX, MB>;
+  using PY = rfft::Plan<LY, MB>;
   extern __shared__ double2 sm[];
-  constexpr int TWX = rfft::Plan<LX>::twsize(), TWY = rfft::Plan<LY>::twsize();
+  constexpr int TWX = PX::twsize(), TWY = PY::twsize();
   double2 *twx = sm, *twy = sm + TWX, *nt = sm + TWX + TWY, *tile = nt + 64;   // nt: M x M node table
   copy_table(twx, st.ptwx, TWX);
   copy_table(twy, st.ptwy, TWY);
@@ -287,14 +292,14 @@ __global__ void __launch_bounds__(kSpThreads, 2)
       if (stage == kStC) {
         if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
         const int li = kk / cPerLine;                       // line within the batch
-        c_item<LX, LY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, b * sp.B * g.M + li,
+        c_item<PX, PY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, b * sp.B * g.M + li,
                        (kk - li * cPerLine) * sp.TC, sp.TC);
       } else {
         if (stage == kStI) wait_count(sync + kStC * sp.nbatch + b, (unsigned)sp.nC);
         const int pi = kk / riPerBatch;                     // slot within the batch
         const int y0 = (kk - pi * riPerBatch) * sp.YR;
-        if (stage == kStR) r_item<LX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
-        else i_item<LX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+        if (stage == kStR) r_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+        else i_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
       }
       publish(sync + stage * sp.nbatch + b);
     }
@@ -305,11 +310,20 @@ __global__ void __launch_bounds__(kSpThreads, 2)
 // ---------------------------------------------------------------------------------------------
 // host side
 
+int spatial_maxb(const Geometry &g) {
+  // Radix-16 plans (E = 16 values per thread, two CTAs per SM).  A radix-32 plan for the
+  // 512/1024-point axes (one exchange instead of two, but 246 registers -> one CTA of 8 warps per
+  // SM) measured 95.5 ms vs 79.1 ms per config-5 spatial launch: latency hiding wins here.
+  (void)g;
+  return 4;
+}
+
 SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth) {
   SpatialPlan sp{};
   sp.lines = lines;
-  const int tplx = g.nx >= 16 ? g.nx / 16 : 1;
-  const int tply = g.ny >= 16 ? g.ny / 16 : 1;
+  const int mb = spatial_maxb(g);
+  const int ex = g.lognx < mb ? g.nx : (1 << mb), ey = g.logny < mb ? g.ny : (1 << mb);
+  const int tplx = g.nx / ex, tply = g.ny / ey;
   sp.YR = kSpThreads / (tplx * g.M);         // rows per R/I item: M*YR lines of TPLx threads
   if (sp.YR < 1) sp.YR = 1;
   while (sp.YR > 1 && (g.ny % sp.YR)) sp.YR >>= 1;
@@ -340,13 +354,15 @@ bool spatial2d_supported(const Geometry &g) {
 }
 
 namespace {
-template <int LX, int LY>
+template <int LX, int LY, int MB>
 cudaError_t launch_sp(const Geometry &g, const StaticTables &st, const AlphaTables &at, const SpatialPlan &sp,
                       double2 *X, const double2 *spec, unsigned *sync, cudaStream_t s) {
-  const void *fn = (const void *)spatial2d_kernel<LX, LY>;
-  const size_t tile = (size_t)sp.YR * g.M * g.nx > (size_t)sp.TC * (g.ny + 8) ? (size_t)sp.YR * g.M * g.nx
-                                                                               : (size_t)sp.TC * (g.ny + 8);
-  const size_t smem = (rfft::Plan<LX>::twsize() + rfft::Plan<LY>::twsize() + 64 + tile) * sizeof(double2);
+  const void *fn = (const void *)spatial2d_kernel<LX, LY, MB>;
+  // tile + one dummy line for the surplus lanes of partly used warps
+  const size_t tile_r = (size_t)(sp.YR * g.M + 1) * g.nx, tile_c = (size_t)(sp.TC + 1) * (g.ny + 8);
+  const size_t tile = tile_r > tile_c ? tile_r : tile_c;
+  const size_t smem =
+      (rfft::Plan<LX, MB>::twsize() + rfft::Plan<LY, MB>::twsize() + 64 + tile) * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per = 0;
@@ -374,7 +390,7 @@ cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const Al
   cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)3 * sp.nbatch * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
 #define PINT_SP(LXX, LYY) \
-  if (g.lognx == LXX && g.logny == LYY) return launch_sp<LXX, LYY>(g, st, at, sp, X, spec, sync, s);
+  if (g.lognx == LXX && g.logny == LYY) return launch_sp<LXX, LYY, 4>(g, st, at, sp, X, spec, sync, s);
 #define PINT_SP3(L_) PINT_SP(L_, L_) PINT_SP(L_, L_ - 1) PINT_SP(L_ - 1, L_)
   PINT_SP(2, 2)
   PINT_SP3(3) PINT_SP3(4) PINT_SP3(5) PINT_SP3(6) PINT_SP3(7) PINT_SP3(8) PINT_SP3(9) PINT_SP3(10)

@@ -1,9 +1,13 @@
+# Round measurement (1 GPU): all GPU tests, bench lines (config 5 default incl. cpu_baseline/e2e,
+# config 5 direct form, configs 3 and 4), ncu launch list and ncu --set full of the dominant kernel.
 set -x
-nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv > gpurun_out/smi.txt
-timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench4.json 2> gpurun_out/bench4.err
-timeout 600 python bench.py --config 3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench3.json 2> gpurun_out/bench3.err
-timeout 900 python bench.py --config 5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench5.json 2> gpurun_out/bench5.err
-timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -k "full_size_sampled" > gpurun_out/gpu_sampled.log 2>&1
-CMD="python bench.py --config 4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
-$CMD > gpurun_out/plain4.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches4.csv $CMD > gpurun_out/ncu4.log 2>&1
-echo finished
+nvidia-smi --query-gpu=name,driver_version,memory.total,clocks.max.sm --format=csv > gpurun_out/smi.txt
+timeout 1500 python -m pytest tests -m gpu -q --timeout 1200 > gpurun_out/gpu_tests_all.log 2>&1
+tail -3 gpurun_out/gpu_tests_all.log
+timeout 900 python bench.py > gpurun_out/bench_cfg5.json 2> gpurun_out/bench_cfg5.err
+timeout 600 python bench.py --form direct --no-cpu-baseline > gpurun_out/bench_cfg5_direct.json 2>> gpurun_out/bench_cfg5.err
+for c in 3 4; do timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_cfg$c.json 2>> gpurun_out/bench_cfg5.err; done
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+$CMD > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg5.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+$CMD > gpurun_out/plain_full.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${TOPK:-spatial2d}" -s 1 -c 1 -o gpurun_out/prof_cfg5_top $CMD > gpurun_out/ncu_full.log 2>&1
+tail -1 gpurun_out/ncu_full.log
