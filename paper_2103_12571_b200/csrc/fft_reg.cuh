@@ -94,26 +94,40 @@ __device__ __forceinline__ void from_smem(double2 (&v)[P::E], const double2 *lin
 }
 
 // slot t of a radix-2^B butterfly carries frequency bitrev_B(t), i.e. exponent r = brev(t);
-// multiply every slot by w^{j r} (CONJ: w^{-j r}) with w^{j 2^k} = tp[k s]
+// multiply every slot by w^{j r} (CONJ: w^{-j r}) with w^{j 2^k} = tp[k s].  Within each block
+// [hb, 2 hb) the other powers come from two interleaved product chains (even and odd offsets,
+// step w^{2j}): depth <= hb / 2 and five live values, error a few ulp.
 template <int B, bool CONJ>
 __device__ __forceinline__ void apply_twiddles(double2 *x, const double2 *tp, int s) {
   constexpr int R = 1 << B;
-  double2 w1 = tp[0];
-  if (CONJ) w1.y = -w1.y;
-  double2 w = w1;
+  auto ld = [&](int k) {
+    double2 w = tp[k * s];
+    if (CONJ) w.y = -w.y;
+    return w;
+  };
+  const double2 w1 = ld(0);
+  x[brev_ct<B>(1)] = cmul(x[brev_ct<B>(1)], w1);
+  if constexpr (B >= 2) {
+    const double2 w2 = ld(1);
+    x[brev_ct<B>(2)] = cmul(x[brev_ct<B>(2)], w2);
+    x[brev_ct<B>(3)] = cmul(x[brev_ct<B>(3)], cmul(w2, w1));
 #pragma unroll
-  for (int r = 1; r < R; ++r) {
-    if (r > 1) {
-      if ((r & (r - 1)) == 0) {        // power of two: fresh table value (resets the chain)
-        w = tp[ilog2_ct(r) * s];
-        if (CONJ) w.y = -w.y;
-      } else {
-        w = cmul(w, w1);
+    for (int k = 2; k < B; ++k) {
+      const int hb = 1 << k;
+      const double2 wh = ld(k);
+      double2 we = wh, wo = cmul(wh, w1);
+#pragma unroll
+      for (int o = 0; o < hb; o += 2) {
+        if (o > 0) {
+          we = cmul(we, w2);
+          wo = cmul(wo, w2);
+        }
+        x[brev_ct<B>(hb + o)] = cmul(x[brev_ct<B>(hb + o)], we);
+        x[brev_ct<B>(hb + o + 1)] = cmul(x[brev_ct<B>(hb + o + 1)], wo);
       }
     }
-    const int t = brev_ct<B>(r);
-    x[t] = cmul(x[t], w);
   }
+  (void)R;
 }
 
 // DIF pass PASS on the thread's values; tw = the plan's twiddle table (shared memory)

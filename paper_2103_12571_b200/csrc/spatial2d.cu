@@ -16,7 +16,7 @@
 // dependency points to an item that comes earlier in the sequence and each CTA walks its items
 // in sequence order, so the earliest unfinished item can always run (no deadlock while all CTAs
 // are resident, which the cooperative launch guarantees).  Producers publish with bar.sync +
-// fence.gpu + atomicAdd; consumers acquire with ld.acquire.gpu and then load with cp.async.cg /
+// red.release.gpu; consumers acquire with ld.acquire.gpu and then load with cp.async.cg /
 // ld.global.cg (L2; never a stale L1 line).
 //
 // Direct form (Alg. 1 as printed): the C stage synthesizes its input spectrum sig_q * r0hat (no
@@ -54,12 +54,11 @@ __device__ __forceinline__ void wait_count(const unsigned *ctr, unsigned need) {
   __syncthreads();
 }
 
+// all threads' stores of the item are ordered before the barrier; thread 0's release-add makes
+// them visible at gpu scope to the consumer that acquires the counter (PTX release/acquire)
 __device__ __forceinline__ void publish(unsigned *ctr) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-  }
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
 }
 
 __device__ __forceinline__ void copy_table(double2 *dst, const double2 *src, int n) {
