@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 
 // ---------------------------------------------------------------------------------------------
 // 2-D residual: X[l][m][n] = alpha^{l/L} (w - C u)[l][m][n] on spatial blocks BY x BX with a
-// one-point halo staged in shared memory (all M nodes of one l per CTA).
+// one-point halo staged in shared memory (all M nodes of one l per CTA).  Each warp stages whole
+// halo rows (lanes along x: no index divisions), each thread then evaluates BX*BY/256 points.
 
 template <int M>
 __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
@@ -348,40 +349,41 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   const int W = BX + 2, H = BY + 2;
   const size_t plane = (size_t)M * g.N;
   const double2 *ul = u + (size_t)l * plane;
-  const int tot = M * W * H;
-  const FastDiv fW((unsigned)W), fH((unsigned)H);
-  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-    const int r = (int)fW.div((unsigned)i), xx = i - r * W;
-    const int j = (int)fH.div((unsigned)r), yy = r - j * H;
-    const int x = (x0 + xx - 1) & (g.nx - 1), y = (y0 + yy - 1) & (g.ny - 1);
-    cp_async16(sm + i, ul + (size_t)j * g.N + ((size_t)y << g.lognx) + x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < M * H; r += blockDim.x >> 5) {
+    const int j = r / H, yy = r - j * H;
+    const int y = (y0 + yy - 1) & (g.ny - 1);
+    const double2 *src = ul + (size_t)j * g.N + ((size_t)y << g.lognx);
+    double2 *dst = sm + r * W;
+    for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - 1) & (g.nx - 1)));
   }
   cp_async_wait_all();
   __syncthreads();
-  const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
-  if (ty >= BY) return;
-  const int n = ((y0 + ty) << g.lognx) + x0 + tx;
-  const double2 base = prev_value(st, l, n);
-  double2 uc[M], Au[M];
-#pragma unroll
-  for (int j = 0; j < M; ++j) {
-    const double2 *s = sm + (j * H + ty + 1) * W + tx + 1;
-    const double2 c = s[0], a = s[-1], bb = s[1], d = s[-W], e = s[W];
-    uc[j] = c;
-    Au[j].x = g.c0 * c.x + g.cxm * a.x + g.cxp * bb.x + g.cym * d.x + g.cyp * e.x;
-    Au[j].y = g.c0 * c.y + g.cxm * a.y + g.cxp * bb.y + g.cym * d.y + g.cyp * e.y;
-  }
   const double sc = __ldg(at.scale_fwd + l);
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    double2 acc = csub(base, uc[m]);
+  for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
+    const int ty = pt / BX, tx = pt - ty * BX;
+    const int n = ((y0 + ty) << g.lognx) + x0 + tx;
+    const double2 base = prev_value(st, l, n);
+    double2 uc[M], Au[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-      const double q = g.dTQ[m * M + j];
-      acc.x = fma(q, Au[j].x, acc.x);
-      acc.y = fma(q, Au[j].y, acc.y);
+      const double2 *s = sm + (j * H + ty + 1) * W + tx + 1;
+      const double2 c = s[0], a = s[-1], bb = s[1], d = s[-W], e = s[W];
+      uc[j] = c;
+      Au[j].x = g.c0 * c.x + g.cxm * a.x + g.cxp * bb.x + g.cym * d.x + g.cyp * e.x;
+      Au[j].y = g.c0 * c.y + g.cxm * a.y + g.cxp * bb.y + g.cym * d.y + g.cyp * e.y;
     }
-    X[(size_t)l * plane + (size_t)m * g.N + n] = cscale(acc, sc);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double2 acc = csub(base, uc[m]);
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const double q = g.dTQ[m * M + j];
+        acc.x = fma(q, Au[j].x, acc.x);
+        acc.y = fma(q, Au[j].y, acc.y);
+      }
+      X[(size_t)l * plane + (size_t)m * g.N + n] = cscale(acc, sc);
+    }
   }
 }
 
@@ -1045,8 +1047,8 @@ static cudaError_t set_smem(const void *fn, size_t bytes) {
 
 // 2-D residual block: BX x BY points, BX*BY <= 256
 static void residual_block(const Geometry &g, int &BX, int &BY) {
-  BX = g.nx < 32 ? g.nx : 32;
-  BY = 256 / BX;
+  BX = g.nx < 64 ? g.nx : 64;     // 64 x 8 points per CTA (halo overhead 66*10/512 = 1.29)
+  BY = 512 / BX;
   if (BY > g.ny) BY = g.ny;
 }
 

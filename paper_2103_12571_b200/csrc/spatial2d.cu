@@ -255,56 +255,6 @@ __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st
 
 }  // namespace
 
-// This CTA's walk over the item sequence: rounds j (stage si of round j works on batch j - si,
-// segments in stage order), items k = cta, cta + G, ... of the global sequence.
-struct ItemIter {
-  int j, k, rn, slo;
-  long long rs;   // sequence position of round j's first item
-  int G, cta;
-  bool valid;
-  __device__ __forceinline__ int first(const SpatialPlan &sp) const { return sp.synth ? kStC : kStR; }
-  __device__ __forceinline__ void setup_round(const SpatialPlan &sp) {
-    slo = j - (sp.nbatch - 1) > 0 ? j - (sp.nbatch - 1) : 0;
-    const int shi = j < sp.nstage - 1 ? j : sp.nstage - 1;
-    rn = 0;
-    for (int si = slo; si <= shi; ++si) rn += (first(sp) + si == kStC) ? sp.nC : sp.nRI;
-    k = (int)(((cta - rs) % G + G) % G);
-  }
-  __device__ __forceinline__ void settle(const SpatialPlan &sp) {
-    while (j < sp.rounds && k >= rn) {
-      rs += rn;
-      ++j;
-      if (j < sp.rounds) setup_round(sp);
-    }
-    valid = j < sp.rounds;
-  }
-  __device__ __forceinline__ void init(const SpatialPlan &sp, int G_, int cta_) {
-    G = G_;
-    cta = cta_;
-    j = 0;
-    rs = 0;
-    setup_round(sp);
-    settle(sp);
-  }
-  __device__ __forceinline__ void next(const SpatialPlan &sp) {
-    if (!valid) return;
-    k += G;
-    settle(sp);
-  }
-  __device__ __forceinline__ void decode(const SpatialPlan &sp, int &stage, int &b, int &kk) const {
-    int si = slo;
-    kk = k;
-    for (;;) {
-      const int n = (first(sp) + si == kStC) ? sp.nC : sp.nRI;
-      if (kk < n) break;
-      kk -= n;
-      ++si;
-    }
-    stage = first(sp) + si;
-    b = j - si;
-  }
-};
-
 template <int LX, int LY, int MB>
 __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
     spatial2d_kernel(const Geometry g, StaticTables st, AlphaTables at, SpatialPlan sp, double2 *__restrict__ X,
@@ -317,30 +267,42 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
   copy_table(twx, st.ptwx, TWX);
   copy_table(twy, st.ptwy, TWY);
   __syncthreads();
+  const int G = gridDim.x, cta = blockIdx.x;
   const int riPerBatch = g.ny / sp.YR, cPerLine = g.nx / sp.TC;
   const bool node = st.P == 1;   // P > 1: the node transforms live in the cross-rank DFT kernels
-  ItemIter cur, nxt;
-  cur.init(sp, gridDim.x, blockIdx.x);
-  nxt = cur;
-  nxt.next(sp);
-  while (cur.valid) {
-    int stage, b, kk;
-    cur.decode(sp, stage, b, kk);
-    if (stage == kStC) {
-      if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
-      const int li = kk / cPerLine;                       // line within the batch
-      c_item<PX, PY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, b * sp.B * g.M + li,
-                     (kk - li * cPerLine) * sp.TC, sp.TC);
-    } else {
-      if (stage == kStI) wait_count(sync + kStC * sp.nbatch + b, (unsigned)sp.nC);
-      const int pi = kk / riPerBatch;                     // slot within the batch
-      const int y0 = (kk - pi * riPerBatch) * sp.YR;
-      if (stage == kStR) r_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
-      else i_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+  long long rs = 0;   // sequence position of the current round's first item
+  for (int j = 0; j < sp.rounds; ++j) {
+    // stage segments of round j: stage index si works on batch j - si
+    const int first = sp.synth ? kStC : kStR;
+    const int slo = j - (sp.nbatch - 1) > 0 ? j - (sp.nbatch - 1) : 0;
+    const int shi = j < sp.nstage - 1 ? j : sp.nstage - 1;
+    int rn = 0;
+    for (int si = slo; si <= shi; ++si) rn += (first + si == kStC) ? sp.nC : sp.nRI;
+    int k = (int)(((cta - rs) % G + G) % G);
+    for (; k < rn; k += G) {
+      int si = slo, kk = k;
+      for (;;) {
+        const int n = (first + si == kStC) ? sp.nC : sp.nRI;
+        if (kk < n) break;
+        kk -= n;
+        ++si;
+      }
+      const int stage = first + si, b = j - si;
+      if (stage == kStC) {
+        if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
+        const int li = kk / cPerLine;                       // line within the batch
+        c_item<PX, PY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, b * sp.B * g.M + li,
+                       (kk - li * cPerLine) * sp.TC, sp.TC);
+      } else {
+        if (stage == kStI) wait_count(sync + kStC * sp.nbatch + b, (unsigned)sp.nC);
+        const int pi = kk / riPerBatch;                     // slot within the batch
+        const int y0 = (kk - pi * riPerBatch) * sp.YR;
+        if (stage == kStR) r_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+        else i_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+      }
+      publish(sync + stage * sp.nbatch + b);
     }
-    publish(sync + stage * sp.nbatch + b);
-    cur = nxt;
-    nxt.next(sp);
+    rs += rn;
   }
 }
 
