@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--grid", type=int, default=0, help="profiling only: override nx (and ny in 2-D)")
     ap.add_argument("--form", default="correction", choices=["correction", "direct"],
                     help="iteration form: correction (north star, default) or direct (Alg. 1 as printed)")
+    ap.add_argument("--hermitian", action="store_true",
+                    help="real-data fast path (SURVEY 8(f) row 1): solve only frequencies k <= L/2")
     args = ap.parse_args()
     rank, world, local = env_rank()
     p = W.CONFIGS[args.config]
@@ -237,6 +239,8 @@ def main():
         s = P.Solver(p, u0, device=local)
     if args.form != "correction":
         s.set_form(args.form)
+    if args.hermitian:
+        s.set_hermitian(True)
     stream = s.stream
     w_inf = s.w_inf()
     nlaunch = s.launches_per_iteration()
@@ -272,7 +276,9 @@ def main():
         kms = s.iterate_profiled(nprof)
     else:
         kms = None
-    algo_tab = ALGO_BYTES_DIRECT if args.form == "direct" else ALGO_BYTES
+    algo_tab = dict(ALGO_BYTES_DIRECT if args.form == "direct" else ALGO_BYTES)
+    if args.hermitian:   # L/2 + 1 of L frequency slots solved; the I stage also writes the conjugates
+        algo_tab["spatial2d_kernel"] = 32 if args.form == "direct" else 56
     model_bytes = sum(algo_tab.get(n_, 32) for n_ in names)
     iteration_roof = {"model_bytes_per_unknown": model_bytes,
                       "achieved_gbs": model_bytes * p.U / world / (ms * 1e-3) / 1e9,
@@ -347,6 +353,7 @@ def main():
                 "data": "synthetic (workloads.py seeded generators; BASELINE.json config recipe)",
                 "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
                            "unknowns": p.U, "bytes_per_vector": 16 * p.U, "form": args.form,
+                           "hermitian": bool(args.hermitian),
                            "l2": "inputs larger than L2 (no flush)" if 16 * p.U > 126e6 else "L2-resident",
                            "parallelism": "single GPU" if world == 1 else
                            f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},

@@ -131,6 +131,16 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
 #define PINT_FORM_DIRECT 1
 pint_status pint_set_form(pint_ctx *c, int32_t form);
 
+/* Real-data fast path, spatial half.  For real A, w and alpha (every
+ * config: real u0, b == 0) the alpha-scaled time spectrum is Hermitian, x_{L-k} = conj(x_k)
+ * (P:164-171 with real J and V^{-1} = F* J^{-1}), and so is the solution of the frequency-block
+ * systems (the blocks of L - k are the complex conjugates of those of k).  on = 1: only the
+ * L/2 + 1 frequencies k <= L/2 are node-transformed and solved; y_{L-k} = conj(y_k) is written
+ * by the solve.  Same result as on = 0 up to the roundoff imaginary part of the iterate (which
+ * on = 1 projects out).  Requirements: dim == 2, nranks == 1, L >= 2, u0 real (imaginary parts
+ * exactly 0; pint_set_initial_value then rejects non-real data).  Errors: PINT_ERR_INVALID. */
+pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
+
 /* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:
  * nullable; if given, n_iter doubles receive ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf (Alg. 2 line 7,
  * P:421) and the call synchronises the stream.  PINT_ERR_SCHEDULE if the schedule would run out. */

@@ -50,6 +50,11 @@ struct StaticTables {
   int P, rank;
   // per-pass twiddle tables of the register FFT engine (fft_reg.cuh) for nx, ny
   const double2 *ptwx, *ptwy;
+  // frequency slots whose spatial solves run (2-D): slots[0 .. nsolve); partner[p] = slot of the
+  // conjugate frequency L - k that receives conj(y_k) (-1: none).  Default: every slot, no
+  // partners; Hermitian mode (real data, pint_set_hermitian): the L/2 + 1 slots with k <= L/2.
+  const int *slots, *partner;
+  int nsolve;
 };
 
 struct Buffers {

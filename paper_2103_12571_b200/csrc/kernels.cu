@@ -1127,7 +1127,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       *out = b.Y;
     }
   } else if (reg2d(g)) {
-    e = launch_spatial2d(g, st, at, b.X, nullptr, b.sync, g.L * g.M, s);
+    e = launch_spatial2d(g, st, at, b.X, nullptr, b.sync, st.nsolve * g.M, s);
     rec(s);
     *out = b.X;
     if (e != cudaSuccess) return e;
@@ -1263,7 +1263,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   cudaError_t e = cudaSuccess;
   const int lines = g.L * g.M;
   if (reg2d(g)) {
-    e = launch_spatial2d(g, st, at, b.X, r0, b.sync, lines, s);
+    e = launch_spatial2d(g, st, at, b.X, r0, b.sync, st.nsolve * g.M, s);
     rec(s);
     *out = b.X;
     return e != cudaSuccess ? e : cudaGetLastError();

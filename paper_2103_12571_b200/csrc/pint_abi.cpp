@@ -36,6 +36,7 @@ struct Layout {
   size_t off_alpha, alpha_bytes_each;
   size_t off_red, red_bytes;
   size_t off_sync, sync_bytes;                // 2-D spatial pipeline completion counters
+  size_t off_sym;                             // solve-slot list and conjugate partners [2][L] int
   size_t total;
   bool two_vectors;
 };
@@ -59,6 +60,7 @@ struct pint_ctx {
   std::vector<double> alphas;
   int k = 0;
   int form = PINT_FORM_CORRECTION;
+  bool hermitian = false;
   bool poisoned = false;
   std::vector<ld> t, Q;
   std::vector<double> u0;          // host copy (2N)
@@ -165,6 +167,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   L.off_sync = off;
   L.sync_bytes = g.dim == 2 ? spatial_sync_bytes(g.L * g.M) : 0;
   off = align_up(off + L.sync_bytes, 256);
+  L.off_sym = off;
+  off = align_up(off + 2 * (size_t)g.L * sizeof(int), 256);
   L.total = off;
   return L;
 }
@@ -333,6 +337,15 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     } else {
       c->loopback = true;
     }
+  }
+  {
+    std::vector<int> sym(2 * (size_t)g.L);
+    for (int q = 0; q < g.L; ++q) { sym[q] = q; sym[g.L + q] = -1; }
+    int *dsym = (int *)(c->work + lay.off_sym);
+    CUDA_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    c->st.slots = dsym;
+    c->st.partner = dsym + g.L;
+    c->st.nsolve = g.L;
   }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
             (double *)(c->work + lay.off_red), (unsigned *)(c->work + lay.off_sync)};
@@ -784,6 +797,9 @@ pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
 pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t reset_iterate) {
   if (!c || !u0_host) return fail(PINT_ERR_INVALID, "NULL argument");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (c->hermitian)
+    for (int n = 0; n < c->g.N; ++n)
+      if (u0_host[2 * n + 1] != 0.0) return fail(PINT_ERR_INVALID, "Hermitian mode needs a real u0");
   c->u0.assign(u0_host, u0_host + 2 * (size_t)c->g.N);
   CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, u0_host, (size_t)c->g.N * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
   if (reset_iterate) {
@@ -848,6 +864,38 @@ pint_status pint_set_form(pint_ctx *c, int32_t form) {
   if (form != PINT_FORM_CORRECTION && form != PINT_FORM_DIRECT) return fail(PINT_ERR_INVALID, "unknown form");
   if (form == PINT_FORM_DIRECT && c->P > 1) return fail(PINT_ERR_INVALID, "the direct form is single-rank only");
   c->form = form;
+  return PINT_OK;
+}
+
+pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  const Geometry &g = c->g;
+  if (on) {
+    if (g.dim != 2) return fail(PINT_ERR_INVALID, "Hermitian mode: 2-D problems only in this build");
+    if (c->P != 1) return fail(PINT_ERR_INVALID, "Hermitian mode is single-rank only");
+    if (g.L < 2) return fail(PINT_ERR_INVALID, "Hermitian mode needs L >= 2");
+    for (int n = 0; n < g.N; ++n)
+      if (c->u0[2 * n + 1] != 0.0) return fail(PINT_ERR_INVALID, "Hermitian mode needs a real u0");
+  }
+  // slot p holds frequency k = bitrev(p) (1 rank); solve the slots with k <= L/2, in slot order
+  std::vector<int> sym(2 * (size_t)g.L, -1);
+  int ns = 0;
+  for (int p = 0; p < g.L; ++p) {
+    const int k = bitrev(p, g.logL);
+    if (!on) {
+      sym[ns++] = p;
+    } else if (k <= g.L / 2) {
+      sym[ns++] = p;
+      const int kc = (g.L - k) % g.L;
+      if (kc != k) sym[g.L + p] = bitrev(kc, g.logL);
+    }
+  }
+  int *dsym = (int *)(c->work + c->lay.off_sym);
+  CUDA_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->st.nsolve = ns;
+  c->hermitian = on != 0;
   return PINT_OK;
 }
 

@@ -21,6 +21,9 @@
 //
 // Direct form (Alg. 1 as printed): the C stage synthesizes its input spectrum sig_q * r0hat (no
 // R stage); see launch_direct_front in kernels.cu.
+//
+// Solved slots: st.slots[0 .. nsolve) (all L, or the L/2 + 1 slots with k <= L/2 in Hermitian
+// mode, where the I stage also writes conj(y) to the conjugate frequency's slot st.partner[p]).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -157,7 +160,7 @@ __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at,
 template <class PX>
 __device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
                                        const double2 *twx,
-                                       double2 *__restrict__ X, int p, int y0, int YR, bool node) {
+                                       double2 *__restrict__ X, int p, int y0, int YR, bool node, int partner) {
   constexpr int LX = PX::LOGN, NX = PX::N;
   constexpr int R = 1 << PX::BL;
   const int M = g.M, nl = M * YR;
@@ -184,10 +187,15 @@ __device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at,
     node_transform<PX>(tile, NX, M, YR, nt);
     __syncthreads();
   }
+  // Hermitian mode: the conjugate frequency's slot receives conj(y) (same rows, all nodes)
+  double2 *xc = partner >= 0 ? X + (size_t)partner * M * g.N : nullptr;
   for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
     const int x = i & (NX - 1), li = i >> LX;
     const int y2 = li / M, m2 = li - y2 * M;
-    xp[(size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x] = tile[(size_t)li * NX + rfft::F<PX>(x)];
+    const size_t off = (size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x;
+    const double2 v = tile[(size_t)li * NX + rfft::F<PX>(x)];
+    xp[off] = v;
+    if (xc) xc[off] = make_double2(v.x, -v.y);
   }
 }
 
@@ -291,14 +299,15 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
       if (stage == kStC) {
         if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
         const int li = kk / cPerLine;                       // line within the batch
-        c_item<PX, PY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, b * sp.B * g.M + li,
-                       (kk - li * cPerLine) * sp.TC, sp.TC);
+        const int q = __ldg(st.slots + b * sp.B + li / g.M) * g.M + li % g.M;
+        c_item<PX, PY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, q, (kk - li * cPerLine) * sp.TC, sp.TC);
       } else {
         if (stage == kStI) wait_count(sync + kStC * sp.nbatch + b, (unsigned)sp.nC);
         const int pi = kk / riPerBatch;                     // slot within the batch
         const int y0 = (kk - pi * riPerBatch) * sp.YR;
-        if (stage == kStR) r_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
-        else i_item<PX>(g, at, tile, nt, twx, X, b * sp.B + pi, y0, sp.YR, node);
+        const int slot = __ldg(st.slots + b * sp.B + pi);
+        if (stage == kStR) r_item<PX>(g, at, tile, nt, twx, X, slot, y0, sp.YR, node);
+        else i_item<PX>(g, at, tile, nt, twx, X, slot, y0, sp.YR, node, __ldg(st.partner + slot));
       }
       publish(sync + stage * sp.nbatch + b);
     }

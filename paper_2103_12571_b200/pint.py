@@ -28,7 +28,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
-           "pint_set_form"]
+           "pint_set_form", "pint_set_hermitian"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -90,6 +90,7 @@ def load_library(path: str = LIB_PATH):
         "pint_group_iterate": (i32, [ctypes.POINTER(vp), i32, i32, dp]),
         "pint_group_residual_norm": (i32, [ctypes.POINTER(vp), i32, dp, dp]),
         "pint_set_form": (i32, [vp, i32]),
+        "pint_set_hermitian": (i32, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -186,6 +187,10 @@ class Solver:
     def set_form(self, form: str):
         """"correction" (default, u += C_a^{-1}(w - C u)) or "direct" (Alg. 1: u = C_a^{-1}((C_a - C)u + w))."""
         _check(self.lib.pint_set_form(self.ctx, FORMS[form]))
+
+    def set_hermitian(self, on: bool = True):
+        """Real-data fast path: solve only the frequencies k <= L/2 (y_{L-k} = conj(y_k))."""
+        _check(self.lib.pint_set_hermitian(self.ctx, 1 if on else 0))
 
     # -- iteration
     def iterate(self, n: int = 1, want_diff: bool = False):

@@ -1,0 +1,77 @@
+"""GPU parity of the real-data fast path (pint_set_hermitian): only the
+frequencies k <= L/2 are solved and y_{L-k} = conj(y_k); compared with the unchanged complex
+oracle (the real-data iterate equals the oracle's up to its roundoff imaginary part)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle.paralpha import ModeOracle, Oracle, mode_coefficients, relative_l2
+from oracle.schedule import adaptive_schedule as oracle_schedule
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def _alphas(p, u0):
+    if p.alpha_mode == "fixed":
+        return [p.alpha_fixed] * p.iters
+    return list(oracle_schedule(p.L, float(np.abs(u0).max()), p.m0, p.iters, p.eps, p.tau)[0])
+
+
+CASES = [W.reduced(4), W.reduced(5)] + [p for p in W.edge_cases() if p.dim == 2] + [
+    W.reduced(5).replace(name="red5_adv2d_32x64_M2_L8", nx=32, ny=64, M=2, L=8)]
+
+
+@pytest.mark.parametrize("form", ["correction", "direct"])
+@pytest.mark.parametrize("p", CASES, ids=lambda p: p.name)
+def test_hermitian_parity(p, form):
+    import paper_2103_12571_b200 as PB
+    u0 = p.u0()
+    if np.iscomplexobj(u0) and np.abs(u0.imag).max() > 0:
+        pytest.skip("complex initial value")
+    a = _alphas(p, u0)
+    s = PB.Solver(p, u0)
+    s.set_form(form)
+    s.set_hermitian(True)
+    s.set_alpha_schedule(a)
+    o = Oracle(p, u0, "dense" if p.M * p.N <= 2048 else "fourier")
+    u = o.initial()
+    for k in range(min(p.iters, 6)):
+        u = o.iterate(u, a[k]) if form == "correction" else o.iterate_direct(u, a[k])
+        s.iterate(1)
+        ug = s.get_iterate()
+        assert relative_l2(ug, u) <= TOL, (k, relative_l2(ug, u))
+        assert np.abs(ug.imag).max() <= TOL * np.abs(ug).max()    # real up to (alpha-amplified) roundoff
+    s.close()
+
+
+def test_hermitian_rejects_complex_data():
+    import paper_2103_12571_b200 as PB
+    p = W.reduced(4)
+    u0 = p.u0().astype(np.complex128) * (1 + 0.5j)
+    s = PB.Solver(p, u0)
+    with pytest.raises(PB.PintError):
+        s.set_hermitian(True)
+    s.close()
+
+
+def test_hermitian_full_size_config5_sampled_modes():
+    import paper_2103_12571_b200 as PB
+    from test_gpu_parity import _gpu_project, _mode_sample
+    p = W.CONFIGS[5]
+    u0 = p.u0()
+    a = _alphas(p, u0)
+    s = PB.Solver(p, u0)
+    s.set_hermitian(True)
+    s.set_alpha_schedule(a)
+    kx, ky = _mode_sample(p, 5)
+    mo = ModeOracle(p, mode_coefficients(p, u0, kx, ky), kx, ky)
+    uh = mo.initial()
+    errs = []
+    for k in range(4):
+        uh = mo.iterate(uh, a[k])
+        s.iterate(1)
+        g = _gpu_project(s, p, kx, ky)
+        errs.append(float(np.linalg.norm((g - uh).ravel()) / np.linalg.norm(uh.ravel())))
+    s.close()
+    assert max(errs) <= TOL, errs
