@@ -50,11 +50,15 @@ struct StaticTables {
   int P, rank;
   // per-pass twiddle tables of the register FFT engine (fft_reg.cuh) for nx, ny
   const double2 *ptwx, *ptwy;
-  // frequency slots whose spatial solves run (2-D): slots[0 .. nsolve); partner[p] = slot of the
-  // conjugate frequency L - k that receives conj(y_k) (-1: none).  Default: every slot, no
-  // partners; Hermitian mode (real data, pint_set_hermitian): the L/2 + 1 slots with k <= L/2.
-  const int *slots, *partner;
+  // Frequency units of the 2-D spatial solves: unit q < nsolve solves slot slots[q].  Default:
+  // every slot (slots[q] = q), X holds the planes.  Hermitian (packed) mode (real data,
+  // pint_set_hermitian): two real spatial points n' and n' + N/2 share one complex time series
+  // Z[l][m][n'] = r(n') + i r(n' + N/2) in the first half of X (N/2 points per plane), units are
+  // the L/2 + 1 frequencies k <= L/2, unit q's full planes live at X + L M N/2 + q M N, and
+  // unitof[p] = q (slot p holds k <= L/2) or -1 - q (slot p holds L - k of unit q).
+  const int *slots, *unitof;
   int nsolve;
+  int packed;
 };
 
 struct Buffers {
@@ -64,6 +68,9 @@ struct Buffers {
   double *red;                // reduction scratch (doubles)
   unsigned *sync;             // 2-D spatial pipeline: per-(stage, batch) completion counters
 };
+
+// packed (Hermitian) mode: start of the unit planes inside the work vector X
+__host__ __device__ inline double2 *unit_planes(const Geometry &g, double2 *X) { return X + (size_t)g.L * g.M * (g.N / 2); }
 
 // ---- launch wrappers (kernels.cu) -----------------------------------------------------------
 // All return cudaGetLastError() after enqueueing on `st`.
@@ -94,6 +101,7 @@ size_t spatial_sync_bytes(int lines);
 cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
                              const double2 *spec, unsigned *sync, int lines, cudaStream_t s);
 bool spatial2d_supported(const Geometry &g);
+bool reg2d_path(const Geometry &g);   // the 2-D path runs spatial2d (else the generic row/column kernels)
 size_t fwd_smem_bytes(const Geometry &g, int T);
 
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,

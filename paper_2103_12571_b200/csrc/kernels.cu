@@ -264,25 +264,63 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   }
 }
 
+// PACK (Hermitian mode, real data): the time series of column n' < N/2 is w = y(n') + i y(n' + N/2);
+// slot p of it is assembled from the unit planes of X2 (unit q = unitof[p]: y_k; -1 - q: conj y_k
+// of the unit of L - k), and the real/imaginary parts of the inverse transform update the two
+// real points n' and n' + N/2 of u (imaginary parts of u are kept at 0).
+template <bool PACK>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tfft_bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
                     double2 *__restrict__ u, int T, unsigned long long *diff_slot, int overwrite) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
   const int lT = 31 - __clz(T);
-  const int per = g.N / T;
+  const int NC = PACK ? g.N / 2 : g.N;     // time-series columns
+  const int per = NC / T;
   const int m = blockIdx.x / per;
   const int n0 = (blockIdx.x - m * per) * T;
   const size_t lstride = (size_t)g.M * g.N;
   const double2 *xb = X2 + (size_t)m * g.N + n0;
   double2 *ub = u + (size_t)m * g.N + n0;
   const int all = g.L * T;
-  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx & (T - 1), p = idx >> lT;
-    cp_async16(sm + sidx<false>(idx), xb + (size_t)p * lstride + t);
+  if (PACK) {
+    // one read of unit q's y_k (points n' and n' + N/2) fills both slots of the tile:
+    // slot p_k <- y(n') + i y(n' + N/2), slot p_{L-k} <- conj y(n') + i conj y(n' + N/2)
+    constexpr int kL = 4;
+    const int units = st.nsolve * T;
+    for (int i0 = threadIdx.x; i0 < units; i0 += kL * blockDim.x) {
+      double2 a[kL], b[kL];
+#pragma unroll
+      for (int k = 0; k < kL; ++k) {
+        const int idx = i0 + k * blockDim.x;
+        if (idx < units) {
+          const int t = idx & (T - 1), q = idx >> lT;
+          const double2 *yp = xb + (size_t)q * g.M * g.N + t;
+          a[k] = __ldg(yp);
+          b[k] = __ldg(yp + g.N / 2);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kL; ++k) {
+        const int idx = i0 + k * blockDim.x;
+        if (idx < units) {
+          const int t = idx & (T - 1), q = idx >> lT;
+          const int p = __ldg(st.slots + q), kf = brev(p, g.logL);
+          const int pc = brev((g.L - kf) & (g.L - 1), g.logL);
+          sm[sidx<false>(p * T + t)] = make_double2(a[k].x - b[k].y, a[k].y + b[k].x);          // a + i b
+          if (pc != p) sm[sidx<false>(pc * T + t)] = make_double2(a[k].x + b[k].y, b[k].x - a[k].y);  // conj a + i conj b
+        }
+      }
+    }
+    __syncthreads();
+  } else {
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+      const int t = idx & (T - 1), p = idx >> lT;
+      cp_async16(sm + sidx<false>(idx), xb + (size_t)p * lstride + t);
+    }
+    cp_async_wait_all();
+    __syncthreads();
   }
-  cp_async_wait_all();
-  __syncthreads();
   if (st.twr) {  // P > 1: inverse four-step twiddle
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x)
       sm[sidx<false>(idx)] = cmulc(sm[sidx<false>(idx)], __ldg(st.twr + (idx >> lT)));
@@ -292,7 +330,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   double dmax = 0.0;
   constexpr int kB = 4;
   for (int b0 = threadIdx.x; b0 < all; b0 += kB * blockDim.x) {
-    double2 uo[kB];
+    double2 uo[kB], uo2[kB];
     double sc[kB];
 #pragma unroll
     for (int k = 0; k < kB; ++k) {
@@ -301,6 +339,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
         const int t = idx & (T - 1), l = idx >> lT;
         const bool need_old = !overwrite || (diff_slot && l == g.L - 1);
         uo[k] = need_old ? ub[(size_t)l * lstride + t] : make_double2(0.0, 0.0);
+        if (PACK) uo2[k] = need_old ? ub[(size_t)l * lstride + t + g.N / 2] : make_double2(0.0, 0.0);
         sc[k] = __ldg(at.scale_bwd + l);
       }
     }
@@ -310,10 +349,20 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), l = idx >> lT;
         const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
-        ub[(size_t)l * lstride + t] = overwrite ? c : cadd(uo[k], c);
-        if (l == g.L - 1) {
-          const double2 dd = overwrite ? csub(c, uo[k]) : c;
-          dmax = fmax(dmax, hypot(dd.x, dd.y));
+        if (PACK) {
+          // real points n' (Re c) and n' + N/2 (Im c); imaginary parts of u stay 0
+          const double2 n1 = make_double2(overwrite ? c.x : uo[k].x + c.x, 0.0);
+          const double2 n2 = make_double2(overwrite ? c.y : uo2[k].x + c.y, 0.0);
+          ub[(size_t)l * lstride + t] = n1;
+          ub[(size_t)l * lstride + t + g.N / 2] = n2;
+          if (l == g.L - 1)
+            dmax = fmax(dmax, fmax(hypot(n1.x - uo[k].x, uo[k].y), hypot(n2.x - uo2[k].x, uo2[k].y)));
+        } else {
+          ub[(size_t)l * lstride + t] = overwrite ? c : cadd(uo[k], c);
+          if (l == g.L - 1) {
+            const double2 dd = overwrite ? csub(c, uo[k]) : c;
+            dmax = fmax(dmax, hypot(dd.x, dd.y));
+          }
         }
       }
     }
@@ -335,12 +384,14 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 // one-point halo staged in shared memory (all M nodes of one l per CTA).  Each warp stages whole
 // halo rows (lanes along x: no index divisions), each thread then evaluates BX*BY/256 points.
 
-template <int M>
+// PACK (Hermitian mode): the CTA also evaluates the partner block BY rows lower by ny/2 and writes
+// Z[l][m][n'] = alpha^{l/L} (Re r(n') + i Re r(n' + N/2)) for its top-half points n' (N/2 per plane).
+template <int M, bool PACK>
 __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
                                                          const double2 *__restrict__ u,
                                                          double2 *__restrict__ X, int BX, int BY) {
-  extern __shared__ double2 sm[];  // [M][BY+2][BX+2]
-  const int bxs = g.nx / BX, bys = g.ny / BY;
+  extern __shared__ double2 sm[];  // [1 + PACK][M][BY+2][BX+2]
+  const int bxs = g.nx / BX, bys = (PACK ? g.ny / 2 : g.ny) / BY;
   int b = blockIdx.x;
   const int bx = b % bxs; b /= bxs;
   const int by = b % bys;
@@ -350,9 +401,11 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   const size_t plane = (size_t)M * g.N;
   const double2 *ul = u + (size_t)l * plane;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < M * H; r += blockDim.x >> 5) {
-    const int j = r / H, yy = r - j * H;
-    const int y = (y0 + yy - 1) & (g.ny - 1);
+  constexpr int NH = PACK ? 2 : 1;
+  for (int r = warp; r < NH * M * H; r += blockDim.x >> 5) {
+    const int hh = r / (M * H), rr = r - hh * M * H;
+    const int j = rr / H, yy = rr - j * H;
+    const int y = (y0 + hh * (g.ny / 2) + yy - 1) & (g.ny - 1);
     const double2 *src = ul + (size_t)j * g.N + ((size_t)y << g.lognx);
     double2 *dst = sm + r * W;
     for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - 1) & (g.nx - 1)));
@@ -363,26 +416,35 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
     const int ty = pt / BX, tx = pt - ty * BX;
     const int n = ((y0 + ty) << g.lognx) + x0 + tx;
-    const double2 base = prev_value(st, l, n);
-    double2 uc[M], Au[M];
+    double2 res[NH][M];
 #pragma unroll
-    for (int j = 0; j < M; ++j) {
-      const double2 *s = sm + (j * H + ty + 1) * W + tx + 1;
-      const double2 c = s[0], a = s[-1], bb = s[1], d = s[-W], e = s[W];
-      uc[j] = c;
-      Au[j].x = g.c0 * c.x + g.cxm * a.x + g.cxp * bb.x + g.cym * d.x + g.cyp * e.x;
-      Au[j].y = g.c0 * c.y + g.cxm * a.y + g.cxp * bb.y + g.cym * d.y + g.cyp * e.y;
+    for (int hh = 0; hh < NH; ++hh) {
+      const double2 base = prev_value(st, l, n + hh * (g.N / 2));
+      double2 uc[M], Au[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const double2 *s = sm + ((hh * M + j) * H + ty + 1) * W + tx + 1;
+        const double2 c = s[0], a = s[-1], bb = s[1], d = s[-W], e = s[W];
+        uc[j] = c;
+        Au[j].x = g.c0 * c.x + g.cxm * a.x + g.cxp * bb.x + g.cym * d.x + g.cyp * e.x;
+        Au[j].y = g.c0 * c.y + g.cxm * a.y + g.cxp * bb.y + g.cym * d.y + g.cyp * e.y;
+      }
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double2 acc = csub(base, uc[m]);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const double q = g.dTQ[m * M + j];
+          acc.x = fma(q, Au[j].x, acc.x);
+          acc.y = fma(q, Au[j].y, acc.y);
+        }
+        res[hh][m] = cscale(acc, sc);
+      }
     }
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      double2 acc = csub(base, uc[m]);
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        const double q = g.dTQ[m * M + j];
-        acc.x = fma(q, Au[j].x, acc.x);
-        acc.y = fma(q, Au[j].y, acc.y);
-      }
-      X[(size_t)l * plane + (size_t)m * g.N + n] = cscale(acc, sc);
+      if (PACK) X[((size_t)l * M + m) * (g.N / 2) + n] = make_double2(res[0][m].x, res[NH - 1][m].x);
+      else X[(size_t)l * plane + (size_t)m * g.N + n] = res[0][m];
     }
   }
 }
@@ -977,6 +1039,7 @@ static bool legacy2d() {
 static bool reg2d(const Geometry &g) {
   return g.dim == 2 && !legacy2d() && spatial2d_supported(g) && g.logL >= 2 && g.logL <= 10;
 }
+bool reg2d_path(const Geometry &g) { return reg2d(g); }
 
 LaunchCfg choose_launch(const Geometry &g) {
   LaunchCfg lc{};
@@ -1070,21 +1133,31 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     });
     rec(s);
   } else {
+    const bool pk = st.packed != 0;   // Hermitian mode: two real points per complex time series
     int BX, BY;
     residual_block(g, BX, BY);
-    const size_t rs = (size_t)g.M * (BX + 2) * (BY + 2) * sizeof(double2);
-    const int rgrid = g.L * (g.nx / BX) * (g.ny / BY);
+    if (pk && BY > g.ny / 2) BY = g.ny / 2;
+    const size_t rs = (size_t)(pk ? 2 : 1) * g.M * (BX + 2) * (BY + 2) * sizeof(double2);
+    const int rgrid = g.L * (g.nx / BX) * ((pk ? g.ny / 2 : g.ny) / BY);
     PINT_DISPATCH_M(g.M, {
-      e = set_smem((const void *)residual2d_kernel<MM>, rs);
-      if (e == cudaSuccess) residual2d_kernel<MM><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
+      if (pk) {
+        e = set_smem((const void *)residual2d_kernel<MM, true>, rs);
+        if (e == cudaSuccess) residual2d_kernel<MM, true><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
+      } else {
+        e = set_smem((const void *)residual2d_kernel<MM, false>, rs);
+        if (e == cudaSuccess) residual2d_kernel<MM, false><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
+      }
     });
     rec(s);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const int T2 = lc.tfft_T;
+    Geometry gt = g;                  // time transform over N (or N/2 packed columns)
+    if (pk) gt.N = g.N / 2;
+    int T2 = lc.tfft_T;
+    while (T2 > gt.N) T2 >>= 1;
     const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
     e = set_smem((const void *)tfft_fwd_kernel, sm2);
-    if (e == cudaSuccess) tfft_fwd_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, b.X, T2);
+    if (e == cudaSuccess) tfft_fwd_kernel<<<g.M * (gt.N / T2), kTileThreads, sm2, s>>>(gt, st, b.X, T2);
     rec(s);
   }
   if (e != cudaSuccess) return e;
@@ -1191,13 +1264,21 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
           bwd_kernel<MM, false><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
       }
     });
+  } else if (st.packed) {
+    int T2 = lc.tfft_T;
+    while (T2 > g.N / 2) T2 >>= 1;
+    const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
+    e = set_smem((const void *)tfft_bwd_kernel<true>, sm2);
+    if (e == cudaSuccess)
+      tfft_bwd_kernel<true><<<g.M * (g.N / 2 / T2), kTileThreads, sm2, s>>>(
+          g, st, at, unit_planes(g, b.X), b.u, T2, (unsigned long long *)diff_slot, overwrite);
   } else {
     const int T2 = lc.tfft_T;
     const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
-    e = set_smem((const void *)tfft_bwd_kernel, sm2);
+    e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
     if (e == cudaSuccess)
-      tfft_bwd_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
-                                                                    (unsigned long long *)diff_slot, overwrite);
+      tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
+                                                                           (unsigned long long *)diff_slot, overwrite);
   }
   rec(s);
   if (e != cudaSuccess) return e;

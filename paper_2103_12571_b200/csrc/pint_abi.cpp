@@ -36,7 +36,7 @@ struct Layout {
   size_t off_alpha, alpha_bytes_each;
   size_t off_red, red_bytes;
   size_t off_sync, sync_bytes;                // 2-D spatial pipeline completion counters
-  size_t off_sym;                             // solve-slot list and conjugate partners [2][L] int
+  size_t off_sym;                             // unit slot list and slot -> unit map [2][L] int
   size_t total;
   bool two_vectors;
 };
@@ -136,7 +136,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   L.two_vectors = (g.dim == 1 && lc.pcr_mode == 1) || P > 1;
   size_t off = 0;
   L.off_X = off;
-  off = align_up(off + L.vec_bytes, 256);
+  // 2-D: one extra M x N unit plane group (Hermitian packed mode: units 0..L/2 after Z)
+  off = align_up(off + L.vec_bytes + (g.dim == 2 ? (size_t)g.M * g.N * sizeof(double2) : 0), 256);
   L.off_Y = L.two_vectors ? off : L.off_X;
   if (L.two_vectors) off = align_up(off + L.vec_bytes, 256);
   L.halo_bytes = P > 1 ? (size_t)g.L * g.N * sizeof(double2) : 0;
@@ -340,12 +341,13 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   }
   {
     std::vector<int> sym(2 * (size_t)g.L);
-    for (int q = 0; q < g.L; ++q) { sym[q] = q; sym[g.L + q] = -1; }
+    for (int q = 0; q < g.L; ++q) { sym[q] = q; sym[g.L + q] = q; }
     int *dsym = (int *)(c->work + lay.off_sym);
     CUDA_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     c->st.slots = dsym;
-    c->st.partner = dsym + g.L;
+    c->st.unitof = dsym + g.L;
     c->st.nsolve = g.L;
+    c->st.packed = 0;
   }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
             (double *)(c->work + lay.off_red), (unsigned *)(c->work + lay.off_sync)};
@@ -872,29 +874,34 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
   if (on) {
-    if (g.dim != 2) return fail(PINT_ERR_INVALID, "Hermitian mode: 2-D problems only in this build");
+    if (g.dim != 2 || !reg2d_path(g) || g.ny < 2)
+      return fail(PINT_ERR_INVALID, "Hermitian mode: 2-D grids of the register FFT engine, 4 <= L <= 1024, only");
     if (c->P != 1) return fail(PINT_ERR_INVALID, "Hermitian mode is single-rank only");
-    if (g.L < 2) return fail(PINT_ERR_INVALID, "Hermitian mode needs L >= 2");
     for (int n = 0; n < g.N; ++n)
       if (c->u0[2 * n + 1] != 0.0) return fail(PINT_ERR_INVALID, "Hermitian mode needs a real u0");
   }
-  // slot p holds frequency k = bitrev(p) (1 rank); solve the slots with k <= L/2, in slot order
-  std::vector<int> sym(2 * (size_t)g.L, -1);
+  // slot p holds frequency k = bitrev(p) (1 rank).  Units: the slots with k <= L/2 in slot order.
+  std::vector<int> sym(2 * (size_t)g.L, 0);
   int ns = 0;
-  for (int p = 0; p < g.L; ++p) {
-    const int k = bitrev(p, g.logL);
-    if (!on) {
-      sym[ns++] = p;
-    } else if (k <= g.L / 2) {
-      sym[ns++] = p;
-      const int kc = (g.L - k) % g.L;
-      if (kc != k) sym[g.L + p] = bitrev(kc, g.logL);
+  if (!on) {
+    for (int p = 0; p < g.L; ++p) { sym[p] = p; sym[g.L + p] = p; }
+    ns = g.L;
+  } else {
+    std::vector<int> unit_of_k(g.L, -1);
+    for (int p = 0; p < g.L; ++p) {
+      const int k = bitrev(p, g.logL);
+      if (k <= g.L / 2) { unit_of_k[k] = ns; sym[ns++] = p; }
+    }
+    for (int p = 0; p < g.L; ++p) {
+      const int k = bitrev(p, g.logL);
+      sym[g.L + p] = k <= g.L / 2 ? unit_of_k[k] : -1 - unit_of_k[g.L - k];
     }
   }
   int *dsym = (int *)(c->work + c->lay.off_sym);
   CUDA_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->st.nsolve = ns;
+  c->st.packed = on ? 1 : 0;
   c->hermitian = on != 0;
   return PINT_OK;
 }

@@ -22,8 +22,9 @@
 // Direct form (Alg. 1 as printed): the C stage synthesizes its input spectrum sig_q * r0hat (no
 // R stage); see launch_direct_front in kernels.cu.
 //
-// Solved slots: st.slots[0 .. nsolve) (all L, or the L/2 + 1 slots with k <= L/2 in Hermitian
-// mode, where the I stage also writes conj(y) to the conjugate frequency's slot st.partner[p]).
+// Units: st.slots[0 .. nsolve) (every slot; Hermitian mode: the L/2 + 1 slots with k <= L/2,
+// whose R stage unpacks X_k from the packed real-data spectra Z_k, Z_{L-k} and whose planes live in
+// the unit area of X, internal.h).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -121,15 +122,50 @@ __device__ __forceinline__ void node_transform(double2 *sm, int ls, int M, int r
 // ---- R item: rows y0 .. y0 + YR - 1 of slot p, all M nodes ---------------------------------
 template <class PX>
 __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
-                                       const double2 *twx,
-                                       double2 *__restrict__ X, int p, int y0, int YR, bool node) {
+                                       const double2 *twx, double2 *__restrict__ xp, int p, int y0, int YR,
+                                       bool node, const double2 *__restrict__ za, const double2 *__restrict__ zb) {
   constexpr int LX = PX::LOGN, NX = PX::N;
   const int M = g.M, nl = M * YR;
-  double2 *xp = X + (size_t)p * M * g.N;
-  for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
-    const int x = i & (NX - 1), l = i >> LX;
-    const int yy = l / M, m = l - yy * M;
-    cp_async16(tile + (size_t)l * NX + rfft::F<PX>(x), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX) + x);
+  if (za) {
+    // Hermitian (packed) mode: unpack X_k from Z_k = za, Z_{L-k} = zb ([m][N/2] each):
+    // top half rows X_k = (Z_k + conj Z_{L-k}) / 2, bottom half X_k = (Z_k - conj Z_{L-k}) / 2i;
+    // za == zb (k = 0, L/2): X_k = Re Z_k (top), Im Z_k (bottom)
+    const int hy = g.ny / 2;
+    constexpr int kL = 4;   // loads batched for memory-level parallelism
+    for (int i0 = threadIdx.x; i0 < nl * NX; i0 += kL * blockDim.x) {
+      double2 a[kL], b[kL];
+#pragma unroll
+      for (int k = 0; k < kL; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < nl * NX) {
+          const int x = i & (NX - 1), l = i >> LX;
+          const int yy = l / M, m = l - yy * M;
+          const int y = y0 + yy;
+          const size_t off = (size_t)m * (g.N / 2) + ((size_t)(y < hy ? y : y - hy) << LX) + x;
+          a[k] = __ldg(za + off);
+          b[k] = __ldg(zb + off);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kL; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < nl * NX) {
+          const int x = i & (NX - 1), l = i >> LX;
+          const int top = y0 + l / M < hy;
+          double2 v;
+          if (za == zb) v = top ? make_double2(a[k].x, 0.0) : make_double2(a[k].y, 0.0);
+          else if (top) v = make_double2(0.5 * (a[k].x + b[k].x), 0.5 * (a[k].y - b[k].y));
+          else v = make_double2(0.5 * (a[k].y + b[k].y), 0.5 * (b[k].x - a[k].x));   // (a - conj b) / (2i)
+          tile[(size_t)l * NX + rfft::F<PX>(x)] = v;
+        }
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
+      const int x = i & (NX - 1), l = i >> LX;
+      const int yy = l / M, m = l - yy * M;
+      cp_async16(tile + (size_t)l * NX + rfft::F<PX>(x), xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX) + x);
+    }
   }
   if (node && threadIdx.x < M * M) nt[threadIdx.x] = __ldg(at.Sinv + (size_t)p * M * M + threadIdx.x);
   cp_async_wait_all();
@@ -159,12 +195,11 @@ __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at,
 // ---- I item: inverse rows ------------------------------------------------------------------
 template <class PX>
 __device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
-                                       const double2 *twx,
-                                       double2 *__restrict__ X, int p, int y0, int YR, bool node, int partner) {
+                                       const double2 *twx, double2 *__restrict__ xp, int p, int y0, int YR,
+                                       bool node) {
   constexpr int LX = PX::LOGN, NX = PX::N;
   constexpr int R = 1 << PX::BL;
   const int M = g.M, nl = M * YR;
-  double2 *xp = X + (size_t)p * M * g.N;
   const int l = threadIdx.x / PX::TPL, tau = threadIdx.x - l * PX::TPL;
   const bool wrun = (int)(threadIdx.x & ~31) / PX::TPL < nl;   // warp holds at least one line
   const int lc = l < nl ? l : nl;                                 // nl: dummy line (see r_item)
@@ -187,22 +222,17 @@ __device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at,
     node_transform<PX>(tile, NX, M, YR, nt);
     __syncthreads();
   }
-  // Hermitian mode: the conjugate frequency's slot receives conj(y) (same rows, all nodes)
-  double2 *xc = partner >= 0 ? X + (size_t)partner * M * g.N : nullptr;
   for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
     const int x = i & (NX - 1), li = i >> LX;
     const int y2 = li / M, m2 = li - y2 * M;
-    const size_t off = (size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x;
-    const double2 v = tile[(size_t)li * NX + rfft::F<PX>(x)];
-    xp[off] = v;
-    if (xc) xc[off] = make_double2(v.x, -v.y);
+    xp[(size_t)m2 * g.N + ((size_t)(y0 + y2) << LX) + x] = tile[(size_t)li * NX + rfft::F<PX>(x)];
   }
 }
 
 // ---- C item: columns (S-slots) kx0 .. kx0 + TC - 1 of line q -----------------------------------
 template <class PX, class PY>
 __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st, const AlphaTables &at,
-                                       double2 *tile, const double2 *twy, double2 *__restrict__ X,
+                                       double2 *tile, const double2 *twy, double2 *__restrict__ xl,
                                        const double2 *__restrict__ spec, int q, int kx0, int TC) {
   constexpr int LX = PX::LOGN, LY = PY::LOGN;
   constexpr int NX = 1 << LX, NY = PY::N;
@@ -210,7 +240,6 @@ __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st
   const int pad = TC >= 8 ? 1 : 8 / TC;
   const int ls = NY + pad;
   const int lT = 31 - __clz(TC);
-  double2 *xl = X + (size_t)q * g.N;
   const int l = threadIdx.x / PY::TPL, tau = threadIdx.x - l * PY::TPL;
   const bool wrun = (int)(threadIdx.x & ~31) / PY::TPL < TC;   // warp holds at least one column
   const int lc = l < TC ? l : TC;                                 // TC: dummy line (see r_item)
@@ -299,15 +328,29 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
       if (stage == kStC) {
         if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
         const int li = kk / cPerLine;                       // line within the batch
-        const int q = __ldg(st.slots + b * sp.B + li / g.M) * g.M + li % g.M;
-        c_item<PX, PY>(g, st, at, tile, twy, X, sp.synth ? spec : nullptr, q, (kk - li * cPerLine) * sp.TC, sp.TC);
+        const int un = b * sp.B + li / g.M, m = li % g.M;   // unit, node
+        const int q = __ldg(st.slots + un) * g.M + m;       // table line (slot, node)
+        double2 *plane = (st.packed ? unit_planes(g, X) + (size_t)un * g.M * g.N : X + (size_t)q / g.M * g.M * g.N) +
+                         (size_t)m * g.N;
+        c_item<PX, PY>(g, st, at, tile, twy, plane, sp.synth ? spec : nullptr, q, (kk - li * cPerLine) * sp.TC, sp.TC);
       } else {
         if (stage == kStI) wait_count(sync + kStC * sp.nbatch + b, (unsigned)sp.nC);
         const int pi = kk / riPerBatch;                     // slot within the batch
         const int y0 = (kk - pi * riPerBatch) * sp.YR;
-        const int slot = __ldg(st.slots + b * sp.B + pi);
-        if (stage == kStR) r_item<PX>(g, at, tile, nt, twx, X, slot, y0, sp.YR, node);
-        else i_item<PX>(g, at, tile, nt, twx, X, slot, y0, sp.YR, node, __ldg(st.partner + slot));
+        const int un = b * sp.B + pi;                       // unit
+        const int slot = __ldg(st.slots + un);
+        double2 *xp = st.packed ? unit_planes(g, X) + (size_t)un * g.M * g.N : X + (size_t)slot * g.M * g.N;
+        if (stage == kStR) {
+          const double2 *za = nullptr, *zb = nullptr;
+          if (st.packed) {   // Z_k and Z_{L-k} (slot of the conjugate frequency) in the packed first half
+            const int k = brev(slot, g.logL), pc = brev((g.L - k) & (g.L - 1), g.logL);
+            za = X + (size_t)slot * g.M * (g.N / 2);
+            zb = X + (size_t)pc * g.M * (g.N / 2);
+          }
+          r_item<PX>(g, at, tile, nt, twx, xp, slot, y0, sp.YR, node, za, zb);
+        } else {
+          i_item<PX>(g, at, tile, nt, twx, xp, slot, y0, sp.YR, node);
+        }
       }
       publish(sync + stage * sp.nbatch + b);
     }
