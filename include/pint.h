@@ -131,14 +131,18 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
 #define PINT_FORM_DIRECT 1
 pint_status pint_set_form(pint_ctx *c, int32_t form);
 
-/* Real-data fast path, spatial half.  For real A, w and alpha (every
+/* Real-data fast path.  For real A, w and alpha (every
  * config: real u0, b == 0) the alpha-scaled time spectrum is Hermitian, x_{L-k} = conj(x_k)
  * (P:164-171 with real J and V^{-1} = F* J^{-1}), and so is the solution of the frequency-block
  * systems (the blocks of L - k are the complex conjugates of those of k).  on = 1: only the
  * L/2 + 1 frequencies k <= L/2 are node-transformed and solved; y_{L-k} = conj(y_k) is written
  * by the solve.  Same result as on = 0 up to the roundoff imaginary part of the iterate (which
- * on = 1 projects out).  Requirements: dim == 2, nranks == 1, L >= 2, u0 real (imaginary parts
- * exactly 0; pint_set_initial_value then rejects non-real data).  Errors: PINT_ERR_INVALID. */
+ * on = 1 projects out).  The time transforms run on complex series that pack two real points,
+ * z_l(n') = r_l(n') + i r_l(n' + N/2), so they do half the work; the solves unpack X_k from the
+ * slots of k and L - k and the backward pass repacks both slots from one read.  The iterate stays
+ * complex128 in u_dev with zero imaginary parts.  Requirements: nranks == 1, u0 real (imaginary
+ * parts exactly 0; pint_set_initial_value then rejects non-real data), 2-D: grids of the register
+ * FFT engine, 4 <= L <= 1024; 1-D: N >= 8.  Errors: PINT_ERR_INVALID. */
 pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
 
 /* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:

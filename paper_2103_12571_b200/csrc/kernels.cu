@@ -86,7 +86,11 @@ constexpr int kTileThreads = 256;
 constexpr int kTileMinBlocks = 3;   // time tiles: radix <= 8, 80 registers
 constexpr int kSpaceMinBlocks = 2;  // spatial FFT passes: radix <= 16, 128 registers
 
-template <int M, bool RESID, bool NODE>
+// PACK (Hermitian mode, real data, 1 rank): column t of the tile is the complex time series
+// r(n') + i r(n' + N/2), n' = n0 + t < N/2; after the FFT the node step unpacks X_k from the slots
+// of k and L - k (both in the tile), applies S_k^{-1} and writes unit q's lines (X + q M N) at n'
+// and n' + N/2.
+template <int M, bool RESID, bool NODE, bool PACK = false>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     fwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ u,
                double2 *__restrict__ X, int T) {
@@ -105,8 +109,15 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       double2 r[M];
       residual_point<M>(g, st, u, l, n0 + t, r);
       const double sc = __ldg(at.scale_fwd + l);
+      if (PACK) {
+        double2 r2[M];
+        residual_point<M>(g, st, u, l, n0 + t + g.N / 2, r2);
 #pragma unroll
-      for (int m = 0; m < M; ++m) sm[sidx<false>((l * M + m) * T + t)] = cscale(r[m], sc);
+        for (int m = 0; m < M; ++m) sm[sidx<false>((l * M + m) * T + t)] = make_double2(r[m].x * sc, r2[m].x * sc);
+      } else {
+#pragma unroll
+        for (int m = 0; m < M; ++m) sm[sidx<false>((l * M + m) * T + t)] = cscale(r[m], sc);
+      }
     }
   } else {
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
@@ -118,7 +129,36 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   __syncthreads();
   // (ii) L-point DIF FFT along l for the M*T columns
   fft_dif<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);
-  if (NODE) {
+  if (PACK) {
+    // (iii) unpack X_k (k <= L/2) from the slots of k and L - k, then S_k^{-1}; one (unit, m) per item
+    for (int it = threadIdx.x; it < st.nsolve * M; it += blockDim.x) {
+      const int m = it % M, q = it / M;
+      const int p = __ldg(st.slots + q), kf = brev(p, g.logL), pc = brev((L - kf) & (L - 1), g.logL);
+      double2 srow[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
+      double2 *dst = X + ((size_t)q * M + m) * g.N + n0;
+      for (int t = 0; t < T; ++t) {
+        double2 at_ = make_double2(0.0, 0.0), ab = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const double2 a = sm[sidx<false>((p * M + j) * T + t)], b = sm[sidx<false>((pc * M + j) * T + t)];
+          double2 xt, xb;
+          if (pc == p) {
+            xt = make_double2(a.x, 0.0);
+            xb = make_double2(a.y, 0.0);
+          } else {
+            xt = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+            xb = make_double2(0.5 * (a.y + b.y), 0.5 * (b.x - a.x));
+          }
+          at_ = cfma(srow[j], xt, at_);
+          ab = cfma(srow[j], xb, ab);
+        }
+        dst[t] = at_;
+        dst[t + g.N / 2] = ab;
+      }
+    }
+  } else if (NODE) {
     // (iii) node transform, one (p, m) row of T outputs per work item (row m of S_p^{-1} loaded once)
     for (int it = threadIdx.x; it < rows; it += blockDim.x) {
       const int m = it % M, p = it / M;
@@ -146,7 +186,10 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 
 __device__ __forceinline__ unsigned long long dbl_bits(double v) { return (unsigned long long)__double_as_longlong(v); }
 
-template <int M, bool NODE>
+// PACK (Hermitian mode, 1 rank): unit q's solved lines at n' and n' + N/2 are node-transformed
+// (G_k^{-1} S_k) and repacked into the slots of k and L - k (w = y(n') + i y(n' + N/2) and its
+// conjugate counterpart); the inverse FFT's real / imaginary parts update u at n' and n' + N/2.
+template <int M, bool NODE, bool PACK = false>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
                double2 *__restrict__ u, int T, unsigned long long *diff_slot, int overwrite) {
@@ -157,21 +200,49 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   const int L = g.L;
   const int rows = L * M;
   const int all = rows * T;
-  // async tile load X2[p][m][n0..n0+T) -> sm, and an L2 prefetch of the u tile for the update
-  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
-    const int t = idx & (T - 1), row = idx >> lT;
-    cp_async16(sm + sidx<false>(idx), X2 + (size_t)row * g.N + n0 + t);
+  if (PACK) {
+    for (int it = threadIdx.x; it < st.nsolve * T; it += blockDim.x) {
+      const int t = it & (T - 1), q = it >> lT;
+      const int p = __ldg(st.slots + q), kf = brev(p, g.logL), pc = brev((L - kf) & (L - 1), g.logL);
+      double2 vt[M], vb[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const double2 *src = X2 + ((size_t)q * M + j) * g.N + n0 + t;
+        vt[j] = __ldg(src);
+        vb[j] = __ldg(src + g.N / 2);
+      }
+      const double2 *SG = at.SG + (size_t)p * M * M;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double2 yt = make_double2(0.0, 0.0), yb = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const double2 c = __ldg(SG + m * M + j);
+          yt = cfma(c, vt[j], yt);
+          yb = cfma(c, vb[j], yb);
+        }
+        sm[sidx<false>((p * M + m) * T + t)] = make_double2(yt.x - yb.y, yt.y + yb.x);               // yt + i yb
+        if (pc != p) sm[sidx<false>((pc * M + m) * T + t)] = make_double2(yt.x + yb.y, yb.x - yt.y);  // conj yt + i conj yb
+      }
+    }
+    __syncthreads();
+  } else {
+    // async tile load X2[p][m][n0..n0+T) -> sm, and an L2 prefetch of the u tile for the update
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+      const int t = idx & (T - 1), row = idx >> lT;
+      cp_async16(sm + sidx<false>(idx), X2 + (size_t)row * g.N + n0 + t);
+    }
+    if (!overwrite)
+      for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
+    cp_async_wait_all();
+    __syncthreads();
   }
-  if (!overwrite)
-    for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
-  cp_async_wait_all();
-  __syncthreads();
   if (!NODE && st.twr) {  // P > 1: inverse four-step twiddle e^{+2 pi i rank kappa/L}
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x)
       sm[sidx<false>(idx)] = cmulc(sm[sidx<false>(idx)], __ldg(st.twr + (idx >> lT) / M));
     __syncthreads();
   }
-  if (NODE) {
+  if (NODE && !PACK) {
     // (v-a) y = G_p^{-1} S_p x2 in place, one (p, t) per work item
     const int items = L * T;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
@@ -196,7 +267,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   double dmax = 0.0;
   constexpr int kB = 4;
   for (int base = threadIdx.x; base < all; base += kB * blockDim.x) {
-    double2 uo[kB];
+    double2 uo[kB], uo2[kB];
     double sc[kB];
 #pragma unroll
     for (int k = 0; k < kB; ++k) {
@@ -205,6 +276,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
         const int t = idx & (T - 1), row = idx >> lT;
         const bool need_old = !overwrite || (diff_slot && row / M == L - 1);
         uo[k] = need_old ? u[(size_t)row * g.N + n0 + t] : make_double2(0.0, 0.0);
+        if (PACK) uo2[k] = need_old ? u[(size_t)row * g.N + n0 + t + g.N / 2] : make_double2(0.0, 0.0);
         sc[k] = __ldg(at.scale_bwd + row / M);
       }
     }
@@ -214,10 +286,19 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), row = idx >> lT;
         const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
-        u[(size_t)row * g.N + n0 + t] = overwrite ? c : cadd(uo[k], c);   // direct form: u = C_a^{-1} r
-        if (row / M == L - 1) {
-          const double2 dd = overwrite ? csub(c, uo[k]) : c;
-          dmax = fmax(dmax, hypot(dd.x, dd.y));
+        if (PACK) {   // real points n' (Re c) and n' + N/2 (Im c); imaginary parts of u stay 0
+          const double2 n1 = make_double2(overwrite ? c.x : uo[k].x + c.x, 0.0);
+          const double2 n2 = make_double2(overwrite ? c.y : uo2[k].x + c.y, 0.0);
+          u[(size_t)row * g.N + n0 + t] = n1;
+          u[(size_t)row * g.N + n0 + t + g.N / 2] = n2;
+          if (row / M == L - 1)
+            dmax = fmax(dmax, fmax(hypot(n1.x - uo[k].x, uo[k].y), hypot(n2.x - uo2[k].x, uo2[k].y)));
+        } else {
+          u[(size_t)row * g.N + n0 + t] = overwrite ? c : cadd(uo[k], c);   // direct form: u = C_a^{-1} r
+          if (row / M == L - 1) {
+            const double2 dd = overwrite ? csub(c, uo[k]) : c;
+            dmax = fmax(dmax, hypot(dd.x, dd.y));
+          }
         }
       }
     }
@@ -463,9 +544,16 @@ constexpr int kPcrIPT = 16;   // items per thread held in registers per level
 
 // Lines of length nq at element stride R (residue classes mod R), T consecutive classes per CTA.
 // Applies coefficient levels j_off .. nlev-1 (the last is the pair level) and multiplies by 1/e.
+// Line indices run over the solved units (Hermitian mode: k <= L/2); the factor tables are indexed
+// by the unit's slot: tline = slots[line / M] M + line % M.
+__device__ __forceinline__ int table_line(const Geometry &g, const int *slots, int line) {
+  return __ldg(slots + line / g.M) * g.M + line % g.M;
+}
+
 __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry g, AlphaTables at,
                                                                   double2 *__restrict__ X, int R, int T,
-                                                                  int j_off, const double2 *__restrict__ r0) {
+                                                                  int j_off, const double2 *__restrict__ r0,
+                                                                  const int *__restrict__ slots) {
   extern __shared__ double2 sm[];  // [nq][T]
   const int lT = 31 - __clz(T);
   const int N = g.N;
@@ -475,13 +563,14 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
   const int line = blockIdx.x / groups;
   const int rr = (blockIdx.x - line * groups) * T;
   double2 *xl = X + (size_t)line * N;
+  const int tline = table_line(g, slots, line);
   const int items = nq * T;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it & (T - 1), q = it >> lT;
-    sm[it] = r0 ? cmul(__ldg(at.sig + line), __ldg(r0 + (size_t)q * R + rr + tt)) : xl[(size_t)q * R + rr + tt];
+    sm[it] = r0 ? cmul(__ldg(at.sig + tline), __ldg(r0 + (size_t)q * R + rr + tt)) : xl[(size_t)q * R + rr + tt];
   }
   __syncthreads();
-  const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
+  const double2 *coef = at.pcr + (size_t)tline * g.logN * 2;
   for (int jj = 0; jj < lognq; ++jj) {
     const int j = j_off + jj;
     const double2 pj = __ldg(coef + 2 * j), qj = __ldg(coef + 2 * j + 1);
@@ -508,7 +597,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
     }
     __syncthreads();
   }
-  const double2 ie = __ldg(at.inv_e + line);
+  const double2 ie = __ldg(at.inv_e + tline);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it & (T - 1), q = it >> lT;
     xl[(size_t)q * R + rr + tt] = cmul(sm[it], ie);
@@ -565,7 +654,8 @@ __device__ __forceinline__ void pcr_block_level(double2 (&y)[E], int b, int S, d
 // (coalesced over the T columns).  Level operators commute (circulant), so the order is free.
 template <int E>
 __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, AlphaTables at, double2 *__restrict__ X,
-                                                         int R, int T, int j_off, const double2 *__restrict__ r0) {
+                                                         int R, int T, int j_off, const double2 *__restrict__ r0,
+                                                         const int *__restrict__ slots) {
   extern __shared__ double2 sm[];  // [nq][T], swizzled
   const int N = g.N;
   const int nq = N / R;
@@ -577,15 +667,16 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
   const int line = blockIdx.x / groups;
   const int rr = (blockIdx.x - line * groups) * T;
   double2 *xl = X + (size_t)line * N;
+  const int tline = table_line(g, slots, line);
   const int items = nq * T;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int tt = it & (T - 1), q = it >> lT;
-    if (r0) sm[swz(it)] = cmul(__ldg(at.sig + line), __ldg(r0 + (size_t)q * R + rr + tt));  // direct form
+    if (r0) sm[swz(it)] = cmul(__ldg(at.sig + tline), __ldg(r0 + (size_t)q * R + rr + tt));  // direct form
     else cp_async16(sm + swz(it), xl + (size_t)q * R + rr + tt);
   }
   cp_async_wait_all();
   __syncthreads();
-  const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
+  const double2 *coef = at.pcr + (size_t)tline * g.logN * 2;
   double2 y[E];
   {  // block arrangement: thread -> (column, block b); the S lanes of a column are consecutive
     const int b = threadIdx.x & (S - 1), col = threadIdx.x >> logS;
@@ -618,7 +709,7 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
 #pragma unroll
     for (int k = 0; k < E; ++k) y[k] = nv[k];
   }
-  const double2 ie = __ldg(at.inv_e + line);
+  const double2 ie = __ldg(at.inv_e + tline);
 #pragma unroll
   for (int k = 0; k < E; ++k) xl[(size_t)(c + (k << logS)) * R + rr + col] = cmul(y[k], ie);
 }
@@ -631,7 +722,7 @@ constexpr int kChunkIPT = 10;
 __global__ void __launch_bounds__(kChunkThreads) pcr_chunk_kernel(const Geometry g, AlphaTables at,
                                                                   const double2 *__restrict__ X,
                                                                   double2 *__restrict__ Y, int C, int H,
-                                                                  int jA) {
+                                                                  int jA, const int *__restrict__ slots) {
   extern __shared__ double2 sm[];  // [C + 2H]
   const int N = g.N;
   const int chunks = N / C;
@@ -641,7 +732,7 @@ __global__ void __launch_bounds__(kChunkThreads) pcr_chunk_kernel(const Geometry
   const int S = C + 2 * H;
   for (int i = threadIdx.x; i < S; i += blockDim.x) sm[i] = __ldg(xl + ((n0 - H + i) & (N - 1)));
   __syncthreads();
-  const double2 *coef = at.pcr + (size_t)line * g.logN * 2;
+  const double2 *coef = at.pcr + (size_t)table_line(g, slots, line) * g.logN * 2;
   int lo = 0;
   for (int j = 0; j < jA; ++j) {
     const int h = 1 << j;
@@ -1117,13 +1208,17 @@ static void residual_block(const Geometry &g, int &BX, int &BY) {
 
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                            const AlphaTables &at, const Buffers &b, cudaStream_t s) {
-  const int T = lc.fwd_T;
+  int T = lc.fwd_T;
+  if (st.packed) while (T > g.N / 2) T >>= 1;
   const size_t smem = fwd_smem_bytes(g, T);
-  const int grid = g.N / T;
+  const int grid = (st.packed ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
   if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
-      if (st.P == 1) {
+      if (st.packed) {
+        e = set_smem((const void *)fwd_kernel<MM, true, true, true>, smem);
+        if (e == cudaSuccess) fwd_kernel<MM, true, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+      } else if (st.P == 1) {
         e = set_smem((const void *)fwd_kernel<MM, true, true>, smem);
         if (e == cudaSuccess) fwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
       } else {
@@ -1167,12 +1262,12 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
 cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                          const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out) {
   cudaError_t e = cudaSuccess;
-  const int lines = g.L * g.M;
+  const int lines = st.nsolve * g.M;   // solved units x nodes (Hermitian mode: k <= L/2)
   if (g.dim == 1) {
     if (lc.pcr_mode == 0) {
       const size_t smem = (size_t)g.N * sizeof(double2);
       if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-      pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, nullptr);
+      pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, nullptr, st.slots);
       rec(s);
       *out = b.X;
     } else {
@@ -1185,17 +1280,17 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
         const size_t smr = (size_t)nq * Tr * sizeof(double2);
         if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
-        pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, nullptr);
+        pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, nullptr, st.slots);
       } else {
         if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-        pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, nullptr);
+        pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, nullptr, st.slots);
       }
       rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       const int C = lc.pcr_chunk, H = R;
       smem = (size_t)(C + 2 * H) * sizeof(double2);
       if ((e = set_smem((const void *)pcr_chunk_kernel, smem)) != cudaSuccess) return e;
-      pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smem, s>>>(g, at, b.X, b.Y, C, H, jOff);
+      pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smem, s>>>(g, at, b.X, b.Y, C, H, jOff, st.slots);
       rec(s);
       *out = b.Y;
     }
@@ -1248,13 +1343,18 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
 cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                             const AlphaTables &at, const Buffers &b, const double2 *x2,
                             double *diff_slot, cudaStream_t s, int overwrite) {
-  const int T = lc.fwd_T;
+  int T = lc.fwd_T;
+  if (st.packed) while (T > g.N / 2) T >>= 1;
   const size_t smem = fwd_smem_bytes(g, T);
-  const int grid = g.N / T;
+  const int grid = (st.packed && g.dim == 1 ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
   if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
-      if (st.P == 1) {
+      if (st.packed) {
+        e = set_smem((const void *)bwd_kernel<MM, true, true>, smem);
+        if (e == cudaSuccess)
+          bwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
+      } else if (st.P == 1) {
         e = set_smem((const void *)bwd_kernel<MM, true>, smem);
         if (e == cudaSuccess)
           bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
@@ -1342,7 +1442,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
                                 const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
                                 double2 **out) {
   cudaError_t e = cudaSuccess;
-  const int lines = g.L * g.M;
+  const int lines = st.nsolve * g.M;   // solved units x nodes (Hermitian mode: k <= L/2)
   if (reg2d(g)) {
     e = launch_spatial2d(g, st, at, b.X, r0, b.sync, st.nsolve * g.M, s);
     rec(s);
@@ -1367,7 +1467,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   if (lc.pcr_mode == 0) {
     const size_t smem = (size_t)g.N * sizeof(double2);
     if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-    pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, r0);
+    pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, r0, st.slots);
     rec(s);
     *out = b.X;
     return cudaGetLastError();
@@ -1380,18 +1480,18 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
     const size_t smr = (size_t)nq * Tr * sizeof(double2);
     if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
-    pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, r0);
+    pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, r0, st.slots);
   } else {
     const size_t smem = (size_t)nq * T * sizeof(double2);
     if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-    pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, r0);
+    pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, r0, st.slots);
   }
   rec(s);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int C = lc.pcr_chunk, H = R;
   const size_t smc = (size_t)(C + 2 * H) * sizeof(double2);
   if ((e = set_smem((const void *)pcr_chunk_kernel, smc)) != cudaSuccess) return e;
-  pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smc, s>>>(g, at, b.X, b.Y, C, H, jOff);
+  pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smc, s>>>(g, at, b.X, b.Y, C, H, jOff, st.slots);
   rec(s);
   *out = b.Y;
   return cudaGetLastError();

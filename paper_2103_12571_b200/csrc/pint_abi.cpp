@@ -874,8 +874,9 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
   if (on) {
-    if (g.dim != 2 || !reg2d_path(g) || g.ny < 2)
+    if (g.dim == 2 && (!reg2d_path(g) || g.ny < 2))
       return fail(PINT_ERR_INVALID, "Hermitian mode: 2-D grids of the register FFT engine, 4 <= L <= 1024, only");
+    if (g.dim == 1 && (g.N < 8 || g.L < 2)) return fail(PINT_ERR_INVALID, "Hermitian mode needs N >= 8 and L >= 2");
     if (c->P != 1) return fail(PINT_ERR_INVALID, "Hermitian mode is single-rank only");
     for (int n = 0; n < g.N; ++n)
       if (c->u0[2 * n + 1] != 0.0) return fail(PINT_ERR_INVALID, "Hermitian mode needs a real u0");

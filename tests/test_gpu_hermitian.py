@@ -1,6 +1,7 @@
-"""GPU parity of the real-data fast path (pint_set_hermitian): only the
-frequencies k <= L/2 are solved and y_{L-k} = conj(y_k); compared with the unchanged complex
-oracle (the real-data iterate equals the oracle's up to its roundoff imaginary part)."""
+"""GPU parity of the real-data fast path (pint_set_hermitian): packed real
+time transforms, only the frequencies k <= L/2 solved, y_{L-k} = conj(y_k); 1-D and 2-D, both
+forms, against the unchanged complex oracle (the real-data iterate equals the oracle's up to its
+roundoff imaginary part)."""
 import numpy as np
 import pytest
 
@@ -18,7 +19,9 @@ def _alphas(p, u0):
     return list(oracle_schedule(p.L, float(np.abs(u0).max()), p.m0, p.iters, p.eps, p.tau)[0])
 
 
-CASES = [W.reduced(4), W.reduced(5)] + [p for p in W.edge_cases() if p.dim == 2] + [
+CASES = [W.CONFIGS[1], W.CONFIGS[2], W.reduced(3), W.reduced(4), W.reduced(5),
+         W.CONFIGS[3].replace(name="twopass_N16384_L8", nx=16384, L=8, iters=4)] + [
+    p for p in W.edge_cases() if p.N >= 8] + [
     W.reduced(5).replace(name="red5_adv2d_32x64_M2_L8", nx=32, ny=64, M=2, L=8)]
 
 
