@@ -12,7 +12,7 @@
 // inverse radix-R DFT from bit-reversed slots), passes in reverse order, unnormalised (N x).
 //
 // Between passes the values go through shared memory (one write, one barrier, one read per
-// pass).  Element P of a line lives at swizzled offset F(P): F XORs the low three 16-byte slot
+// pass); a radix-2/4 third pass runs across lanes with warp shuffles instead (SHL).  Element P of a line lives at swizzled offset F(P): F XORs the low three 16-byte slot
 // bits with higher position bits so that every quarter-warp access of every pass of the plan is
 // bank-conflict free (tests/test_fft_plan.py checks it).  Twiddles: per-pass tables of the
 // powers tw_i[k s_i + j] = w_{m_i}^{j 2^k}, k < B_i (host long double, staged in shared memory,
@@ -40,6 +40,11 @@ struct Plan {
   static constexpr int E = 1 << B0;
   static constexpr int TPL = N / E;
   static constexpr int BL = NP == 3 ? B2 : (NP == 2 ? B1 : B0);   // radix (log2) of the last pass
+  // Option: three-pass plans with a radix-2/4 last pass can run it across the 2^B2 lanes that hold
+  // one block (warp shuffles, values stay at their pass-1 positions), saving the third shared-memory
+  // exchange.  Parity-green, but measured slower on config 5 (spatial2d 89 vs 79-84 ms: the shuffle
+  // window costs ~500 B of register spills at the 128-register cap), so it is off.
+  static constexpr bool SHL = false && NP == 3 && B2 <= 2;
   static constexpr int b(int p) { return p == 0 ? B0 : (p == 1 ? B1 : B2); }
   static constexpr int logm(int p) { return p == 0 ? LOGN : (p == 1 ? LOGN - B0 : LOGN - B0 - B1); }
   static constexpr int logs(int p) { return logm(p) - b(p); }
@@ -169,6 +174,63 @@ __device__ __forceinline__ void line_sync(int l) {
   }
 }
 
+// SHL plans: the last pass (radix R = 2^B2, blocks of R consecutive positions) across the R lanes
+// j = tau mod R that hold one block (pass 1 left position beta m1 + j + R t in lane (beta, j),
+// value t).  DIF stage with half h: the lower lane keeps a + b, the upper (b_partner - own) w_{2h}^e
+// (e = j mod h); after the stages lane j holds the block's DFT at bitrev(j), i.e. exactly what the
+// shared-memory pass leaves at that position.  lane_dit undoes it (conjugate twiddle, unnormalised).
+template <class P>
+__device__ __forceinline__ void lane_dif(double2 (&v)[P::E], int tau) {
+  constexpr int BR = P::B2;
+  const int j = tau & ((1 << BR) - 1);
+#pragma unroll
+  for (int st = 0; st < BR; ++st) {
+    const int h = (1 << BR) >> (st + 1);
+    const bool low = (j & h) == 0;
+    const bool rot = h == 2 && (j & 1);   // w_4^1 = -i (only non-trivial twiddle for R <= 4)
+#pragma unroll
+    for (int t0 = 0; t0 < P::E; t0 += 4) {
+#pragma unroll
+      for (int t = t0; t < t0 + 4; ++t) {
+        double2 r;
+        r.x = __shfl_xor_sync(0xffffffffu, v[t].x, h);
+        r.y = __shfl_xor_sync(0xffffffffu, v[t].y, h);
+        if (low) {
+          v[t] = cadd(v[t], r);
+        } else {
+          const double2 d = csub(r, v[t]);
+          v[t] = rot ? make_double2(d.y, -d.x) : d;
+        }
+      }
+      asm volatile("" ::: "memory");   // bound the shuffle window (register pressure)
+    }
+  }
+}
+template <class P>
+__device__ __forceinline__ void lane_dit(double2 (&v)[P::E], int tau) {
+  constexpr int BR = P::B2;
+  const int j = tau & ((1 << BR) - 1);
+#pragma unroll
+  for (int st = BR - 1; st >= 0; --st) {
+    const int h = (1 << BR) >> (st + 1);
+    const bool low = (j & h) == 0;
+    const bool rot = h == 2 && (j & 1);   // conj(w_4^1) = +i
+#pragma unroll
+    for (int t0 = 0; t0 < P::E; t0 += 4) {
+#pragma unroll
+      for (int t = t0; t < t0 + 4; ++t) {
+        double2 w = v[t];
+        if (!low && rot) w = make_double2(-w.y, w.x);
+        double2 r;
+        r.x = __shfl_xor_sync(0xffffffffu, w.x, h);
+        r.y = __shfl_xor_sync(0xffffffffu, w.y, h);
+        v[t] = low ? cadd(w, r) : csub(r, w);
+      }
+      asm volatile("" ::: "memory");
+    }
+  }
+}
+
 // Forward transform of a line whose values sit in shared memory at `line` (swizzled, natural
 // order).  Returns with the values of the LAST pass in registers (positions pos<NP-1>).
 // Contains NP - 1 exchanges; the first statement is a read, so the caller must have barriered
@@ -184,7 +246,9 @@ __device__ __forceinline__ void forward_regs(double2 (&v)[P::E], double2 *line, 
     from_smem<P, 1>(v, line, tau);
     dif<P, 1>(v, tau, tw);
   }
-  if constexpr (P::NP >= 3) {
+  if constexpr (P::NP >= 3 && P::SHL) {
+    lane_dif<P>(v, tau);
+  } else if constexpr (P::NP >= 3) {
     line_sync<P>(l);
     to_smem<P, 1>(v, line, tau);
     line_sync<P>(l);
@@ -206,7 +270,9 @@ __device__ __forceinline__ void forward_from_smem(double2 (&v)[P::E], double2 *l
 template <class P>
 __device__ __forceinline__ void inverse_in_regs(double2 (&v)[P::E], double2 *line, int l, int tau,
                                                 const double2 *tw) {
-  if constexpr (P::NP >= 3) {
+  if constexpr (P::NP >= 3 && P::SHL) {
+    lane_dit<P>(v, tau);
+  } else if constexpr (P::NP >= 3) {
     dit<P, 2>(v, tau, tw);
     to_smem<P, 2>(v, line, tau);
     line_sync<P>(l);
@@ -230,19 +296,26 @@ __device__ __forceinline__ int natural_pos(int tau, int t) { return tau + P::TPL
 // S-layout: storage slot of last-pass value (u, t) of thread tau in spectral (bit-reversed
 // position) data kept in global memory: slot q = t * (N / R_L) + beta, beta = tau + TPL u; the
 // lanes of a warp write consecutive slots.  slot_to_pos inverts it.
+// (SHL plans: register i = u R_L + t stays at pass-1 position pos<1>(tau, 0, i); slot q = i TPL + tau.)
 template <class P>
 __device__ __forceinline__ int s_slot(int tau, int u, int t) {
-  return (t << (P::LOGN - P::BL)) + tau + P::TPL * u;
+  if constexpr (P::SHL) return ((u << P::BL) + t) * P::TPL + tau;   // register i = u R_L + t
+  else return (t << (P::LOGN - P::BL)) + tau + P::TPL * u;
 }
 template <class P>
 __device__ __forceinline__ int slot_to_pos(int q) {
-  constexpr int sh = P::LOGN - P::BL;
-  return ((q & ((1 << sh) - 1)) << P::BL) + (q >> sh);
+  if constexpr (P::SHL) {
+    return pos<P, 1>(q % P::TPL, 0, q / P::TPL);
+  } else {
+    constexpr int sh = P::LOGN - P::BL;
+    return ((q & ((1 << sh) - 1)) << P::BL) + (q >> sh);
+  }
 }
 // position of last-pass value (u, t) of thread tau (its frequency is bitrev_N of it)
 template <class P>
 __device__ __forceinline__ int last_pos(int tau, int u, int t) {
-  return pos<P, P::NP - 1>(tau, u, t);
+  if constexpr (P::SHL) return pos<P, 1>(tau, 0, (u << P::BL) + t);
+  else return pos<P, P::NP - 1>(tau, u, t);
 }
 
 }  // namespace rfft
