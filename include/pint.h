@@ -145,6 +145,19 @@ pint_status pint_set_form(pint_ctx *c, int32_t form);
  * FFT engine, 4 <= L <= 1024; 1-D: N >= 8.  Errors: PINT_ERR_INVALID. */
 pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
 
+/* Algorithm 2 of the paper, the stopping driver: gamma = L (3 eps + tau) ||w||_inf;
+ * while m_k > tol: m_{k+1} = 2 sqrt(m_k gamma), alpha_{k+1} = sqrt(gamma / m_k), one iteration
+ * (pint_iterate, current form), stop as soon as ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf <= tol.  Also
+ * stops at max_iter and when m_k < 4 gamma (alpha would exceed 1/2).  The whole alpha
+ * schedule (a function of gamma / m0 only) is built up front (replaces the current schedule);
+ * one 8-byte read-back per iteration.  Outputs: *iters = iterations done; diffs (nullable,
+ * max_iter entries) = the consecutive-iterate norms; m_out (nullable, max_iter + 1 entries) =
+ * m_0 .. m_iters; *stop_reason (nullable): 0 consecutive iterates <= tol, 1 m_k <= tol,
+ * 2 max_iter, 3 m_k < 4 gamma.  Errors: PINT_ERR_INVALID (m0, tol <= 0, max_iter outside
+ * [1, PINT_MAX_SCHEDULE]), those of pint_set_alpha_schedule and pint_iterate. */
+pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double tol, int32_t max_iter,
+                       int32_t *iters, double *diffs, double *m_out, int32_t *stop_reason);
+
 /* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:
  * nullable; if given, n_iter doubles receive ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf (Alg. 2 line 7,
  * P:421) and the call synchronises the stream.  PINT_ERR_SCHEDULE if the schedule would run out. */

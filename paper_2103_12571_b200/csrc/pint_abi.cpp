@@ -907,6 +907,44 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   return PINT_OK;
 }
 
+pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double tol, int32_t max_iter,
+                       int32_t *iters, double *diffs, double *m_out, int32_t *stop_reason) {
+  if (!c || !iters) return fail(PINT_ERR_INVALID, "NULL argument");
+  if (!(m0 > 0) || !(tol > 0) || max_iter < 1 || max_iter > PINT_MAX_SCHEDULE || !(eps >= 0) || !(tau >= 0))
+    return fail(PINT_ERR_INVALID, "need m0 > 0, tol > 0, eps, tau >= 0, 1 <= max_iter <= PINT_MAX_SCHEDULE");
+  double w_inf = 0;
+  for (int n = 0; n < c->g.N; ++n) w_inf = std::fmax(w_inf, std::hypot(c->u0[2 * n], c->u0[2 * n + 1]));
+  const ld gam = (ld)c->prob.L * (3.0L * eps + tau) * w_inf;          // Alg. 2 line 1
+  if (!(gam > 0)) return fail(PINT_ERR_INVALID, "gamma = L(3 eps + tau)||w||_inf must be > 0");
+  std::vector<double> alphas, ms{m0};
+  int reason = 2;
+  ld mk = m0;
+  while ((int)alphas.size() < max_iter) {
+    if (mk <= tol) { reason = 1; break; }                              // while m_k > tol
+    if (4 * gam > mk) { reason = 3; break; }                           // alpha would exceed 1/2
+    alphas.push_back((double)sqrtl(gam / mk));                         // alpha_{k+1} = sqrt(gamma/m_k)
+    mk = 2 * sqrtl(mk * gam);                                          // m_{k+1} = 2 sqrt(m_k gamma)
+    ms.push_back((double)mk);
+  }
+  *iters = 0;
+  if (!alphas.empty()) {
+    pint_status st = pint_set_alpha_schedule(c, alphas.data(), (int32_t)alphas.size());
+    if (st != PINT_OK) return st;
+  }
+  for (size_t i = 0; i < alphas.size(); ++i) {
+    double d = 0;
+    pint_status st = pint_iterate(c, 1, &d);
+    if (st != PINT_OK) return st;
+    if (diffs) diffs[i] = d;
+    *iters = (int32_t)i + 1;
+    if (d <= tol) { reason = 0; break; }                              // ||u_L^{k+1} - u_L^k|| <= tol
+  }
+  if (m_out)
+    for (int i = 0; i <= *iters; ++i) m_out[i] = ms[i];
+  if (stop_reason) *stop_reason = reason;
+  return PINT_OK;
+}
+
 pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, double *S, double *Sinv,
                              double *d_km) {
   if (!c || a < 0 || a >= (int)c->h_S.size() || k < 0 || k >= c->prob.L)

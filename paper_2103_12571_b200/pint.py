@@ -28,7 +28,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
-           "pint_set_form", "pint_set_hermitian"]
+           "pint_set_form", "pint_set_hermitian", "pint_solve"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH):
         "pint_group_residual_norm": (i32, [ctypes.POINTER(vp), i32, dp, dp]),
         "pint_set_form": (i32, [vp, i32]),
         "pint_set_hermitian": (i32, [vp, i32]),
+        "pint_solve": (i32, [vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, i32,
+                             ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -187,6 +189,17 @@ class Solver:
     def set_form(self, form: str):
         """"correction" (default, u += C_a^{-1}(w - C u)) or "direct" (Alg. 1: u = C_a^{-1}((C_a - C)u + w))."""
         _check(self.lib.pint_set_form(self.ctx, FORMS[form]))
+
+    def solve(self, m0: float, tol: float, max_iter: int, eps: float = 2.0 ** -52, tau: float = 0.0):
+        """Algorithm 2: adaptive alphas, stop on consecutive iterates <= tol (C ABI)."""
+        it, why = ctypes.c_int32(0), ctypes.c_int32(0)
+        d = np.zeros(max_iter)
+        m = np.zeros(max_iter + 1)
+        _check(self.lib.pint_solve(self.ctx, m0, eps, tau, tol, max_iter, ctypes.byref(it), _dp(d), _dp(m),
+                                   ctypes.byref(why)))
+        n = it.value
+        return {"iters": n, "diffs": d[:n], "m": m[:n + 1],
+                "stop": ["consecutive iterates", "m_k <= tol", "max_iter", "m_k < 4 gamma"][why.value]}
 
     def set_hermitian(self, on: bool = True):
         """Real-data fast path: solve only the frequencies k <= L/2 (y_{L-k} = conj(y_k))."""

@@ -73,3 +73,29 @@ def test_direct_form_refused_when_sharded():
         grp.ranks[0].set_form("direct")
     assert e.value.status == 1
     grp.close()
+
+
+@pytest.mark.parametrize("form", ["correction", "direct"])
+@pytest.mark.parametrize("p", [W.reduced(3), W.reduced(5)], ids=lambda p: p.name)
+def test_algorithm2_driver(p, form):
+    """pint_solve (Algorithm 2): the schedule is the oracle's recurrence, the driver stops
+    at the first consecutive-iterate norm <= tol, and the iterate it stops at matches the oracle
+    run for the same number of iterations with the same alphas."""
+    import paper_2103_12571_b200 as PB
+    u0 = p.u0()
+    tol = 1e-9 * float(np.abs(u0).max())
+    s = PB.Solver(p, u0)
+    s.set_form(form)
+    r = s.solve(p.m0, tol, 12, p.eps, p.tau)
+    n = r["iters"]
+    assert 1 <= n <= 12 and r["stop"] in ("consecutive iterates", "m_k <= tol", "max_iter")
+    if r["stop"] == "consecutive iterates":
+        assert r["diffs"][-1] <= tol and (n == 1 or np.all(r["diffs"][:-1] > tol))
+    a_or, m_or = oracle_schedule(p.L, float(np.abs(u0).max()), p.m0, n, p.eps, p.tau)
+    np.testing.assert_allclose(r["m"], m_or[:n + 1], rtol=1e-13)
+    o = Oracle(p, u0, "dense" if p.M * p.N <= 2048 else "fourier")
+    u = o.initial()
+    for k in range(n):
+        u = o.iterate(u, a_or[k]) if form == "correction" else o.iterate_direct(u, a_or[k])
+    assert relative_l2(s.get_iterate(), u) <= TOL
+    s.close()
