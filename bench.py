@@ -277,8 +277,15 @@ def main():
     else:
         kms = None
     algo_tab = dict(ALGO_BYTES_DIRECT if args.form == "direct" else ALGO_BYTES)
-    if args.hermitian:   # L/2 + 1 of L frequency slots solved; the I stage also writes the conjugates
-        algo_tab["spatial2d_kernel"] = 32 if args.form == "direct" else 56
+    if args.hermitian:
+        # packed real data: time series of N/2 complex columns (8 B per unknown), L/2 + 1 of L
+        # frequencies solved (unit data ~8 B per unknown), u stays complex128 (16 B per unknown)
+        algo_tab.update({"residual2d_kernel": 24, "tfft_fwd_kernel": 16, "fwd_kernel": 24,
+                         "pcr_classes_kernel": 16, "pcr_chunk_kernel": 16, "spatial2d_kernel": 56,
+                         "tfft_bwd_kernel": 40, "bwd_kernel": 40})
+        if args.form == "direct":
+            algo_tab.update({"spatial2d_kernel": 24, "tfft_bwd_kernel": 24, "bwd_kernel": 24,
+                             "pcr_classes_kernel": 8, "pcr_chunk_kernel": 16})
     model_bytes = sum(algo_tab.get(n_, 32) for n_ in names)
     iteration_roof = {"model_bytes_per_unknown": model_bytes,
                       "achieved_gbs": model_bytes * p.U / world / (ms * 1e-3) / 1e9,
