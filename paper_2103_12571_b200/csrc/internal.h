@@ -93,6 +93,7 @@ struct SpatialPlan {
   int nRI, nC;                // items per batch of the R/I stages and of the C stage
   int synth;                  // direct form: C synthesizes sig_q * r0hat, no R stage
   int nstage, rounds;         // 3 (R, C, I) or 2 (C, I); nbatch + nstage - 1
+  int skip;                   // timing experiments only (PINT_SP_SKIP): bit s = stage s does no work
 };
 SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth);
 int spatial_maxb(const Geometry &g);   // largest radix (log2) of the spatial FFT plan in use

@@ -325,7 +325,9 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
         ++si;
       }
       const int stage = first + si, b = j - si;
-      if (stage == kStC) {
+      if ((sp.skip >> stage) & 1) {
+        // timing experiments only (PINT_SP_SKIP): the stage's items do no work
+      } else if (stage == kStC) {
         if (!sp.synth) wait_count(sync + kStR * sp.nbatch + b, (unsigned)sp.nRI);
         const int li = kk / cPerLine;                       // line within the batch
         const int un = b * sp.B + li / g.M, m = li % g.M;   // unit, node
@@ -392,6 +394,8 @@ SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth) {
   sp.nC = sp.B * g.M * (g.nx / sp.TC);
   sp.synth = synth ? 1 : 0;
   sp.nstage = synth ? 2 : 3;
+  const char *sk = getenv("PINT_SP_SKIP");   // timing experiments only: bit s skips stage s (R, C, I)
+  sp.skip = sk ? atoi(sk) : 0;
   sp.rounds = sp.nbatch + sp.nstage - 1;
   return sp;
 }
