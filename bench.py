@@ -196,6 +196,7 @@ def main():
     ap.add_argument("--grid", type=int, default=0, help="profiling only: override nx (and ny in 2-D)")
     ap.add_argument("--form", default="correction", choices=["correction", "direct"],
                     help="iteration form: correction (north star, default) or direct (Alg. 1 as printed)")
+    ap.add_argument("--no-sequential", action="store_true", help="skip the sequential Radau IIA baseline")
     ap.add_argument("--hermitian", action="store_true",
                     help="real-data fast path (SURVEY 8(f) row 1): solve only frequencies k <= L/2")
     args = ap.parse_args()
@@ -347,6 +348,25 @@ def main():
                "d2h_bytes_per_step": 16 * p.N, "ms_per_step": ems,
                "what": "per step: H2D u0 (pinned) -> pint_iterate(1) -> D2H u_{L-1,M-1} (solution at T)"}
 
+    # ---- sequential Radau IIA baseline on the same GPU (2-D, 1 rank) ------------
+    seq = None
+    if world == 1 and p.dim == 2 and not args.no_sequential:
+        s.sequential()                                   # warm-up
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.sequential()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sms_ = e0.elapsed_time(e1)
+        s.set_initial_value(u0, reset=True)
+        tol = 1e-10 * float(np.abs(u0).max())
+        r = s.solve(p.m0, tol, 40, p.eps, p.tau)        # Algorithm 2 to tol (host-timed, not the metric)
+        seq = {"ms": sms_, "steps": p.L, "per_step_ms": sms_ / p.L,
+               "paralpha_iterations_to_tol": r["iters"], "tol_rel": 1e-10, "stop": r["stop"],
+               "paralpha_time_to_tol_ms": r["iters"] * ms,
+               "what": "pint_sequential: L collocation steps, each an FFT-diagonal solve on the same kernels"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample, _ = cpu_oracle_rate(p, target_s=args.cpu_target_s)
@@ -364,7 +384,7 @@ def main():
                            "l2": "inputs larger than L2 (no flush)" if 16 * p.U > 126e6 else "L2-resident",
                            "parallelism": "single GPU" if world == 1 else
                            f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sequential_baseline": seq,
                 "gpu_launches": (nlaunch if world == 1 else nlaunch + 3) * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     s.close()

@@ -155,6 +155,15 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
  * m_0 .. m_iters; *stop_reason (nullable): 0 consecutive iterates <= tol, 1 m_k <= tol,
  * 2 max_iter, 3 m_k < 4 gamma.  Errors: PINT_ERR_INVALID (m0, tol <= 0, max_iter outside
  * [1, PINT_MAX_SCHEDULE]), those of pint_set_alpha_schedule and pint_iterate. */
+/* Sequential Radau IIA baseline: overwrites u_dev with the
+ * sequential collocation solution u* of C u = w, step by step: (I - dT Q (x) A) U_l = 1 (x)
+ * u_{l-1,M-1} (u_{-1} = u0), solved per step through Q = V diag(lambda) V^{-1} and the FFT
+ * diagonal spatial solves on the same kernels as the iteration (one spatial pipeline launch per
+ * step).  The fixed point of the iteration; used as the honest single-GPU time-stepping baseline.
+ * Synchronous.  Requirements: dim == 2 (grids of the spatial pipeline), nranks == 1.  Errors:
+ * PINT_ERR_INVALID, PINT_ERR_NOT_DIAGONALIZABLE, PINT_ERR_CUDA. */
+pint_status pint_sequential(pint_ctx *c);
+
 pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double tol, int32_t max_iter,
                        int32_t *iters, double *diffs, double *m_out, int32_t *stop_reason);
 

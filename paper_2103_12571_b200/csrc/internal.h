@@ -126,6 +126,11 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
                                 double2 **out);
 int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc);
 const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, int i);
+// Sequential Radau IIA baseline (2-D, one step): the spectrum of r0 (in place), then the direct-form
+// synthesized spatial pipeline with the Q-eigen tables `at` (sig, shift, SG = V) writing the M
+// stage planes of the step at `out`.
+cudaError_t launch_sequential_step(const Geometry &g, const StaticTables &st, const AlphaTables &at,
+                                   const Buffers &b, double2 *r0, double2 *out, cudaStream_t s);
 cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
                                  double *out2, cudaStream_t s);
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,

@@ -1438,6 +1438,25 @@ cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const St
   return cudaGetLastError();
 }
 
+cudaError_t launch_sequential_step(const Geometry &g, const StaticTables &st, const AlphaTables &at,
+                                   const Buffers &b, double2 *r0, double2 *out, cudaStream_t s) {
+  int YG = 4096 / g.nx;
+  if (YG < 1) YG = 1;
+  if (YG > g.ny) YG = g.ny;
+  cudaError_t e;
+  size_t smr = (size_t)YG * g.nx * sizeof(double2);
+  if ((e = set_smem((const void *)plane_rows_dif_kernel, smr)) != cudaSuccess) return e;
+  plane_rows_dif_kernel<<<g.ny / YG, kFftThreads, smr, s>>>(g, st, r0, YG);
+  int Tp = 4096 / g.ny;
+  if (Tp < 1) Tp = 1;
+  if (Tp > g.nx) Tp = g.nx;
+  size_t smc = (size_t)g.ny * Tp * sizeof(double2);
+  if ((e = set_smem((const void *)plane_cols_dif_kernel, smc)) != cudaSuccess) return e;
+  plane_cols_dif_kernel<<<g.nx / Tp, kFftThreads, smc, s>>>(g, st, r0, Tp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return launch_spatial2d(g, st, at, out, r0, b.sync, g.M, s);
+}
+
 cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                                 const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
                                 double2 **out) {

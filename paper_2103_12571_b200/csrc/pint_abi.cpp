@@ -37,6 +37,7 @@ struct Layout {
   size_t off_red, red_bytes;
   size_t off_sync, sync_bytes;                // 2-D spatial pipeline completion counters
   size_t off_sym;                             // unit slot list and slot -> unit map [2][L] int
+  size_t off_seq;                             // sequential baseline: Q eigen tables (sig, shift, V)
   size_t total;
   bool two_vectors;
 };
@@ -170,6 +171,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   off = align_up(off + L.sync_bytes, 256);
   L.off_sym = off;
   off = align_up(off + 2 * (size_t)g.L * sizeof(int), 256);
+  L.off_seq = off;
+  off = align_up(off + (size_t)(2 * g.M + g.M * g.M) * sizeof(double2), 256);
   L.total = off;
   return L;
 }
@@ -942,6 +945,52 @@ pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double to
   if (m_out)
     for (int i = 0; i <= *iters; ++i) m_out[i] = ms[i];
   if (stop_reason) *stop_reason = reason;
+  return PINT_OK;
+}
+
+pint_status pint_sequential(pint_ctx *c) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  const Geometry &g = c->g;
+  if (g.dim != 2 || !reg2d_path(g) || c->P != 1)
+    return fail(PINT_ERR_INVALID, "sequential baseline: 2-D grids of the spatial pipeline, one rank");
+  const int M = g.M;
+  // Q = V diag(lambda) V^{-1} (Radau IIA): step l solves (I - dT Q (x) A) U_l = 1 (x) u_{l-1,M-1}
+  // as z_m = (V^{-1} 1)_m (I - dT lambda_m A)^{-1} u_{l-1,M-1}, U_l = (V (x) I) z
+  std::vector<cld> B((size_t)M * M), lam, S, Si;
+  for (int i = 0; i < M * M; ++i) B[i] = c->Q[i];
+  ld cond, gap;
+  if (!eig_diagonalize(M, B, lam, S, Si, cond, gap)) return fail(PINT_ERR_NOT_DIAGONALIZABLE, "Q not diagonalisable");
+  const ld dT = (ld)c->prob.T / c->prob.L;
+  std::vector<double2> tab(2 * M + M * M);
+  for (int m = 0; m < M; ++m) {
+    cld rs = 0;
+    for (int j = 0; j < M; ++j) rs += Si[(size_t)m * M + j];
+    tab[m] = make_double2((double)rs.real(), (double)rs.imag());                       // sig
+    const cld sh = lam[m] * dT;
+    tab[M + m] = make_double2((double)sh.real(), (double)sh.imag());                   // shift
+    for (int j = 0; j < M; ++j) {
+      const cld v = S[(size_t)m * M + j];
+      tab[2 * M + m * M + j] = make_double2((double)v.real(), (double)v.imag());       // V
+    }
+  }
+  double2 *dtab = (double2 *)(c->work + c->lay.off_seq);
+  CUDA_TRY(c, cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+  AlphaTables at{};
+  at.sig = dtab;
+  at.shift = dtab + M;
+  at.SG = dtab + 2 * M;
+  StaticTables st = c->st;       // one "slot" (slot 0) per step, never packed
+  st.nsolve = 1;
+  st.packed = 0;
+  Buffers b = buffers(c);
+  double2 *r0 = (double2 *)(c->work + c->lay.off_r0);
+  for (int l = 0; l < g.L; ++l) {
+    const double2 *prev = l == 0 ? c->st.u0 : c->u + ((size_t)(l - 1) * M + (M - 1)) * g.N;
+    CUDA_TRY(c, cudaMemcpyAsync(r0, prev, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(c, launch_sequential_step(g, st, at, b, r0, c->u + (size_t)l * M * g.N, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PINT_OK;
 }
 

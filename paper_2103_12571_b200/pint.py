@@ -28,7 +28,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
-           "pint_set_form", "pint_set_hermitian", "pint_solve"]
+           "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH):
         "pint_set_hermitian": (i32, [vp, i32]),
         "pint_solve": (i32, [vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, i32,
                              ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32)]),
+        "pint_sequential": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -200,6 +201,10 @@ class Solver:
         n = it.value
         return {"iters": n, "diffs": d[:n], "m": m[:n + 1],
                 "stop": ["consecutive iterates", "m_k <= tol", "max_iter", "m_k < 4 gamma"][why.value]}
+
+    def sequential(self):
+        """Overwrite the iterate with the sequential Radau IIA solution (2-D baseline)."""
+        _check(self.lib.pint_sequential(self.ctx))
 
     def set_hermitian(self, on: bool = True):
         """Real-data fast path: solve only the frequencies k <= L/2 (y_{L-k} = conj(y_k))."""
