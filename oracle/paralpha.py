@@ -3,7 +3,8 @@
 Definition (PAPER.md, with the block matrix of P:115-135 — DESIGN.md reading R2):
     C     = I_L (x) C_coll + E (x) H,      C_coll = I_MN - dT Q (x) A,  H = H_M (x) I_N
     C_a   = I_L (x) C_coll + E_a (x) H     (eq. prec, P:145-156)
-    w     = (u0 + v_1, v_2, ..., v_L),     v_l = 0 since b == 0 in every config
+    w     = (u0 + v_1, v_2, ..., v_L),     v_l = dT (Q (x) I) b_l, b_l[m] = b(t_l + tau_m dT)
+            (P:105); v = 0 in every config (b == 0), optional forcing otherwise
 and the iteration, in correction form (reading R1; algebraically eq. Riteration):
     u^{k+1} = u^k + C_{a_k}^{-1} (w - C u^k).
 C_a^{-1} is applied exactly as the paper's three steps s1-s3 with
@@ -69,11 +70,18 @@ def E_matrix(L: int, alpha: float | None = None) -> np.ndarray:
 # ---------------------------------------------------------------------------------------------
 # residual (step (i))
 
-def w_vector(p, u0: np.ndarray) -> np.ndarray:
-    """w = (u0 replicated over the M nodes, 0, ..., 0) for b == 0."""
-    w = np.zeros((p.L, p.M, p.N), dtype=np.complex128)
-    w[0, :, :] = u0[None, :]
+def w_vector(p, u0: np.ndarray, v: np.ndarray | None = None) -> np.ndarray:
+    """w = (u0 replicated over the M nodes + v_1, v_2, ..., v_L); v = None: b == 0."""
+    w = np.zeros((p.L, p.M, p.N), dtype=np.complex128) if v is None else np.array(v, dtype=np.complex128)
+    w[0, :, :] += u0[None, :]
     return w
+
+
+def forcing_vector(p, tab: Tableau, b) -> np.ndarray:
+    """v_l = dT (Q (x) I) b_l with b_l[m] = b(t_l + tau_m dT) (collocation integral of the forcing,
+    P:105); b(t) returns the N-vector b(., t)."""
+    bl = np.array([[b((l + tab.t[m]) * p.dT) for m in range(p.M)] for l in range(p.L)], dtype=np.complex128)
+    return p.dT * np.einsum("mj,ljn->lmn", tab.Q, bl)
 
 
 def apply_C(p, tab: Tableau, u: np.ndarray) -> np.ndarray:
@@ -86,9 +94,9 @@ def apply_C(p, tab: Tableau, u: np.ndarray) -> np.ndarray:
     return Cu - Hu_prev                                      # E has -1 on the sub-diagonal
 
 
-def residual(p, tab: Tableau, u: np.ndarray, u0: np.ndarray) -> np.ndarray:
+def residual(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, v: np.ndarray | None = None) -> np.ndarray:
     """r = w - C u."""
-    return w_vector(p, u0) - apply_C(p, tab, u)
+    return w_vector(p, u0, v) - apply_C(p, tab, u)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -145,10 +153,11 @@ class FourierBlockSolver:
 # one iteration (Alg. 1 order: residual, J^-1 + DFT, block solves, inverse DFT + J, update)
 
 class Oracle:
-    def __init__(self, p, u0: np.ndarray, tier: str = "auto"):
+    def __init__(self, p, u0: np.ndarray, tier: str = "auto", v: np.ndarray | None = None):
         self.p = p
         self.tab = Tableau(p.M)
         self.u0 = np.asarray(u0, dtype=np.complex128)
+        self.v = v                                          # forcing part of w (None: b == 0)
         if tier == "auto":
             tier = "dense" if p.M * p.N <= 2048 else "fourier"
         self.tier = tier
@@ -160,7 +169,7 @@ class Oracle:
 
     def iterate(self, u: np.ndarray, alpha: float) -> np.ndarray:
         p = self.p
-        r = residual(p, self.tab, u, self.u0)                               # (i)
+        r = residual(p, self.tab, u, self.u0, self.v)                       # (i)
         x = np.einsum("kl,lmn->kmn", V_inverse(p.L, alpha), r)              # (ii)  eq. s1
         y = self.solver.solve(alpha, x)                                     # (iii)-(iv) eq. s2
         c = np.einsum("lk,kmn->lmn", V_matrix(p.L, alpha), y)               # (v)   eq. s3
@@ -168,16 +177,16 @@ class Oracle:
 
     def iterate_direct(self, u: np.ndarray, alpha: float) -> np.ndarray:
         """Alg. 1 as printed (eq. Riteration): u^{k+1} = C_a^{-1} ((C_a - C) u + w).
-        (C_a - C) u + w = w - alpha e_1 (x) H u_L: only block 0 is non-zero."""
+        (C_a - C) u + w = w - alpha e_1 (x) H u_L: only block 0 of (C_a - C) u is non-zero."""
         p = self.p
-        r = w_vector(p, self.u0)
+        r = w_vector(p, self.u0, self.v)
         r[0, :, :] -= alpha * u[p.L - 1, p.M - 1, :][None, :]
         x = np.einsum("kl,lmn->kmn", V_inverse(p.L, alpha), r)
         y = self.solver.solve(alpha, x)
         return np.einsum("lk,kmn->lmn", V_matrix(p.L, alpha), y)
 
     def residual_norms(self, u: np.ndarray):
-        r = residual(self.p, self.tab, u, self.u0)
+        r = residual(self.p, self.tab, u, self.u0, self.v)
         return float(np.linalg.norm(r.ravel())), float(np.abs(r).max())
 
 
@@ -264,32 +273,37 @@ def assemble_C(p, tab: Tableau, alpha: float | None = None) -> np.ndarray:
     return np.kron(np.eye(p.L), Ccoll) + np.kron(E_matrix(p.L, alpha), H)
 
 
-def brute_force_iterate_direct(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, alpha: float) -> np.ndarray:
+def brute_force_iterate_direct(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, alpha: float,
+                               v: np.ndarray | None = None) -> np.ndarray:
     """u^{k+1} = solve(C_a, (C_a - C) u + w) with C, C_a assembled densely (eq. Riteration)."""
     C = assemble_C(p, tab)
     Ca = assemble_C(p, tab, alpha)
-    w = w_vector(p, u0).reshape(-1)
+    w = w_vector(p, u0, v).reshape(-1)
     return np.linalg.solve(Ca, (Ca - C) @ u.reshape(-1) + w).reshape(u.shape)
 
 
-def brute_force_iterate(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, alpha: float) -> np.ndarray:
+def brute_force_iterate(p, tab: Tableau, u: np.ndarray, u0: np.ndarray, alpha: float,
+                        v: np.ndarray | None = None) -> np.ndarray:
     C = assemble_C(p, tab)
     Ca = assemble_C(p, tab, alpha)
-    w = w_vector(p, u0).reshape(-1)
+    w = w_vector(p, u0, v).reshape(-1)
     uf = u.reshape(-1)
     return (uf + np.linalg.solve(Ca, w - C @ uf)).reshape(u.shape)
 
 
-def sequential_solution(p, tab: Tableau, u0: np.ndarray) -> np.ndarray:
+def sequential_solution(p, tab: Tableau, u0: np.ndarray, v: np.ndarray | None = None) -> np.ndarray:
     """u* of C u = w by L sequential collocation steps:
-    (I - dT Q (x) A) u_l = 1 (x) u_{l-1, M-1},  u_{-1, M-1} := u0.  Spatial-FFT solve per step."""
+    (I - dT Q (x) A) u_l = 1 (x) u_{l-1, M-1} + v_l,  u_{-1, M-1} := u0.  Spatial-FFT solve per step."""
     lam = FourierBlockSolver(p, tab).lam
     B = np.eye(p.M)[None] - p.dT * lam[:, None, None] * tab.Q[None]      # (N, M, M)
     out = np.empty((p.L, p.M, p.N), dtype=np.complex128)
     prev = np.asarray(u0, dtype=np.complex128)
     for l in range(p.L):
         rhs = np.fft.fft2(prev.reshape(p.ny, p.nx)).reshape(-1)
-        yh = np.linalg.solve(B, np.repeat(rhs[:, None], p.M, axis=1)[:, :, None])[:, :, 0]
+        rhs = np.repeat(rhs[:, None], p.M, axis=1)                        # (N, M)
+        if v is not None:
+            rhs = rhs + np.fft.fft2(v[l].reshape(p.M, p.ny, p.nx), axes=(-2, -1)).reshape(p.M, p.N).T
+        yh = np.linalg.solve(B, rhs[:, :, None])[:, :, 0]
         y = np.fft.ifft2(yh.T.reshape(p.M, p.ny, p.nx), axes=(-2, -1)).reshape(p.M, p.N)
         out[l] = y
         prev = y[p.M - 1]
