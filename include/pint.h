@@ -101,7 +101,8 @@ size_t pint_workspace_bytes(const pint_problem *p, const pint_dist *d);
  * aligned; local steps j hold global steps rank + nranks*j), set here to u^(0) = u0 replicated
  * over all (l, m).  work_dev/work_bytes: caller-owned
  * device scratch (256-byte aligned, >= pint_workspace_bytes).  u0_host: 2N doubles (re, im),
- * copied.  forcing_host must be NULL (b == 0; forcing is not supported in this build).
+ * copied.  forcing_host must be NULL (b == 0 at creation; a forcing is attached with
+ * pint_set_forcing).
  * Errors: PINT_ERR_INVALID (sizes, alignment, NULL), PINT_ERR_CUDA. */
 pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, void *work_dev,
                         size_t work_bytes, const double *u0_host, const double *forcing_host,
@@ -144,6 +145,16 @@ pint_status pint_set_form(pint_ctx *c, int32_t form);
  * parts exactly 0; pint_set_initial_value then rejects non-real data), 2-D: grids of the register
  * FFT engine, 4 <= L <= 1024; 1-D: N >= 8.  Errors: PINT_ERR_INVALID. */
 pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
+
+/* Forcing b != 0: w = (u0 + v_0, v_1, ..., v_{L-1}) with
+ * v_l = dT (Q (x) I_N) b_l, b_l[m] = b(t_l + tau_m dT) (the collocation integral of the forcing,
+ * P:105).  v_dev: caller-owned device buffer, complex128 [L/P][M][N] (the local
+ * steps l = rank + P j of this rank), 16-byte aligned, read by every iteration's residual (never
+ * written; the caller keeps it alive); NULL removes the forcing.  The residual norms include it.
+ * Not combinable with the direct form, the Hermitian mode or pint_sequential (the direct form's
+ * single non-zero block and the packed real data assume b == 0).  The Algorithm 2 driver keeps
+ * gamma = L (3 eps + tau) ||u0||_inf.  Errors: PINT_ERR_INVALID. */
+pint_status pint_set_forcing(pint_ctx *c, const void *v_dev);
 
 /* Algorithm 2 of the paper, the stopping driver: gamma = L (3 eps + tau) ||w||_inf;
  * while m_k > tol: m_{k+1} = 2 sqrt(m_k gamma), alpha_{k+1} = sqrt(gamma / m_k), one iteration

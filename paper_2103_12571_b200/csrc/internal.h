@@ -59,6 +59,7 @@ struct StaticTables {
   const int *slots, *unitof;
   int nsolve;
   int packed;
+  const double2 *v;           // forcing part of w, [L][M][N] local steps (nullptr: b == 0)
 };
 
 struct Buffers {

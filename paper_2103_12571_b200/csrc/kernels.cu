@@ -63,6 +63,7 @@ __device__ __forceinline__ void residual_point(const Geometry &g, const StaticTa
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     double2 acc = csub(base, uc[m]);
+    if (st.v) acc = cadd(acc, __ldg(st.v + ((size_t)l * M + m) * g.N + n));   // forcing part of w
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const double q = g.dTQ[m * M + j];
@@ -513,6 +514,7 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         double2 acc = csub(base, uc[m]);
+        if (!PACK && st.v) acc = cadd(acc, __ldg(st.v + ((size_t)l * M + m) * g.N + n));   // forcing part of w
 #pragma unroll
         for (int j = 0; j < M; ++j) {
           const double q = g.dTQ[m * M + j];

@@ -228,7 +228,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   if (s != PINT_OK) return s;
   if (!d) return fail(PINT_ERR_INVALID, "dist is NULL");
   if (!u_dev || !work_dev || !u0_host) return fail(PINT_ERR_INVALID, "NULL buffer");
-  if (forcing_host) return fail(PINT_ERR_INVALID, "forcing b != 0 is not supported in this build");
+  if (forcing_host) return fail(PINT_ERR_INVALID, "forcing_host must be NULL (attach a forcing with pint_set_forcing)");
   if (((uintptr_t)u_dev) % 16) return fail(PINT_ERR_INVALID, "u_dev must be 16-byte aligned");
   if (((uintptr_t)work_dev) % 256) return fail(PINT_ERR_INVALID, "work_dev must be 256-byte aligned");
   const int P = d->nranks, rank = d->rank;
@@ -351,6 +351,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     c->st.unitof = dsym + g.L;
     c->st.nsolve = g.L;
     c->st.packed = 0;
+    c->st.v = nullptr;
   }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
             (double *)(c->work + lay.off_red), (unsigned *)(c->work + lay.off_sync)};
@@ -868,6 +869,7 @@ pint_status pint_set_form(pint_ctx *c, int32_t form) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
   if (form != PINT_FORM_CORRECTION && form != PINT_FORM_DIRECT) return fail(PINT_ERR_INVALID, "unknown form");
   if (form == PINT_FORM_DIRECT && c->P > 1) return fail(PINT_ERR_INVALID, "the direct form is single-rank only");
+  if (form == PINT_FORM_DIRECT && c->st.v) return fail(PINT_ERR_INVALID, "the direct form assumes b == 0");
   c->form = form;
   return PINT_OK;
 }
@@ -881,6 +883,7 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
       return fail(PINT_ERR_INVALID, "Hermitian mode: 2-D grids of the register FFT engine, 4 <= L <= 1024, only");
     if (g.dim == 1 && (g.N < 8 || g.L < 2)) return fail(PINT_ERR_INVALID, "Hermitian mode needs N >= 8 and L >= 2");
     if (c->P != 1) return fail(PINT_ERR_INVALID, "Hermitian mode is single-rank only");
+    if (c->st.v) return fail(PINT_ERR_INVALID, "Hermitian mode assumes b == 0");
     for (int n = 0; n < g.N; ++n)
       if (c->u0[2 * n + 1] != 0.0) return fail(PINT_ERR_INVALID, "Hermitian mode needs a real u0");
   }
@@ -948,8 +951,18 @@ pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double to
   return PINT_OK;
 }
 
+pint_status pint_set_forcing(pint_ctx *c, const void *v_dev) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (((uintptr_t)v_dev) % 16) return fail(PINT_ERR_INVALID, "v_dev must be 16-byte aligned");
+  if (v_dev && c->form == PINT_FORM_DIRECT) return fail(PINT_ERR_INVALID, "forcing needs the correction form");
+  if (v_dev && c->hermitian) return fail(PINT_ERR_INVALID, "forcing is not combinable with the Hermitian mode");
+  c->st.v = (const double2 *)v_dev;
+  return PINT_OK;
+}
+
 pint_status pint_sequential(pint_ctx *c) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->st.v) return fail(PINT_ERR_INVALID, "the sequential baseline assumes b == 0");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
   if (g.dim != 2 || !reg2d_path(g) || c->P != 1)

@@ -28,7 +28,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
-           "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential"]
+           "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential", "pint_set_forcing"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
         "pint_solve": (i32, [vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, i32,
                              ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32)]),
         "pint_sequential": (i32, [vp]),
+        "pint_set_forcing": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -201,6 +202,17 @@ class Solver:
         n = it.value
         return {"iters": n, "diffs": d[:n], "m": m[:n + 1],
                 "stop": ["consecutive iterates", "m_k <= tol", "max_iter", "m_k < 4 gamma"][why.value]}
+
+    def set_forcing(self, v: Optional[np.ndarray]):
+        """Attach w's forcing part v[l][m][n] (complex128, this rank's local steps; None removes it)."""
+        import torch
+        if v is None:
+            _check(self.lib.pint_set_forcing(self.ctx, None))
+            self.v = None
+            return
+        vv = np.ascontiguousarray(np.asarray(v, dtype=np.complex128).reshape(self.L, self.M, self.N))
+        self.v = torch.from_numpy(vv).to(self.device)
+        _check(self.lib.pint_set_forcing(self.ctx, ctypes.c_void_p(self.v.data_ptr())))
 
     def sequential(self):
         """Overwrite the iterate with the sequential Radau IIA solution (2-D baseline)."""
