@@ -198,6 +198,13 @@ pint_status pint_get_final_value(pint_ctx *c, double *u_host);
  * to u0 replicated.  Used by the end-to-end benchmark. */
 pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t reset_iterate);
 
+/* Windowed time stepping: start the next window of L steps from the current
+ * iterate's final value, u0 := u_{L-1,M-1} (device copy; the host copy used by pint_w_inf and the
+ * Hermitian check is refreshed), reset the iterate to it replicated and the schedule counter to 0.
+ * Covering W L steps with W windows of Paralpha reproduces the paper's windowed runs.
+ * One rank only.  Errors: PINT_ERR_INVALID, PINT_ERR_CUDA. */
+pint_status pint_next_window(pint_ctx *c);
+
 /* nranks > 1: a fresh 128-byte NCCL unique id for pint_dist.nccl_unique_id (call on rank 0 and
  * broadcast).  PINT_ERR_NCCL on failure. */
 pint_status pint_nccl_unique_id(void *out128);

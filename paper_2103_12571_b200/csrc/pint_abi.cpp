@@ -815,6 +815,32 @@ pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t r
   return PINT_OK;
 }
 
+pint_status pint_next_window(pint_ctx *c) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (c->P != 1) return fail(PINT_ERR_INVALID, "windowed stepping is single-rank only");
+  const Geometry &g = c->g;
+  const double2 *last = c->u + ((size_t)(g.L - 1) * g.M + (g.M - 1)) * g.N;
+  CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToDevice,
+                              c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->u0.data(), last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, launch_init_iterate(c->g, c->st, buffers(c), c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->hermitian) {   // the projection keeps the final value real up to roundoff: make it exact
+    bool changed = false;
+    for (int n = 0; n < g.N; ++n)
+      if (c->u0[2 * n + 1] != 0.0) { c->u0[2 * n + 1] = 0.0; changed = true; }
+    if (changed) {
+      CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, c->u0.data(), (size_t)g.N * sizeof(double2),
+                                  cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, launch_init_iterate(c->g, c->st, buffers(c), c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  c->k = 0;
+  return PINT_OK;
+}
+
 pint_status pint_destroy(pint_ctx *c) {
   if (c && c->comm) ncclCommDestroy(c->comm);
   delete c;

@@ -28,7 +28,8 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_abi_version", "pint_launches_per_iteration", "pint_get_factors", "pint_tableau",
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
-           "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential", "pint_set_forcing"]
+           "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential", "pint_set_forcing",
+           "pint_next_window"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -95,6 +96,7 @@ def load_library(path: str = LIB_PATH):
                              ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32)]),
         "pint_sequential": (i32, [vp]),
         "pint_set_forcing": (i32, [vp, vp]),
+        "pint_next_window": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -213,6 +215,10 @@ class Solver:
         vv = np.ascontiguousarray(np.asarray(v, dtype=np.complex128).reshape(self.L, self.M, self.N))
         self.v = torch.from_numpy(vv).to(self.device)
         _check(self.lib.pint_set_forcing(self.ctx, ctypes.c_void_p(self.v.data_ptr())))
+
+    def next_window(self):
+        """Start the next window of L steps from the final value (windowed Paralpha)."""
+        _check(self.lib.pint_next_window(self.ctx))
 
     def sequential(self):
         """Overwrite the iterate with the sequential Radau IIA solution (2-D baseline)."""
