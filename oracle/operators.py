@@ -1,86 +1,118 @@
-"""Spatial operators A of u_t = A u + b for the configs (oracle; test infrastructure only).
+"""Spatial operators A of u_t = A u + b (oracle; test infrastructure only).
 
-Periodic grid x_j = j/n on [0,1) (2-D: n = y*nx + x).  SURVEY.md §8(c) C9 reading:
-  heat:       (A u)_j = nu * n^2 (u_{j-1} - 2 u_j + u_{j+1})        per axis, summed in 2-D
-  advection:  (A u)_j = -c * n/2 (u_{j+1} - u_{j-1})                per axis (c = cx, cy)
-Fourier symbols (A e^{2 pi i k j/n} = lambda(k) e^{2 pi i k j/n}), cancellation-free forms
-(SURVEY §8(c) C6):
-  heat:       lambda = -4 nu (nx^2 sin^2(pi kx/nx) + ny^2 sin^2(pi ky/ny))
-  advection:  lambda = -i (cx nx sin(2 pi kx/nx) + cy ny sin(2 pi ky/ny))
+Periodic grid x_j = j/n on [0,1) (2-D: n = y*nx + x); 2-D sums the two axes.
+reading for the configs, plus the paper's other discretisations (
+DESIGN.md reading R14): centred differences of order kappa = 2, 4, 6 for the second derivative
+and upwind differences of order 1, 3, 5 for the first derivative.
+  heat  (kappa):   (A u)_j = nu n^2 sum_s d2[s] u_{j+s}
+  advection:       (A u)_j = -c n/2 (u_{j+1} - u_{j-1})                      (centred, kappa 2)
+  upwind (kappa):  (A u)_j = -c n sum_s d1[s] u_{j+s},  d1 biased against the flow (c > 0: left)
+Stencil weights (exact rationals):
+  d2, kappa 2: (1, -2, 1);  4: (-1/12, 4/3, -5/2, 4/3, -1/12);  6: (1/90, -3/20, 3/2, -49/18, ...)
+  d1 (c > 0), kappa 1: {-1: -1, 0: 1};  3: (u_{j-2} - 6u_{j-1} + 3u_j + 2u_{j+1})/6;
+              5: (-2u_{j-3} + 15u_{j-2} - 60u_{j-1} + 20u_j + 30u_{j+1} - 3u_{j+2})/60;  c < 0: mirrored.
+Fourier symbols (A e^{2 pi i k j/n} = lambda(k) e^{2 pi i k j/n}) in cancellation-free forms
+(SURVEY §8(c) C6): with theta = 2 pi k/n (index reduced mod n),
+  symmetric d2:  lambda = -4 nu n^2 sum_{s>=1} d2[s] sin^2(s theta/2)
+  d1:            sum_s d1[s] e^{i s theta} = -2 sum_s d1[s] sin^2(s theta/2) + i sum_s d1[s] sin(s theta)
+  advection:     lambda = -i c n sin(theta)
 """
 from __future__ import annotations
 
 import numpy as np
 
 
-def apply_A(p, v: np.ndarray) -> np.ndarray:
-    """A applied along the trailing spatial axis (length N = nx*ny) of v."""
-    nx, ny = p.nx, p.ny
-    shp = v.shape
-    w = v.reshape(shp[:-1] + (ny, nx))
-    out = np.zeros_like(w)
-    if p.op == "heat":
-        out += p.nu * nx * nx * (np.roll(w, 1, axis=-1) - 2.0 * w + np.roll(w, -1, axis=-1))
-        if p.dim == 2:
-            out += p.nu * ny * ny * (np.roll(w, 1, axis=-2) - 2.0 * w + np.roll(w, -1, axis=-2))
-    elif p.op == "advection":
-        # np.roll(w, -1)[j] = w[j+1]
-        out += -p.cx * nx / 2.0 * (np.roll(w, -1, axis=-1) - np.roll(w, 1, axis=-1))
-        if p.dim == 2:
-            out += -p.cy * ny / 2.0 * (np.roll(w, -1, axis=-2) - np.roll(w, 1, axis=-2))
+D2 = {2: {-1: 1.0, 0: -2.0, 1: 1.0},
+      4: {-2: -1 / 12, -1: 4 / 3, 0: -5 / 2, 1: 4 / 3, 2: -1 / 12},
+      6: {-3: 1 / 90, -2: -3 / 20, -1: 3 / 2, 0: -49 / 18, 1: 3 / 2, 2: -3 / 20, 3: 1 / 90}}
+D1_LEFT = {1: {-1: -1.0, 0: 1.0},
+           3: {-2: 1 / 6, -1: -1.0, 0: 1 / 2, 1: 1 / 3},
+           5: {-3: -2 / 60, -2: 15 / 60, -1: -60 / 60, 0: 20 / 60, 1: 30 / 60, 2: -3 / 60}}
+HEAT_OPS = {"heat": 2, "heat4": 4, "heat6": 6}
+UPWIND_OPS = {"upwind1": 1, "upwind3": 3, "upwind5": 5}
+
+
+def axis_stencil(op: str, n: int, coef: float) -> dict:
+    """{offset s: weight} of A along one axis of n points (coef = nu for heat, c for advection)."""
+    if op in HEAT_OPS:
+        return {s: coef * n * n * w for s, w in D2[HEAT_OPS[op]].items()}
+    if op == "advection":
+        return {-1: coef * n / 2.0, 1: -coef * n / 2.0}
+    if op in UPWIND_OPS:
+        d = D1_LEFT[UPWIND_OPS[op]]
+        if coef < 0:
+            d = {-s: -w for s, w in d.items()}           # flow to the left: mirrored stencil
+        return {s: -coef * n * w for s, w in d.items()}
+    raise ValueError(op)
+
+
+def _axes(p):
+    if p.op in HEAT_OPS:
+        cx, cy = p.nu, p.nu
     else:
-        raise ValueError(p.op)
+        cx, cy = p.cx, p.cy
+    out = [(-1, axis_stencil(p.op, p.nx, cx))]
+    if p.dim == 2:
+        out.append((-2, axis_stencil(p.op, p.ny, cy)))
+    return out
+
+
+def apply_A(p, v: np.ndarray) -> np.ndarray:
+    """A applied along the trailing spatial axis (length N = nx*ny) of v: the stencil sum with
+    np.roll (np.roll(w, -s)[j] = w[j+s])."""
+    shp = v.shape
+    w = v.reshape(shp[:-1] + (p.ny, p.nx))
+    out = np.zeros_like(w)
+    for axis, st in _axes(p):
+        for sft, wt in st.items():
+            out += wt * np.roll(w, -sft, axis=axis)
     return out.reshape(shp)
 
 
 def dense_A(p) -> np.ndarray:
     """A as an explicit N x N matrix, entry by entry from the stencil definition (tiny N only)."""
     nx, ny = p.nx, p.ny
-    N = nx * ny
-    A = np.zeros((N, N), dtype=np.complex128)
+    A = np.zeros((nx * ny, nx * ny), dtype=np.complex128)
+    axes = dict(_axes(p))
     for y in range(ny):
         for x in range(nx):
             i = y * nx + x
-            xm, xp = y * nx + (x - 1) % nx, y * nx + (x + 1) % nx
-            if p.op == "heat":
-                A[i, xm] += p.nu * nx * nx
-                A[i, i] += -2.0 * p.nu * nx * nx
-                A[i, xp] += p.nu * nx * nx
-            else:
-                A[i, xp] += -p.cx * nx / 2.0
-                A[i, xm] += p.cx * nx / 2.0
+            for sft, wt in axes[-1].items():
+                A[i, y * nx + (x + sft) % nx] += wt
             if p.dim == 2:
-                ym, yp = ((y - 1) % ny) * nx + x, ((y + 1) % ny) * nx + x
-                if p.op == "heat":
-                    A[i, ym] += p.nu * ny * ny
-                    A[i, i] += -2.0 * p.nu * ny * ny
-                    A[i, yp] += p.nu * ny * ny
-                else:
-                    A[i, yp] += -p.cy * ny / 2.0
-                    A[i, ym] += p.cy * ny / 2.0
+                for sft, wt in axes[-2].items():
+                    A[i, ((y + sft) % ny) * nx + x] += wt
     return A
 
 
 def symbol_1d(op: str, n: int, k: np.ndarray, coef: float) -> np.ndarray:
     """Per-axis symbol for integer wavenumbers k (coef = nu for heat, c for advection)."""
     k = np.asarray(k, dtype=np.int64) % n
-    if op == "heat":
-        s = np.sin(np.pi * k.astype(np.float64) / n)
-        return np.asarray(-4.0 * coef * n * n * s * s, dtype=np.complex128)
-    # sin(2 pi k/n) from the reduced index k mod n
-    return np.asarray(-1j * coef * n * np.sin(2.0 * np.pi * k.astype(np.float64) / n), dtype=np.complex128)
+    th = 2.0 * np.pi * k.astype(np.float64) / n
+    if op in HEAT_OPS:
+        acc = np.zeros_like(th)
+        for sft, w in D2[HEAT_OPS[op]].items():
+            if sft > 0:
+                acc = acc + w * np.sin(sft * th / 2) ** 2
+        return np.asarray(-4.0 * coef * n * n * acc, dtype=np.complex128)
+    if op == "advection":
+        # sin(2 pi k/n) from the reduced index k mod n
+        return np.asarray(-1j * coef * n * np.sin(th), dtype=np.complex128)
+    st = axis_stencil(op, n, coef)
+    re = np.zeros_like(th)
+    im = np.zeros_like(th)
+    for sft, w in st.items():
+        re = re - 2.0 * w * np.sin(sft * th / 2) ** 2
+        im = im + w * np.sin(sft * th)
+    return re + 1j * im
 
 
 def symbol(p, kx: np.ndarray, ky: np.ndarray) -> np.ndarray:
     """lambda(kx, ky) for mode exp(2 pi i (kx x + ky y)) (broadcasting)."""
-    if p.op == "heat":
-        lam = symbol_1d("heat", p.nx, kx, p.nu)
-        if p.dim == 2:
-            lam = lam + symbol_1d("heat", p.ny, ky, p.nu)
-    else:
-        lam = symbol_1d("advection", p.nx, kx, p.cx)
-        if p.dim == 2:
-            lam = lam + symbol_1d("advection", p.ny, ky, p.cy)
+    cx, cy = (p.nu, p.nu) if p.op in HEAT_OPS else (p.cx, p.cy)
+    lam = symbol_1d(p.op, p.nx, kx, cx)
+    if p.dim == 2:
+        lam = lam + symbol_1d(p.op, p.ny, ky, cy)
     return lam
 
 

@@ -11,6 +11,11 @@ SMALL = [
     W.Problem("h2", 2, 8, 4, "heat", 0.3, 0, 0, 1, 2, 1, "random", "fixed", 0.1, 1),
     W.Problem("a2", 2, 8, 16, "advection", 0, 1.0, -0.5, 1, 2, 1, "random", "fixed", 0.1, 1),
 ]
+# the paper's other discretisations: centred kappa 4, 6 and upwind 1, 3, 5 (both flow signs)
+SMALL += [W.Problem(op + ("_2d" if d == 2 else ""), d, 16, 8 if d == 2 else 1, op, 0.4,
+                    1.1 if op != "heat4" else 0, -0.6 if d == 2 else 0, 1, 2, 1, "random", "fixed", 0.1, 1)
+          for op in ("heat4", "heat6", "upwind1", "upwind3", "upwind5") for d in (1, 2)]
+SMALL += [W.Problem("up3_neg", 1, 16, 1, "upwind3", 0, -0.8, 0, 1, 2, 1, "random", "fixed", 0.1, 1)]
 
 
 @pytest.mark.parametrize("p", SMALL, ids=lambda p: p.name)
@@ -22,8 +27,13 @@ def test_dense_matches_stencil(p):
 
 @pytest.mark.parametrize("p", SMALL + [W.CONFIGS[2], W.reduced(4), W.reduced(5)], ids=lambda p: p.name)
 def test_constants_in_kernel(p):
-    """A 1 = 0 for both operators."""
-    assert np.abs(apply_A(p, np.ones(p.N, dtype=complex))).max() == 0.0
+    """A 1 = 0 for every operator: exact for the 3-point stencils,
+    to rounding of the weight sum (|weights|_1 * 8 eps) for the wider ones (thirds, twelfths)."""
+    r = np.abs(apply_A(p, np.ones(p.N, dtype=complex))).max()
+    if p.op in ("heat", "advection"):
+        assert r == 0.0
+    else:
+        assert r <= 8 * np.finfo(float).eps * np.abs(dense_A(p)).sum(1).max()
 
 
 @pytest.mark.parametrize("p", SMALL + [W.CONFIGS[2], W.reduced(4), W.reduced(5)], ids=lambda p: p.name)
@@ -50,3 +60,36 @@ def test_heat_symbol_is_nonpositive_and_advection_imaginary():
     q = W.reduced(5)
     lam = symbol_grid(q)
     assert np.all(lam.real == 0)
+
+
+@pytest.mark.parametrize("op,order", [("heat", 2), ("heat4", 4), ("heat6", 6), ("advection", 2),
+                                      ("upwind1", 1), ("upwind3", 3), ("upwind5", 5)])
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_consistency_order(op, order, sign):
+    """A applied to sin(2 pi x) (+ 0.5 cos(4 pi x)) approaches nu u'' (heat) or -c u' (advection,
+    upwind) with error ~ n^-order: pins every stencil weight (a wrong weight breaks the rate)."""
+    errs = []
+    for n in (32, 64, 128):
+        p = W.Problem("c", 1, n, 1, op, 0.3, sign * 0.9, 0, 1, 2, 1, "random", "fixed", 0.1, 1)
+        x = np.arange(n) / n
+        u = np.sin(2 * np.pi * x) + 0.5 * np.cos(4 * np.pi * x)
+        if op.startswith("heat"):
+            exact = 0.3 * (-(2 * np.pi) ** 2 * np.sin(2 * np.pi * x) - 0.5 * (4 * np.pi) ** 2 * np.cos(4 * np.pi * x))
+        else:
+            exact = -sign * 0.9 * (2 * np.pi * np.cos(2 * np.pi * x) - 0.5 * 4 * np.pi * np.sin(4 * np.pi * x))
+        errs.append(np.abs(apply_A(p, u.astype(complex)) - exact).max())
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(np.abs(rates - order) < 0.3), (errs, rates)
+
+
+def test_upwind_damps_and_centred_heat_is_real():
+    """Upwind symbols have Re lambda <= 0 (dissipative, flow-sign independent); centred heat symbols
+    of every order are real and non-positive."""
+    for op in ("upwind1", "upwind3", "upwind5"):
+        for c in (1.0, -1.0):
+            p = W.Problem("u", 2, 16, 8, op, 0, c, 0.5 * c, 1, 2, 1, "random", "fixed", 0.1, 1)
+            assert np.all(symbol_grid(p).real <= 1e-12)
+    for op in ("heat4", "heat6"):
+        p = W.Problem("h", 2, 16, 8, op, 0.5, 0, 0, 1, 2, 1, "random", "fixed", 0.1, 1)
+        lam = symbol_grid(p)
+        assert np.all(lam.imag == 0) and np.all(lam.real <= 0)
