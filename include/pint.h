@@ -19,9 +19,16 @@
  *   (iv)  (I - d_km dT A) x2 = x1 for every (k, m)
  *   (v)   y_k = G_k^{-1} S_k x2_k, inverse DFT, alpha^{-l/L}/L, u += c
  *
- * Spatial operators (periodic [0,1)^dim, x_j = j/nx, n = y*nx + x, centred 2nd order):
+ * Spatial operators (periodic [0,1)^dim, x_j = j/nx, n = y*nx + x; 2-D sums the axes):
  *   PINT_OP_HEAT:       A = nu * Laplacian  ((u_{j-1} - 2u_j + u_{j+1}) nx^2 per axis)
  *   PINT_OP_ADVECTION:  A = -(cx d/dx + cy d/dy)  (-c n/2 (u_{j+1} - u_{j-1}) per axis)
+ * and the paper's other discretisations (Tables 1-2; reading R14):
+ *   PINT_OP_HEAT4/6:    nu * centred second differences of order 4 / 6 (5- / 7-point)
+ *   PINT_OP_UPWIND1/3/5: -(cx d/dx + cy d/dy) by upwind-biased first differences of order 1/3/5
+ *                        (offsets -(k+1)/2 .. (k-1)/2 for c > 0, mirrored per axis for c < 0)
+ * 1-D solves (I - s A) by PCR on the tridiagonal factors of I - s A (the 3-point operators are
+ * one factor; wider stencils are factored on the host per (alpha, k, m); pint_set_alpha_schedule
+ * fails with PINT_ERR_NUMERIC if a factor cannot be formed).  2-D solves are diagonal in Fourier.
  *
  * Data layout: complex128, interleaved (re, im) doubles, u[l][m][n], n fastest.
  *
@@ -64,7 +71,15 @@ typedef enum {
   PINT_ERR_STATE = 7                /* context poisoned by an earlier CUDA/NCCL error          */
 } pint_status;
 
-typedef enum { PINT_OP_HEAT = 0, PINT_OP_ADVECTION = 1 } pint_op;
+typedef enum {
+  PINT_OP_HEAT = 0,
+  PINT_OP_ADVECTION = 1,
+  PINT_OP_HEAT4 = 2,
+  PINT_OP_HEAT6 = 3,
+  PINT_OP_UPWIND1 = 4,
+  PINT_OP_UPWIND3 = 5,
+  PINT_OP_UPWIND5 = 6
+} pint_op;
 
 typedef struct {
   int32_t dim;     /* 1 or 2                                                                  */

@@ -1,5 +1,6 @@
 // Host numerics of libpint in long double (see host_numerics.h).
 #include "host_numerics.h"
+#include "pint.h"
 
 #include <algorithm>
 #include <cmath>
@@ -332,6 +333,175 @@ size_t pass_twiddle_count(int logn, int maxb) {
   std::vector<cld> v;
   pass_twiddles(logn, maxb, v);
   return v.size();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Spatial operators.  Centred second differences of order 2, 4, 6 and upwind-biased first
+// differences of order 1, 3, 5 (c > 0; mirrored for c < 0); exact rational weights.
+
+static const ld kD2[3][4] = {{-2.0L, 1.0L, 0, 0},                                   // kappa 2: d_0, d_1
+                             {-5.0L / 2, 4.0L / 3, -1.0L / 12, 0},                  // kappa 4
+                             {-49.0L / 18, 3.0L / 2, -3.0L / 20, 1.0L / 90}};       // kappa 6
+// upwind (c > 0): offsets -3 .. 2 at index o + 3
+static const ld kD1[3][6] = {{0, 0, -1.0L, 1.0L, 0, 0},
+                             {0, 1.0L / 6, -1.0L, 1.0L / 2, 1.0L / 3, 0},
+                             {-2.0L / 60, 15.0L / 60, -1.0L, 20.0L / 60, 30.0L / 60, -3.0L / 60}};
+
+bool op_is_heat(int op) { return op == PINT_OP_HEAT || op == PINT_OP_HEAT4 || op == PINT_OP_HEAT6; }
+
+static int heat_row(int op) { return op == PINT_OP_HEAT ? 0 : op == PINT_OP_HEAT4 ? 1 : 2; }
+static int upwind_row(int op) { return op == PINT_OP_UPWIND1 ? 0 : op == PINT_OP_UPWIND3 ? 1 : 2; }
+
+bool axis_stencil(int op, long long n, ld coef, AxisStencil &st) {
+  st = AxisStencil{};
+  const ld nn = (ld)n;
+  if (op_is_heat(op)) {
+    const int r = heat_row(op), h = r + 1;
+    st.h0 = st.h1 = h;
+    for (int o = 0; o <= h; ++o) st.w[3 + o] = st.w[3 - o] = coef * nn * nn * kD2[r][o];
+    return true;
+  }
+  if (op == PINT_OP_ADVECTION) {
+    st.h0 = st.h1 = 1;
+    st.w[2] = coef * nn / 2;
+    st.w[4] = -coef * nn / 2;
+    return true;
+  }
+  if (op == PINT_OP_UPWIND1 || op == PINT_OP_UPWIND3 || op == PINT_OP_UPWIND5) {
+    const ld *d = kD1[upwind_row(op)];
+    const bool mirror = coef < 0;
+    st.h0 = st.h1 = 3;
+    for (int o = -3; o <= 2; ++o) {
+      const int oo = mirror ? -o : o;                     // c < 0: w(o) = -d(-o)
+      st.w[3 + oo] = -coef * nn * (mirror ? -d[o + 3] : d[o + 3]);
+    }
+    // trim to the nonzero offsets
+    while (st.h0 > 0 && st.w[3 - st.h0] == 0) --st.h0;
+    while (st.h1 > 0 && st.w[3 + st.h1] == 0) --st.h1;
+    if (coef == 0) st.h0 = st.h1 = 0;
+    return true;
+  }
+  return false;
+}
+
+// sin^2(pi q / n) and sin(2 pi q / n) from the integer-reduced q (no large-argument rounding)
+static ld sin2_pi(long long q, long long n) {
+  q %= n;
+  if (q < 0) q += n;
+  const ld sn = sinl(kPi * (ld)q / (ld)n);
+  return sn * sn;
+}
+
+cld axis_symbol(int op, long long n, long long k, ld coef) {
+  AxisStencil st;
+  axis_stencil(op, n, coef, st);
+  if (op_is_heat(op)) {
+    // sum_o w_o e^{i o theta} = -4 sum_{o >= 1} w_o sin^2(o theta / 2)
+    ld acc = 0;
+    for (int o = 1; o <= st.h1; ++o) acc += st.w[3 + o] * sin2_pi((long long)o * k, n);
+    return cld(-4 * acc, 0);
+  }
+  // sum_o w_o e^{i o theta} = -2 sum_o w_o sin^2(o theta / 2) + i sum_o w_o sin(o theta)
+  ld re = 0, im = 0;
+  for (int o = -st.h0; o <= st.h1; ++o) {
+    if (o == 0) continue;
+    re += -2 * st.w[3 + o] * sin2_pi((long long)o * k, n);
+    im += st.w[3 + o] * unit_root((long long)o * k, n, +1).imag();
+  }
+  return cld(re, im);
+}
+
+int stencil_factor_count(int op, const AxisStencil &st) {
+  if (st.h0 <= 1 && st.h1 <= 1) return 1;
+  if (op_is_heat(op)) return st.h1;
+  return std::max(st.h0, st.h1);
+}
+
+// roots of sum_j p[j] z^j (p[deg] != 0): Durand-Kerner in long double, then Newton polishing
+static void poly_roots(const std::vector<cld> &p, std::vector<cld> &r) {
+  const int deg = (int)p.size() - 1;
+  std::vector<cld> m(deg + 1);
+  for (int j = 0; j <= deg; ++j) m[j] = p[j] / p[deg];
+  auto eval = [&](cld z, cld *dp) {
+    cld v = m[deg], d = 0;
+    for (int j = deg - 1; j >= 0; --j) { d = d * z + v; v = v * z + m[j]; }
+    if (dp) *dp = d;
+    return v;
+  };
+  ld rad = 0;
+  for (int j = 0; j < deg; ++j) rad = std::max(rad, std::pow(std::abs(m[j]), 1.0L / (deg - j)));
+  rad = 2 * rad + 1e-3L;
+  r.resize(deg);
+  for (int i = 0; i < deg; ++i) r[i] = std::polar(rad * (0.4L + 0.1L * i), 0.9L + 2 * kPi * i / deg);
+  for (int it = 0; it < 2000; ++it) {
+    ld mv = 0;
+    for (int i = 0; i < deg; ++i) {
+      cld den = 1;
+      for (int j = 0; j < deg; ++j) if (j != i) den *= r[i] - r[j];
+      const cld dz = eval(r[i], nullptr) / den;
+      r[i] -= dz;
+      mv = std::max(mv, std::abs(dz) / std::max(1.0L, std::abs(r[i])));
+    }
+    if (mv < 1e-30L) break;
+  }
+  for (int i = 0; i < deg; ++i)
+    for (int it = 0; it < 4; ++it) {
+      cld d;
+      const cld v = eval(r[i], &d);
+      if (d == cld(0)) break;
+      r[i] -= v / d;
+    }
+}
+
+bool factor_shifted(int op, const AxisStencil &st, cld s, std::vector<TriFactor> &f, cld &lead,
+                    std::string &err) {
+  f.clear();
+  if (st.h0 <= 1 && st.h1 <= 1) {
+    // one factor; A 1 = 0 makes the row sum exactly 1 - s (w_-1 + w_0 + w_1) = 1 (reading R6)
+    const cld a = -s * st.w[2], c = -s * st.w[4];
+    const cld e = 1.0L - s * (st.w[2] + st.w[3] + st.w[4]);
+    f.push_back({a, e - a - c, c, e});
+    lead = 1;
+    return true;
+  }
+  if (op_is_heat(op)) {
+    // A(tau) = sum_{o>=1} w_o (z^o + z^-o - 2), z^o + z^-o - 2 = tau, tau^2 + 4 tau, tau^3 + 6 tau^2 + 9 tau
+    static const int P[4][4] = {{0, 0, 0, 0}, {0, 1, 0, 0}, {0, 4, 1, 0}, {0, 9, 6, 1}};
+    const int h = st.h1;
+    std::vector<cld> p(h + 1, cld(0));
+    p[0] = 1;                                        // 1 - s A(tau)
+    for (int o = 1; o <= h; ++o)
+      for (int j = 1; j <= h; ++j) p[j] -= s * st.w[3 + o] * (ld)P[o][j];
+    std::vector<cld> tau;
+    poly_roots(p, tau);
+    for (const cld &t : tau) {
+      if (std::abs(t) == 0) { err = "zero factor root"; return false; }
+      f.push_back({cld(1), -2.0L - t, cld(1), -t});
+    }
+    lead = p[h];
+    return true;
+  }
+  const int deg = st.h0 + st.h1;
+  std::vector<cld> p(deg + 1, cld(0));
+  for (int o = -st.h0; o <= st.h1; ++o) p[o + st.h0] = (o == 0 ? cld(1) : cld(0)) - s * st.w[3 + o];
+  std::vector<cld> r;
+  poly_roots(p, r);
+  std::vector<cld> in, out;
+  for (const cld &z : r) {
+    const ld az = std::abs(z);
+    if (std::fabs(az - 1) < 1e-12L) { err = "factor root on the unit circle"; return false; }
+    (az < 1 ? in : out).push_back(z);
+  }
+  if ((int)in.size() != st.h0) { err = "factor roots do not split h0 inside / h1 outside the unit circle"; return false; }
+  size_t i = 0;
+  for (; i < in.size() && i < out.size(); ++i) {     // z^-1 (z - r_in)(z - r_out)
+    const cld ri = in[i], ro = out[i];
+    f.push_back({ri * ro, -(ri + ro), cld(1), (1.0L - ri) * (1.0L - ro)});
+  }
+  for (size_t j = i; j < in.size(); ++j) f.push_back({-in[j], cld(1), cld(0), 1.0L - in[j]});   // 1 - r z^-1
+  for (size_t j = i; j < out.size(); ++j) f.push_back({cld(0), -out[j], cld(1), 1.0L - out[j]});  // z - r
+  lead = p[deg];
+  return true;
 }
 
 }  // namespace pint

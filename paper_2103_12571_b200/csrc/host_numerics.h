@@ -44,4 +44,29 @@ cld unit_root(long long q, long long n, int sign);
 void pass_twiddles(int logn, int maxb, std::vector<cld> &out);
 size_t pass_twiddle_count(int logn, int maxb);
 
+// ---- spatial operators (readings R8, R14) -----------------------
+// Op codes are pint_op's (include/pint.h).  Weights of A along one axis of n points: (A u)_j =
+// sum_{o=-h0}^{h1} w[3+o] u_{j+o}; coef = nu (heat family) or the axis velocity c (advection).
+struct AxisStencil {
+  int h0 = 0, h1 = 0;
+  ld w[7] = {0, 0, 0, 0, 0, 0, 0};
+};
+bool axis_stencil(int op, long long n, ld coef, AxisStencil &st);
+bool op_is_heat(int op);
+// Fourier symbol of A along one axis at integer wavenumber k (cancellation-free sin^2 forms)
+cld axis_symbol(int op, long long n, long long k, ld coef);
+
+// I - s A (1-D) as a product of tridiagonal circulant factors (PCR, kernels.cu):
+//   I - s A = lead * prod_f (a_f S^{-1} + b_f + c_f S),   (S u)_j = u_{j+1},
+// with e_f = a_f + b_f + c_f (row sum, carried through PCR, reading R6).  3-point operators are
+// one factor (a, 1 - s wc, c) with e = 1; the centred heat family is factored in
+// tau = z + 1/z - 2 = -4 sin^2(theta/2) (factors S^{-1} + S - 2 - tau_f, e_f = -tau_f exactly);
+// other stencils by the roots of z^{h0} (1 - s A(z)), pairing a root inside the unit circle
+// with one outside per factor so every PCR level stays diagonally dominated.  Returns false
+// (err) if a root lies on the unit circle or the roots do not split h0 inside / h1 outside.
+struct TriFactor { cld a, b, c, e; };
+int stencil_factor_count(int op, const AxisStencil &st);
+bool factor_shifted(int op, const AxisStencil &st, cld s, std::vector<TriFactor> &f, cld &lead,
+                    std::string &err);
+
 }  // namespace pint

@@ -24,8 +24,12 @@ struct Geometry {
   int dim, nx, ny, N, L, M, op;
   int logL, logN, lognx, logny;
   double dT;
-  // stencil: (A u)_n = cxm u[x-1] + cxp u[x+1] + cym u[y-1] + cyp u[y+1] + c0 u[n]
-  double cxm, cxp, cym, cyp, c0;
+  // stencil of A (the paper's discretisations P:751-799, readings R8, R14):
+  //   (A u)_n = sum_{o=-hx0}^{hx1} wx[3+o] u[x+o, y] + sum_{o=-hy0}^{hy1} wy[3+o] u[x, y+o]
+  // periodic; the centre weights of both axes are folded into wx[3] (wy[3] = 0); hw = widest halo
+  int hx0, hx1, hy0, hy1, hw;
+  double wx[7], wy[7];
+  int nfac;                   // 1-D: tridiagonal factors of I - s A solved by PCR (1..3)
   double dTQ[8 * 8];          // dT * Q, row-major
 };
 

@@ -39,23 +39,27 @@ __device__ __forceinline__ void residual_point(const Geometry &g, const StaticTa
   const double2 *ul = u + (size_t)l * plane;
   const int x = n & (g.nx - 1);
   const int y = n >> g.lognx;
-  const int nxm = (y << g.lognx) + ((x - 1) & (g.nx - 1));
-  const int nxp = (y << g.lognx) + ((x + 1) & (g.nx - 1));
+  const int row = y << g.lognx;
   double2 uc[M], Au[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) {
     const double2 *uj = ul + (size_t)j * g.N;
-    double2 c = __ldg(uj + n), a = __ldg(uj + nxm), b = __ldg(uj + nxp);
+    const double2 c = __ldg(uj + n);
     uc[j] = c;
-    double2 s;
-    s.x = g.c0 * c.x + g.cxm * a.x + g.cxp * b.x;
-    s.y = g.c0 * c.y + g.cxm * a.y + g.cxp * b.y;
+    double2 s = make_double2(g.wx[3] * c.x, g.wx[3] * c.y);
+    for (int o = -g.hx0; o <= g.hx1; ++o) {
+      if (o == 0) continue;
+      const double2 v = __ldg(uj + row + ((x + o) & (g.nx - 1)));
+      s.x = fma(g.wx[3 + o], v.x, s.x);
+      s.y = fma(g.wx[3 + o], v.y, s.y);
+    }
     if (g.dim == 2) {
-      const int nym = (((y - 1) & (g.ny - 1)) << g.lognx) + x;
-      const int nyp = (((y + 1) & (g.ny - 1)) << g.lognx) + x;
-      double2 d = __ldg(uj + nym), e = __ldg(uj + nyp);
-      s.x += g.cym * d.x + g.cyp * e.x;
-      s.y += g.cym * d.y + g.cyp * e.y;
+      for (int o = -g.hy0; o <= g.hy1; ++o) {
+        if (o == 0) continue;
+        const double2 v = __ldg(uj + ((((y + o) & (g.ny - 1)) << g.lognx) + x));
+        s.x = fma(g.wy[3 + o], v.x, s.x);
+        s.y = fma(g.wy[3 + o], v.y, s.y);
+      }
     }
     Au[j] = s;
   }
@@ -468,18 +472,20 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 
 // PACK (Hermitian mode): the CTA also evaluates the partner block BY rows lower by ny/2 and writes
 // Z[l][m][n'] = alpha^{l/L} (Re r(n') + i Re r(n' + N/2)) for its top-half points n' (N/2 per plane).
-template <int M, bool PACK>
+// HW: halo width (1 for the 3-point operators, up to 3 for the kappa-6 / upwind-5 stencils);
+// weights outside [-hx0, hx1] x [-hy0, hy1] are zero in g.wx / g.wy.
+template <int M, bool PACK, int HW>
 __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
                                                          const double2 *__restrict__ u,
                                                          double2 *__restrict__ X, int BX, int BY) {
-  extern __shared__ double2 sm[];  // [1 + PACK][M][BY+2][BX+2]
+  extern __shared__ double2 sm[];  // [1 + PACK][M][BY+2HW][BX+2HW]
   const int bxs = g.nx / BX, bys = (PACK ? g.ny / 2 : g.ny) / BY;
   int b = blockIdx.x;
   const int bx = b % bxs; b /= bxs;
   const int by = b % bys;
   const int l = b / bys;
   const int x0 = bx * BX, y0 = by * BY;
-  const int W = BX + 2, H = BY + 2;
+  const int W = BX + 2 * HW, H = BY + 2 * HW;
   const size_t plane = (size_t)M * g.N;
   const double2 *ul = u + (size_t)l * plane;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -487,10 +493,10 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   for (int r = warp; r < NH * M * H; r += blockDim.x >> 5) {
     const int hh = r / (M * H), rr = r - hh * M * H;
     const int j = rr / H, yy = rr - j * H;
-    const int y = (y0 + hh * (g.ny / 2) + yy - 1) & (g.ny - 1);
+    const int y = (y0 + hh * (g.ny / 2) + yy - HW) & (g.ny - 1);
     const double2 *src = ul + (size_t)j * g.N + ((size_t)y << g.lognx);
     double2 *dst = sm + r * W;
-    for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - 1) & (g.nx - 1)));
+    for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
   }
   cp_async_wait_all();
   __syncthreads();
@@ -505,11 +511,20 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
       double2 uc[M], Au[M];
 #pragma unroll
       for (int j = 0; j < M; ++j) {
-        const double2 *s = sm + ((hh * M + j) * H + ty + 1) * W + tx + 1;
-        const double2 c = s[0], a = s[-1], bb = s[1], d = s[-W], e = s[W];
+        const double2 *s = sm + ((hh * M + j) * H + ty + HW) * W + tx + HW;
+        const double2 c = s[0];
         uc[j] = c;
-        Au[j].x = g.c0 * c.x + g.cxm * a.x + g.cxp * bb.x + g.cym * d.x + g.cyp * e.x;
-        Au[j].y = g.c0 * c.y + g.cxm * a.y + g.cxp * bb.y + g.cym * d.y + g.cyp * e.y;
+        double2 acc = make_double2(g.wx[3] * c.x, g.wx[3] * c.y);
+#pragma unroll
+        for (int o = -HW; o <= HW; ++o) {
+          if (o == 0) continue;
+          const double2 a = s[o], d = s[o * W];
+          acc.x = fma(g.wx[3 + o], a.x, acc.x);
+          acc.y = fma(g.wx[3 + o], a.y, acc.y);
+          acc.x = fma(g.wy[3 + o], d.x, acc.x);
+          acc.y = fma(g.wy[3 + o], d.y, acc.y);
+        }
+        Au[j] = acc;
       }
 #pragma unroll
       for (int m = 0; m < M; ++m) {
@@ -572,10 +587,12 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
     sm[it] = r0 ? cmul(__ldg(at.sig + tline), __ldg(r0 + (size_t)q * R + rr + tt)) : xl[(size_t)q * R + rr + tt];
   }
   __syncthreads();
-  const double2 *coef = at.pcr + (size_t)tline * g.logN * 2;
-  for (int jj = 0; jj < lognq; ++jj) {
+  const int F = g.nfac;
+  const double2 *coef = at.pcr + (size_t)tline * g.logN * F * 2;
+  for (int jf = 0; jf < lognq * F; ++jf) {   // level jj, factor f (all circulant: any order)
+    const int jj = jf / F;
     const int j = j_off + jj;
-    const double2 pj = __ldg(coef + 2 * j), qj = __ldg(coef + 2 * j + 1);
+    const double2 pj = __ldg(coef + 2 * (j * F + jf % F)), qj = __ldg(coef + 2 * (j * F + jf % F) + 1);
     const int h = 1 << jj;
     const bool pair = (jj == lognq - 1);
     double2 nv[kPcrIPT];
@@ -654,7 +671,7 @@ __device__ __forceinline__ void pcr_block_level(double2 (&y)[E], int b, int S, d
 // q = c + S k), where every stride h' >= S is closed in registers (cyclic in k).  Large strides
 // are applied last, so the 1/e scaling and the store happen from the class arrangement
 // (coalesced over the T columns).  Level operators commute (circulant), so the order is free.
-template <int E>
+template <int E, int F>
 __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, AlphaTables at, double2 *__restrict__ X,
                                                          int R, int T, int j_off, const double2 *__restrict__ r0,
                                                          const int *__restrict__ slots) {
@@ -678,15 +695,16 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
   }
   cp_async_wait_all();
   __syncthreads();
-  const double2 *coef = at.pcr + (size_t)tline * g.logN * 2;
+  const double2 *coef = at.pcr + (size_t)tline * g.logN * F * 2;   // F == g.nfac
   double2 y[E];
   {  // block arrangement: thread -> (column, block b); the S lanes of a column are consecutive
     const int b = threadIdx.x & (S - 1), col = threadIdx.x >> logS;
 #pragma unroll
     for (int e = 0; e < E; ++e) y[e] = sm[swz(((b * E + e) << lT) + col)];
-    const double2 *cb = coef + 2 * j_off;
+    const double2 *cb = coef + 2 * j_off * F;
 #define PINT_BLK(H, JJ) \
-    if ((H) < S) pcr_block_level<E, H>(y, b, S, __ldg(cb + 2 * (JJ)), __ldg(cb + 2 * (JJ) + 1));
+    if ((H) < S) _Pragma("unroll") for (int f = 0; f < F; ++f) \
+      pcr_block_level<E, H>(y, b, S, __ldg(cb + 2 * ((JJ) * F + f)), __ldg(cb + 2 * ((JJ) * F + f) + 1));
     PINT_BLK(1, 0) PINT_BLK(2, 1) PINT_BLK(4, 2) PINT_BLK(8, 3) PINT_BLK(16, 4)
 #undef PINT_BLK
 #pragma unroll
@@ -697,9 +715,11 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
   const int col = threadIdx.x & (T - 1), c = threadIdx.x >> lT;
 #pragma unroll
   for (int k = 0; k < E; ++k) y[k] = sm[swz(((c + (k << logS)) << lT) + col)];
-  for (int jj = logS; jj < lognq; ++jj) {   // strides h' = S 2^i, i.e. 2^i in k (cyclic over E)
+  for (int jf = logS * F; jf < lognq * F; ++jf) {   // strides h' = S 2^i, i.e. 2^i in k (cyclic over E)
+    const int jj = jf / F;
     const int hk = 1 << (jj - logS);
-    const double2 pj = __ldg(coef + 2 * (j_off + jj)), qj = __ldg(coef + 2 * (j_off + jj) + 1);
+    const double2 *cj = coef + 2 * ((j_off + jj) * F + jf % F);
+    const double2 pj = __ldg(cj), qj = __ldg(cj + 1);
     const bool pair = (jj == lognq - 1);
     double2 nv[E];
 #pragma unroll
@@ -716,8 +736,8 @@ __global__ void __launch_bounds__(256, 3) pcr_reg_kernel(const Geometry g, Alpha
   for (int k = 0; k < E; ++k) xl[(size_t)(c + (k << logS)) * R + rr + col] = cmul(y[k], ie);
 }
 
-// Small-stride levels 0..jA-1 on contiguous chunks of C with halos of H >= 2^jA - 1 (redundant
-// halo computation, out of place X -> Y).
+// Small-stride levels 0..jA-1 (each for all F factors) on contiguous chunks of C with halos of
+// H >= F (2^jA - 1) (redundant halo computation, out of place X -> Y).
 constexpr int kChunkThreads = 512;
 constexpr int kChunkIPT = 10;
 
@@ -734,12 +754,13 @@ __global__ void __launch_bounds__(kChunkThreads) pcr_chunk_kernel(const Geometry
   const int S = C + 2 * H;
   for (int i = threadIdx.x; i < S; i += blockDim.x) sm[i] = __ldg(xl + ((n0 - H + i) & (N - 1)));
   __syncthreads();
-  const double2 *coef = at.pcr + (size_t)table_line(g, slots, line) * g.logN * 2;
+  const int F = g.nfac;
+  const double2 *coef = at.pcr + (size_t)table_line(g, slots, line) * g.logN * F * 2;
   int lo = 0;
-  for (int j = 0; j < jA; ++j) {
-    const int h = 1 << j;
-    lo += h;  // valid region after this level: [lo, S - lo)
-    const double2 pj = __ldg(coef + 2 * j), qj = __ldg(coef + 2 * j + 1);
+  for (int jf = 0; jf < jA * F; ++jf) {
+    const int h = 1 << (jf / F);
+    lo += h;  // valid region after this (level, factor): [lo, S - lo)
+    const double2 pj = __ldg(coef + 2 * jf), qj = __ldg(coef + 2 * jf + 1);
     const int cnt = S - 2 * lo;
     double2 nv[kChunkIPT];
 #pragma unroll
@@ -1154,13 +1175,19 @@ LaunchCfg choose_launch(const Geometry &g) {
     } else {
       lc.pcr_mode = 1;
       int jA = g.logN / 2;            // R = 2^jA classes of length N/R
+      lc.pcr_chunk = 4096;
+      if (g.nfac > 1) {
+        // chunk halo F R: keep C + 2 F R within the chunk kernel's register capacity
+        // (kChunkThreads * kChunkIPT) and the class length N/R within the class pass's (4096)
+        lc.pcr_chunk = 2048;
+        while (jA > 1 && lc.pcr_chunk + 2 * g.nfac * (1 << jA) > kChunkThreads * kChunkIPT) --jA;
+      }
       lc.pcr_R = 1 << jA;
       int nq = g.N / lc.pcr_R;
       int t = 4096 / nq;
       if (t > lc.pcr_R) t = lc.pcr_R;
       if (t < 1) t = 1;
       lc.pcr_T = t;
-      lc.pcr_chunk = 4096;
       if (lc.pcr_chunk > g.N) lc.pcr_chunk = g.N;
     }
   }
@@ -1188,6 +1215,19 @@ static cudaError_t set_smem(const void *fn, size_t bytes) {
   // always opt in: static shared memory (reduction scratch) adds to the dynamic bytes
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
+
+template <int E>
+static cudaError_t launch_pcr_reg(const Geometry &g, const AlphaTables &at, double2 *X, int R, int T, int jOff,
+                                  const double2 *r0, const int *slots, int grid, size_t smem, cudaStream_t s) {
+  cudaError_t e;
+#define PINT_PCRREG(F_)                                                                       \
+  if ((e = set_smem((const void *)pcr_reg_kernel<E, F_>, smem)) != cudaSuccess) return e;     \
+  pcr_reg_kernel<E, F_><<<grid, 256, smem, s>>>(g, at, X, R, T, jOff, r0, slots);
+  if (g.nfac == 1) { PINT_PCRREG(1) } else if (g.nfac == 2) { PINT_PCRREG(2) } else { PINT_PCRREG(3) }
+#undef PINT_PCRREG
+  return cudaGetLastError();
+}
+
 
 #define PINT_DISPATCH_M(M_, ...)       \
   switch (M_) {                        \
@@ -1234,17 +1274,27 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     int BX, BY;
     residual_block(g, BX, BY);
     if (pk && BY > g.ny / 2) BY = g.ny / 2;
-    const size_t rs = (size_t)(pk ? 2 : 1) * g.M * (BX + 2) * (BY + 2) * sizeof(double2);
+    const int hw = g.hw < 1 ? 1 : g.hw;
+    auto rbytes = [&](int bx, int by) {
+      return (size_t)(pk ? 2 : 1) * g.M * (bx + 2 * hw) * (by + 2 * hw) * sizeof(double2);
+    };
+    while (rbytes(BX, BY) > 200 * 1024) {   // wide halos at large M: smaller blocks
+      if (BY > 1) BY >>= 1;
+      else BX >>= 1;
+    }
+    const size_t rs = rbytes(BX, BY);
     const int rgrid = g.L * (g.nx / BX) * ((pk ? g.ny / 2 : g.ny) / BY);
+#define PINT_RES2D(MM_, PK_, HW_)                                                                   \
+  e = set_smem((const void *)residual2d_kernel<MM_, PK_, HW_>, rs);                                  \
+  if (e == cudaSuccess) residual2d_kernel<MM_, PK_, HW_><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
     PINT_DISPATCH_M(g.M, {
       if (pk) {
-        e = set_smem((const void *)residual2d_kernel<MM, true>, rs);
-        if (e == cudaSuccess) residual2d_kernel<MM, true><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
+        if (hw == 1) { PINT_RES2D(MM, true, 1) } else if (hw == 2) { PINT_RES2D(MM, true, 2) } else { PINT_RES2D(MM, true, 3) }
       } else {
-        e = set_smem((const void *)residual2d_kernel<MM, false>, rs);
-        if (e == cudaSuccess) residual2d_kernel<MM, false><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
+        if (hw == 1) { PINT_RES2D(MM, false, 1) } else if (hw == 2) { PINT_RES2D(MM, false, 2) } else { PINT_RES2D(MM, false, 3) }
       }
     });
+#undef PINT_RES2D
     rec(s);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1281,15 +1331,15 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       const int Sr = nq / E, Tr = Sr > 0 ? 256 / Sr : 0;
       if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
         const size_t smr = (size_t)nq * Tr * sizeof(double2);
-        if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
-        pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, nullptr, st.slots);
+        if ((e = launch_pcr_reg<E>(g, at, b.X, R, Tr, jOff, nullptr, st.slots, lines * (R / Tr), smr, s)) != cudaSuccess)
+          return e;
       } else {
         if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
         pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, nullptr, st.slots);
       }
       rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
-      const int C = lc.pcr_chunk, H = R;
+      const int C = lc.pcr_chunk, H = R * g.nfac;
       smem = (size_t)(C + 2 * H) * sizeof(double2);
       if ((e = set_smem((const void *)pcr_chunk_kernel, smem)) != cudaSuccess) return e;
       pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smem, s>>>(g, at, b.X, b.Y, C, H, jOff, st.slots);
@@ -1500,8 +1550,8 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   const int Sr = nq / E, Tr = Sr > 0 ? 256 / Sr : 0;
   if (nq >= E && Sr <= 32 && Tr >= 1 && Tr <= R) {
     const size_t smr = (size_t)nq * Tr * sizeof(double2);
-    if ((e = set_smem((const void *)pcr_reg_kernel<E>, smr)) != cudaSuccess) return e;
-    pcr_reg_kernel<E><<<lines * (R / Tr), 256, smr, s>>>(g, at, b.X, R, Tr, jOff, r0, st.slots);
+    if ((e = launch_pcr_reg<E>(g, at, b.X, R, Tr, jOff, r0, st.slots, lines * (R / Tr), smr, s)) != cudaSuccess)
+      return e;
   } else {
     const size_t smem = (size_t)nq * T * sizeof(double2);
     if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
@@ -1509,7 +1559,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   }
   rec(s);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int C = lc.pcr_chunk, H = R;
+  const int C = lc.pcr_chunk, H = R * g.nfac;
   const size_t smc = (size_t)(C + 2 * H) * sizeof(double2);
   if ((e = set_smem((const void *)pcr_chunk_kernel, smc)) != cudaSuccess) return e;
   pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smc, s>>>(g, at, b.X, b.Y, C, H, jOff, st.slots);

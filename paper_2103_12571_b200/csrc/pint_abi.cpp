@@ -78,7 +78,7 @@ static pint_status validate(const pint_problem *p, const pint_dist *d) {
   if (p->dim == 2 && (!is_pow2(p->ny) || p->ny < 4)) return fail(PINT_ERR_INVALID, "ny must be a power of two >= 4");
   if (p->nx > (1 << 20) || p->ny > 4096) return fail(PINT_ERR_INVALID, "grid too large");
   if (p->dim == 2 && (p->nx > 4096)) return fail(PINT_ERR_INVALID, "2-D nx must be <= 4096");
-  if (p->op != PINT_OP_HEAT && p->op != PINT_OP_ADVECTION) return fail(PINT_ERR_INVALID, "unknown op");
+  if (p->op < PINT_OP_HEAT || p->op > PINT_OP_UPWIND5) return fail(PINT_ERR_INVALID, "unknown op");
   if (!is_pow2(p->L) || p->L > 1024) return fail(PINT_ERR_INVALID, "L must be a power of two <= 1024 (P:592)");
   if (p->M < 1 || p->M > PINT_MAX_M) return fail(PINT_ERR_INVALID, "M must be in [1, 8]");
   if (!(p->T > 0) || !std::isfinite(p->T)) return fail(PINT_ERR_INVALID, "T must be > 0");
@@ -111,23 +111,17 @@ static Geometry make_geometry(const pint_problem *p, int P) {
   g.lognx = ilog2(g.nx);
   g.logny = ilog2(g.ny);
   g.dT = p->T / p->L;      // global step size
-  const double nx = g.nx, ny = g.ny;
-  if (p->op == PINT_OP_HEAT) {
-    g.cxm = g.cxp = p->nu * nx * nx;
-    g.c0 = -2.0 * p->nu * nx * nx;
-    if (g.dim == 2) {
-      g.cym = g.cyp = p->nu * ny * ny;
-      g.c0 += -2.0 * p->nu * ny * ny;
-    }
-  } else {
-    g.cxm = p->cx * nx / 2.0;   // -c n/2 (u_{j+1} - u_{j-1})
-    g.cxp = -p->cx * nx / 2.0;
-    if (g.dim == 2) {
-      g.cym = p->cy * ny / 2.0;
-      g.cyp = -p->cy * ny / 2.0;
-    }
-    g.c0 = 0.0;
+  // stencil weights (long double rationals rounded once; readings R8, R14)
+  AxisStencil sx, sy;
+  axis_stencil(p->op, g.nx, op_is_heat(p->op) ? p->nu : p->cx, sx);
+  if (g.dim == 2) axis_stencil(p->op, g.ny, op_is_heat(p->op) ? p->nu : p->cy, sy);
+  g.hx0 = sx.h0; g.hx1 = sx.h1; g.hy0 = sy.h0; g.hy1 = sy.h1;
+  g.hw = std::max(std::max(sx.h0, sx.h1), std::max(sy.h0, sy.h1));
+  for (int o = 0; o < 7; ++o) {
+    g.wx[o] = (double)(o == 3 ? sx.w[3] + sy.w[3] : sx.w[o]);
+    g.wy[o] = o == 3 ? 0.0 : (double)sy.w[o];
   }
+  g.nfac = g.dim == 1 ? stencil_factor_count(p->op, sx) : 1;
   return g;
 }
 
@@ -160,7 +154,7 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   per += 2 * LM * g.M * sizeof(double2);                                   // Sinv, SG
   per += LM * sizeof(double2);                                             // shift
   per += LM * sizeof(double2);                                             // sig (row sums of S^{-1})
-  if (g.dim == 1) per += LM * g.logN * 2 * sizeof(double2) + LM * sizeof(double2);  // pcr, inv_e
+  if (g.dim == 1) per += LM * g.logN * g.nfac * 2 * sizeof(double2) + LM * sizeof(double2);  // pcr, inv_e
   L.alpha_bytes_each = align_up(per, 256);
   off += L.alpha_bytes_each * PINT_MAX_SCHEDULE;
   L.off_red = off;
@@ -272,17 +266,13 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   size_t o_twy = o; tw(g.ny);
   auto lam = [&](int n, double coef) {
     for (int k = 0; k < n; ++k) {
-      if (p->op == PINT_OP_HEAT) {
-        ld sn = sinl(3.141592653589793238462643383279502884L * k / n);
-        host[o++] = make_double2((double)(-4.0L * coef * (ld)n * n * sn * sn), 0.0);
-      } else {
-        cld w = unit_root(k, n, +1);  // sin(2 pi k / n) = Im e^{+2 pi i k/n}
-        host[o++] = make_double2(0.0, (double)(-(ld)coef * n * w.imag()));
-      }
+      const cld v = axis_symbol(p->op, n, k, coef);
+      host[o++] = make_double2((double)v.real(), (double)v.imag());
     }
   };
-  size_t o_lx = o; lam(g.nx, p->op == PINT_OP_HEAT ? p->nu : p->cx);
-  size_t o_ly = o; lam(g.ny, p->op == PINT_OP_HEAT ? p->nu : p->cy);
+  const bool heat = op_is_heat(p->op);
+  size_t o_lx = o; lam(g.nx, heat ? p->nu : p->cx);
+  size_t o_ly = o; lam(g.ny, heat ? p->nu : p->cy);
   if (g.dim == 1) for (size_t i = o_ly; i < o_ly + g.ny; ++i) host[i] = make_double2(0, 0);
   size_t o_u0 = o;
   c->u0.assign(u0_host, u0_host + 2 * (size_t)g.N);
@@ -385,13 +375,10 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
   const int L = g.L, M = g.M;            // L: local step / frequency-slot count
   const int Lg = c->prob.L, P = c->P, rank = c->rank;
   const ld dT = (ld)c->prob.T / Lg;
-  // A's stencil as (sub, diag, super) for the 1-D PCR coefficients
-  ld aA, bA, cA;
-  if (c->prob.op == PINT_OP_HEAT) {
-    aA = (ld)c->prob.nu * g.nx * g.nx; cA = aA; bA = -2 * aA;
-  } else {
-    aA = (ld)c->prob.cx * g.nx / 2; cA = -aA; bA = 0;
-  }
+  // A's stencil along x for the 1-D PCR factors (host_numerics: factor_shifted)
+  AxisStencil sx;
+  axis_stencil(c->prob.op, g.nx, op_is_heat(c->prob.op) ? c->prob.nu : c->prob.cx, sx);
+  const int F = g.nfac;
   std::vector<AlphaTables> tabs(K);
   std::vector<std::vector<cld>> hS(K), hSi(K), hD(K), hdk(K);
   std::vector<char> blob(c->lay.alpha_bytes_each);
@@ -409,7 +396,7 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
     size_t off_pcr = 0, off_inv = 0;
     if (g.dim == 1) {
       off_pcr = off;
-      pcr = (double2 *)(blob.data() + off); off += (size_t)L * M * g.logN * 2 * sizeof(double2);
+      pcr = (double2 *)(blob.data() + off); off += (size_t)L * M * g.logN * F * 2 * sizeof(double2);
       off_inv = off;
       inv_e = (double2 *)(blob.data() + off); off += (size_t)L * M * sizeof(double2);
     }
@@ -466,24 +453,36 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
         const cld s = lam[m] * dT;                          // (I - d_km dT A)
         shift[(size_t)p * M + m] = make_double2((double)s.real(), (double)s.imag());
         if (g.dim == 1) {
-          // row-sum-carrying PCR coefficients (reading R6): e = a + b + c = 1 - s*(aA+bA+cA)
-          cld ca = -s * aA, cc = -s * cA;
-          cld e = 1.0L - s * (aA + bA + cA);
-          cld cb = e - ca - cc;
-          double2 *lev = pcr + ((size_t)p * M + m) * g.logN * 2;
-          for (int j = 0; j < g.logN - 1; ++j) {
-            cld pj = ca / cb, qj = cc / cb;
-            lev[2 * j] = make_double2((double)pj.real(), (double)pj.imag());
-            lev[2 * j + 1] = make_double2((double)qj.real(), (double)qj.imag());
-            cld e2 = e * (e - 2.0L * (ca + cc)) / cb;
-            cld a2 = -ca * ca / cb, c2 = -cc * cc / cb;
-            ca = a2; cc = c2; e = e2; cb = e - ca - cc;
+          // I - s A = lead prod_f T_f; row-sum-carrying PCR coefficients per factor (DESIGN.md
+          // reading R6), levels interleaved: lev[(j F + f) 2 + {0, 1}] = (p_j, q_j) of factor f
+          std::vector<TriFactor> fac;
+          cld lead;
+          std::string ferr;
+          if (!factor_shifted(c->prob.op, sx, s, fac, lead, ferr) || (int)fac.size() != F) {
+            char buf[256];
+            snprintf(buf, sizeof buf, "1-D spatial factorisation failed for alpha=%.6g, k=%d, m=%d: %s",
+                     (double)al, k, m, ferr.c_str());
+            return fail(PINT_ERR_NUMERIC, buf);
           }
-          cld pl = (ca + cc) / cb;                          // pair level: i-h == i+h
-          lev[2 * (g.logN - 1)] = make_double2((double)pl.real(), (double)pl.imag());
-          lev[2 * (g.logN - 1) + 1] = make_double2(0.0, 0.0);
-          e = e * (e - 2.0L * (ca + cc)) / cb;
-          cld ie = 1.0L / e;
+          double2 *lev = pcr + ((size_t)p * M + m) * g.logN * F * 2;
+          cld ie = 1.0L / lead;
+          for (int f = 0; f < F; ++f) {
+            cld ca = fac[f].a, cc = fac[f].c, e = fac[f].e;
+            cld cb = e - ca - cc;
+            for (int j = 0; j < g.logN - 1; ++j) {
+              cld pj = ca / cb, qj = cc / cb;
+              lev[(j * F + f) * 2] = make_double2((double)pj.real(), (double)pj.imag());
+              lev[(j * F + f) * 2 + 1] = make_double2((double)qj.real(), (double)qj.imag());
+              cld e2 = e * (e - 2.0L * (ca + cc)) / cb;
+              cld a2 = -ca * ca / cb, c2 = -cc * cc / cb;
+              ca = a2; cc = c2; e = e2; cb = e - ca - cc;
+            }
+            cld pl = (ca + cc) / cb;                        // pair level: i-h == i+h
+            lev[((g.logN - 1) * F + f) * 2] = make_double2((double)pl.real(), (double)pl.imag());
+            lev[((g.logN - 1) * F + f) * 2 + 1] = make_double2(0.0, 0.0);
+            e = e * (e - 2.0L * (ca + cc)) / cb;
+            ie /= e;
+          }
           inv_e[(size_t)p * M + m] = make_double2((double)ie.real(), (double)ie.imag());
         }
       }

@@ -178,3 +178,33 @@ def edge_cases():
         base.replace(name="edge_2d_adv_16x8_M3", dim=2, nx=16, ny=8, op="advection", nu=0.0,
                      cx=1.0, cy=-0.5, M=3, L=8),
     ]
+
+
+def discretisation_cases():
+    """The paper's other spatial discretisations (Tables 1-2; reading R14) at
+    parity size: the Table 2 pairings (heat: kappa 2/4/6 with M 1/2/3; advection u_t + u_x + u_y = 0
+    (P:715-718), upwind kappa 1/3/5 with M 1/2/3) on small periodic grids, L = 16 steps of
+    dT = T_64/64, plus 1-D variants, a two-pass 1-D size, a smem-engine 2-D shape and a mirrored
+    (c < 0) upwind stencil.  Seeded random u0 (complex) unless stated."""
+    heat = Problem("disc", 2, 32, 32, "heat", 1.0, 0.0, 0.0, 0.16 / 4, 16, 2, "random", "fixed", 1e-3, 3)
+    adv = heat.replace(op="upwind1", nu=0.0, cx=1.0, cy=1.0)
+    out = []
+    for op, M, T64 in (("heat", 1, 0.32), ("heat4", 2, 0.16), ("heat6", 3, 0.16)):
+        out.append(heat.replace(name=f"disc_{op}_2d_M{M}", op=op, M=M, T=T64 / 4))
+        out.append(heat.replace(name=f"disc_{op}_1d_M{M}", op=op, M=M, T=T64 / 4, dim=1, nx=128, ny=1))
+    for op, M, T64 in (("upwind1", 1, 0.00016), ("upwind3", 2, 0.00064), ("upwind5", 3, 0.0128)):
+        out.append(adv.replace(name=f"disc_{op}_2d_M{M}", op=op, M=M, T=T64 / 4))
+        out.append(adv.replace(name=f"disc_{op}_1d_M{M}", op=op, M=M, T=T64 / 4, dim=1, nx=128, ny=1, cy=0.0))
+    # stiffer advection (|s c n| ~ 10) and flow to the left (mirrored stencils)
+    out.append(adv.replace(name="disc_upwind5_1d_neg_stiff", op="upwind5", M=3, T=1.0, cx=-1.0, cy=0.0,
+                           dim=1, nx=128, ny=1))
+    out.append(adv.replace(name="disc_upwind3_2d_mixed_sign", op="upwind3", M=2, T=0.05, cx=0.8, cy=-0.6))
+    # two-pass 1-D PCR (class pass + chunk pass with halo F R) and a 2-D shape served by the
+    # smem-engine kernels (|log nx - log ny| > 1)
+    out.append(heat.replace(name="disc_heat6_1d_N16384", op="heat6", M=2, T=0.01, dim=1, nx=16384, ny=1,
+                            L=4, nu=1e-2))
+    out.append(adv.replace(name="disc_upwind5_1d_N16384", op="upwind5", M=2, T=0.01, dim=1, nx=16384, ny=1,
+                           L=4, cy=0.0))
+    out.append(heat.replace(name="disc_heat4_2d_64x8", op="heat4", M=2, nx=64, ny=8))
+    out.append(heat.replace(name="disc_heat6_2d_M8", op="heat6", M=8, nx=16, ny=16, L=4, T=0.01))
+    return out
