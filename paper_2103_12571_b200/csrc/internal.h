@@ -99,6 +99,7 @@ struct SpatialPlan {
   int synth;                  // direct form: C synthesizes sig_q * r0hat, no R stage
   int nstage, rounds;         // 3 (R, C, I) or 2 (C, I); nbatch + nstage - 1
   int skip;                   // timing experiments only (PINT_SP_SKIP): bit s = stage s does no work
+  int claim;                  // 1: items claimed from a device counter; 0: static t = cta (mod grid)
 };
 SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth);
 int spatial_maxb(const Geometry &g);   // largest radix (log2) of the spatial FFT plan in use

@@ -304,19 +304,41 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
   copy_table(twx, st.ptwx, TWX);
   copy_table(twy, st.ptwy, TWY);
   __syncthreads();
-  const int G = gridDim.x, cta = blockIdx.x;
   const int riPerBatch = g.ny / sp.YR, cPerLine = g.nx / sp.TC;
   const bool node = st.P == 1;   // P > 1: the node transforms live in the cross-rank DFT kernels
-  long long rs = 0;   // sequence position of the current round's first item
-  for (int j = 0; j < sp.rounds; ++j) {
-    // stage segments of round j: stage index si works on batch j - si
-    const int first = sp.synth ? kStC : kStR;
+  const int first = sp.synth ? kStC : kStR;
+  // Items are claimed dynamically in sequence order (round j: the active stage segments, stage
+  // index si works on batch j - si; R(j), C(j-1), I(j-2)) from one device counter.  Every item
+  // depends only on items of earlier rounds (lower sequence numbers), all of which were claimed
+  // before it by CTAs that are running (cooperative launch), so the waits cannot deadlock.  The
+  // next claim is issued at the start of an item and consumed at its end (latency hidden).
+  unsigned *claim = sync + 3 * sp.nbatch;
+  __shared__ unsigned s_next;
+  auto round_count = [&](int j) {
     const int slo = j - (sp.nbatch - 1) > 0 ? j - (sp.nbatch - 1) : 0;
     const int shi = j < sp.nstage - 1 ? j : sp.nstage - 1;
     int rn = 0;
     for (int si = slo; si <= shi; ++si) rn += (first + si == kStC) ? sp.nC : sp.nRI;
-    int k = (int)(((cta - rs) % G + G) % G);
-    for (; k < rn; k += G) {
+    return rn;
+  };
+  if (threadIdx.x == 0) s_next = sp.claim ? atomicAdd(claim, 1u) : blockIdx.x;
+  __syncthreads();
+  unsigned t = s_next;
+  int j = 0;
+  long long rs = 0;            // sequence number of round j's first item
+  int rn = round_count(0);
+  for (;;) {
+    while (j < sp.rounds && (long long)t >= rs + rn) {
+      rs += rn;
+      ++j;
+      if (j < sp.rounds) rn = round_count(j);
+    }
+    if (j >= sp.rounds) break;
+    unsigned nxt = 0;
+    if (threadIdx.x == 0) nxt = sp.claim ? atomicAdd(claim, 1u) : t + gridDim.x;   // static: t = cta mod G
+    const int slo = j - (sp.nbatch - 1) > 0 ? j - (sp.nbatch - 1) : 0;
+    {
+      const int k = (int)((long long)t - rs);
       int si = slo, kk = k;
       for (;;) {
         const int n = (first + si == kStC) ? sp.nC : sp.nRI;
@@ -354,9 +376,11 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
           i_item<PX>(g, at, tile, nt, twx, xp, slot, y0, sp.YR, node);
         }
       }
-      publish(sync + stage * sp.nbatch + b);
+      if (threadIdx.x == 0) s_next = nxt;
+      publish(sync + stage * sp.nbatch + b);   // its barrier also publishes s_next to the CTA
+      t = s_next;
+      __syncthreads();   // every thread has read s_next before thread 0 may overwrite it
     }
-    rs += rn;
   }
 }
 
@@ -396,11 +420,13 @@ SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth) {
   sp.nstage = synth ? 2 : 3;
   const char *sk = getenv("PINT_SP_SKIP");   // timing experiments only: bit s skips stage s (R, C, I)
   sp.skip = sk ? atoi(sk) : 0;
+  const char *cl = getenv("PINT_SP_CLAIM");  // A/B experiments: 0 = static round-robin assignment
+  sp.claim = cl ? atoi(cl) : 1;
   sp.rounds = sp.nbatch + sp.nstage - 1;
   return sp;
 }
 
-size_t spatial_sync_bytes(int lines) { return (size_t)3 * lines * sizeof(unsigned); }
+size_t spatial_sync_bytes(int lines) { return (size_t)(3 * lines + 1) * sizeof(unsigned); }   // + claim counter
 
 bool spatial2d_supported(const Geometry &g) {
   const int d = g.lognx - g.logny;
@@ -442,7 +468,7 @@ cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const Al
                              const double2 *spec, unsigned *sync, int lines, cudaStream_t s) {
   if (!spatial2d_supported(g)) return cudaErrorInvalidValue;
   const SpatialPlan sp = make_spatial_plan(g, lines, spec != nullptr);
-  cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)3 * sp.nbatch * sizeof(unsigned), s);
+  cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)(3 * sp.nbatch + 1) * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
 #define PINT_SP(LXX, LYY) \
   if (g.lognx == LXX && g.logny == LYY) return launch_sp<LXX, LYY, 4>(g, st, at, sp, X, spec, sync, s);
