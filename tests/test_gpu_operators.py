@@ -76,3 +76,40 @@ def test_paper_heat_problem_converges_to_sequential():
     ref = sequential_solution(p, Tableau(p.M), u0, v)
     assert relative_l2(s.get_iterate(), ref) < 1e-10
     s.close()
+
+
+SHARDED = [("disc_heat6_2d_M3", 2), ("disc_upwind5_2d_M3", 4), ("disc_upwind3_1d_M2", 2),
+           ("disc_heat6_1d_N16384", 2)]
+
+
+@pytest.mark.parametrize("name,P", SHARDED, ids=lambda x: str(x))
+def test_operator_parity_sharded(name, P):
+    """Wider stencils through the time-sharded path (P virtual ranks on one GPU, loopback group)."""
+    import paper_2103_12571_b200 as PB
+    p = next(c for c in CASES if c.name == name)
+    u0 = p.u0()
+    grp = PB.Group(p, u0, P)
+    grp.set_alpha_schedule([1e-3] * 3)
+    o = Oracle(p, u0, "dense" if p.M * p.N <= 1024 else "fourier")
+    u = o.initial()
+    for k in range(3):
+        u = o.iterate(u, 1e-3)
+        grp.iterate(1)
+        e = relative_l2(grp.get_iterate(), u)
+        assert e <= TOL, (k, e)
+    grp.close()
+
+
+@pytest.mark.parametrize("name", ["disc_heat6_2d_M3", "disc_upwind5_2d_M3", "disc_upwind3_2d_mixed_sign"])
+def test_operator_sequential_baseline(name):
+    """The GPU sequential Radau IIA baseline with the wider stencils against the oracle's stepping."""
+    import paper_2103_12571_b200 as PB
+    from oracle.collocation import Tableau
+    from oracle.paralpha import sequential_solution
+    p = next(c for c in CASES if c.name == name)
+    u0 = p.u0()
+    s = PB.Solver(p, u0)
+    s.sequential()
+    ref = sequential_solution(p, Tableau(p.M), u0)
+    assert relative_l2(s.get_iterate(), ref) <= 1e-11
+    s.close()
