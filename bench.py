@@ -351,6 +351,8 @@ def main():
     # ---- sequential Radau IIA baseline on the same GPU (2-D, 1 rank) ------------
     seq = None
     if world == 1 and p.dim == 2 and not args.no_sequential:
+        if args.hermitian:
+            s.set_hermitian(False)                       # the sequential baseline uses complex storage
         s.sequential()                                   # warm-up
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -359,6 +361,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         sms_ = e0.elapsed_time(e1)
+        if args.hermitian:
+            s.set_hermitian(True)
         s.set_initial_value(u0, reset=True)
         tol = 1e-10 * float(np.abs(u0).max())
         r = s.solve(p.m0, tol, 40, p.eps, p.tau)        # Algorithm 2 to tol (host-timed, not the metric)

@@ -155,10 +155,14 @@ pint_status pint_set_form(pint_ctx *c, int32_t form);
  * by the solve.  Same result as on = 0 up to the roundoff imaginary part of the iterate (which
  * on = 1 projects out).  The time transforms run on complex series that pack two real points,
  * z_l(n') = r_l(n') + i r_l(n' + N/2), so they do half the work; the solves unpack X_k from the
- * slots of k and L - k and the backward pass repacks both slots from one read.  The iterate stays
- * complex128 in u_dev with zero imaginary parts.  Requirements: nranks == 1, u0 real (imaginary
+ * slots of k and L - k and the backward pass repacks both slots from one read.  Storage: while
+ * on, the iterate is REAL fp64 u[l][m][n] in the first L M N doubles of u_dev (half the bytes of
+ * every iterate read and write); switching on converts the current iterate (dropping its
+ * roundoff imaginary parts), switching off converts back to complex128.  pint_get_iterate and
+ * pint_get_final_value still return (re, 0) pairs.  Requirements: nranks == 1, u0 real (imaginary
  * parts exactly 0; pint_set_initial_value then rejects non-real data), 2-D: grids of the register
- * FFT engine, 4 <= L <= 1024; 1-D: N >= 8.  Errors: PINT_ERR_INVALID. */
+ * FFT engine, 4 <= L <= 1024; 1-D: N >= 8; not with pint_sequential.  Errors:
+ * PINT_ERR_INVALID, PINT_ERR_CUDA (storage conversion). */
 pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
 
 /* Forcing b != 0: w = (u0 + v_0, v_1, ..., v_{L-1}) with

@@ -32,38 +32,50 @@ __device__ __forceinline__ double2 prev_value(const StaticTables &st, int l, int
   return jj < 0 ? __ldg(st.u0 + n) : __ldg(st.prev_base + (long long)jj * st.prev_stride + n);
 }
 
-template <int M>
+// Hermitian (packed) mode stores the iterate as real fp64 u[l][m][n] in the first L M N doubles
+// of u_dev (its imaginary parts are zero in exact arithmetic)
+__device__ __forceinline__ double2 u_at(const double2 *__restrict__ u, size_t i, bool real) {
+  return real ? make_double2(__ldg((const double *)u + i), 0.0) : __ldg(u + i);
+}
+
+template <int M, bool REAL = false, int HW = 3>
 __device__ __forceinline__ void residual_point(const Geometry &g, const StaticTables &st,
                                                const double2 *__restrict__ u, int l, int n, double2 r[M]) {
+  constexpr bool real = REAL;   // Hermitian mode: real storage (st.packed)
   const size_t plane = (size_t)M * g.N;
-  const double2 *ul = u + (size_t)l * plane;
+  const size_t ul = (size_t)l * plane;
   const int x = n & (g.nx - 1);
   const int y = n >> g.lognx;
   const int row = y << g.lognx;
   double2 uc[M], Au[M];
 #pragma unroll
   for (int j = 0; j < M; ++j) {
-    const double2 *uj = ul + (size_t)j * g.N;
-    const double2 c = __ldg(uj + n);
+    const size_t uj = ul + (size_t)j * g.N;
+    const double2 c = u_at(u, uj + n, real);
     uc[j] = c;
     double2 s = make_double2(g.wx[3] * c.x, g.wx[3] * c.y);
-    for (int o = -g.hx0; o <= g.hx1; ++o) {
-      if (o == 0) continue;
-      const double2 v = __ldg(uj + row + ((x + o) & (g.nx - 1)));
+    // unrolled over the halo HW (1: the 3-point operators, whose missing offsets carry weight 0;
+    // 3: any stencil, offsets outside [-h0, h1] skipped by uniform predicates)
+#pragma unroll
+    for (int o = -HW; o <= HW; ++o) {
+      if (o == 0 || (HW > 1 && (o < -g.hx0 || o > g.hx1))) continue;
+      const double2 v = u_at(u, uj + row + ((x + o) & (g.nx - 1)), real);
       s.x = fma(g.wx[3 + o], v.x, s.x);
       s.y = fma(g.wx[3 + o], v.y, s.y);
     }
     if (g.dim == 2) {
-      for (int o = -g.hy0; o <= g.hy1; ++o) {
-        if (o == 0) continue;
-        const double2 v = __ldg(uj + ((((y + o) & (g.ny - 1)) << g.lognx) + x));
+#pragma unroll
+      for (int o = -HW; o <= HW; ++o) {
+        if (o == 0 || (HW > 1 && (o < -g.hy0 || o > g.hy1))) continue;
+        const double2 v = u_at(u, uj + ((((y + o) & (g.ny - 1)) << g.lognx) + x), real);
         s.x = fma(g.wy[3 + o], v.x, s.x);
         s.y = fma(g.wy[3 + o], v.y, s.y);
       }
     }
     Au[j] = s;
   }
-  const double2 base = prev_value(st, l, n);   // w (global l = 0) or the H-term u_{l-1, M-1}
+  // w (global l = 0) or the H-term u_{l-1, M-1} (real storage: one rank, previous local step)
+  const double2 base = real ? (l == 0 ? __ldg(st.u0 + n) : u_at(u, ul - g.N + n, true)) : prev_value(st, l, n);
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     double2 acc = csub(base, uc[m]);
@@ -95,7 +107,7 @@ constexpr int kSpaceMinBlocks = 2;  // spatial FFT passes: radix <= 16, 128 regi
 // r(n') + i r(n' + N/2), n' = n0 + t < N/2; after the FFT the node step unpacks X_k from the slots
 // of k and L - k (both in the tile), applies S_k^{-1} and writes unit q's lines (X + q M N) at n'
 // and n' + N/2.
-template <int M, bool RESID, bool NODE, bool PACK = false>
+template <int M, bool RESID, bool NODE, bool PACK = false, int HW = 1>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     fwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ u,
                double2 *__restrict__ X, int T) {
@@ -112,11 +124,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
       const int t = it & (T - 1), l = it >> lT;
       double2 r[M];
-      residual_point<M>(g, st, u, l, n0 + t, r);
+      residual_point<M, PACK, HW>(g, st, u, l, n0 + t, r);
       const double sc = __ldg(at.scale_fwd + l);
       if (PACK) {
         double2 r2[M];
-        residual_point<M>(g, st, u, l, n0 + t + g.N / 2, r2);
+        residual_point<M, PACK, HW>(g, st, u, l, n0 + t + g.N / 2, r2);
 #pragma unroll
         for (int m = 0; m < M; ++m) sm[sidx<false>((l * M + m) * T + t)] = make_double2(r[m].x * sc, r2[m].x * sc);
       } else {
@@ -280,8 +292,13 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), row = idx >> lT;
         const bool need_old = !overwrite || (diff_slot && row / M == L - 1);
-        uo[k] = need_old ? u[(size_t)row * g.N + n0 + t] : make_double2(0.0, 0.0);
-        if (PACK) uo2[k] = need_old ? u[(size_t)row * g.N + n0 + t + g.N / 2] : make_double2(0.0, 0.0);
+        if (PACK) {   // real storage
+          const double *ur = (const double *)u + (size_t)row * g.N + n0 + t;
+          uo[k] = make_double2(need_old ? ur[0] : 0.0, 0.0);
+          uo2[k] = make_double2(need_old ? ur[g.N / 2] : 0.0, 0.0);
+        } else {
+          uo[k] = need_old ? u[(size_t)row * g.N + n0 + t] : make_double2(0.0, 0.0);
+        }
         sc[k] = __ldg(at.scale_bwd + row / M);
       }
     }
@@ -291,13 +308,13 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), row = idx >> lT;
         const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
-        if (PACK) {   // real points n' (Re c) and n' + N/2 (Im c); imaginary parts of u stay 0
-          const double2 n1 = make_double2(overwrite ? c.x : uo[k].x + c.x, 0.0);
-          const double2 n2 = make_double2(overwrite ? c.y : uo2[k].x + c.y, 0.0);
-          u[(size_t)row * g.N + n0 + t] = n1;
-          u[(size_t)row * g.N + n0 + t + g.N / 2] = n2;
-          if (row / M == L - 1)
-            dmax = fmax(dmax, fmax(hypot(n1.x - uo[k].x, uo[k].y), hypot(n2.x - uo2[k].x, uo2[k].y)));
+        if (PACK) {   // real points n' (Re c) and n' + N/2 (Im c), stored real
+          const double n1 = overwrite ? c.x : uo[k].x + c.x;
+          const double n2 = overwrite ? c.y : uo2[k].x + c.y;
+          double *ur = (double *)u + (size_t)row * g.N + n0 + t;
+          ur[0] = n1;
+          ur[g.N / 2] = n2;
+          if (row / M == L - 1) dmax = fmax(dmax, fmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
         } else {
           u[(size_t)row * g.N + n0 + t] = overwrite ? c : cadd(uo[k], c);   // direct form: u = C_a^{-1} r
           if (row / M == L - 1) {
@@ -424,8 +441,13 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (idx < all) {
         const int t = idx & (T - 1), l = idx >> lT;
         const bool need_old = !overwrite || (diff_slot && l == g.L - 1);
-        uo[k] = need_old ? ub[(size_t)l * lstride + t] : make_double2(0.0, 0.0);
-        if (PACK) uo2[k] = need_old ? ub[(size_t)l * lstride + t + g.N / 2] : make_double2(0.0, 0.0);
+        if (PACK) {   // real storage (u_dev holds doubles; same element offsets)
+          const double *ur = (const double *)u + (size_t)m * g.N + n0 + (size_t)l * lstride + t;
+          uo[k] = make_double2(need_old ? ur[0] : 0.0, 0.0);
+          uo2[k] = make_double2(need_old ? ur[g.N / 2] : 0.0, 0.0);
+        } else {
+          uo[k] = need_old ? ub[(size_t)l * lstride + t] : make_double2(0.0, 0.0);
+        }
         sc[k] = __ldg(at.scale_bwd + l);
       }
     }
@@ -436,13 +458,13 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
         const int t = idx & (T - 1), l = idx >> lT;
         const double2 c = cscale(sm[sidx<false>(idx)], sc[k]);
         if (PACK) {
-          // real points n' (Re c) and n' + N/2 (Im c); imaginary parts of u stay 0
-          const double2 n1 = make_double2(overwrite ? c.x : uo[k].x + c.x, 0.0);
-          const double2 n2 = make_double2(overwrite ? c.y : uo2[k].x + c.y, 0.0);
-          ub[(size_t)l * lstride + t] = n1;
-          ub[(size_t)l * lstride + t + g.N / 2] = n2;
-          if (l == g.L - 1)
-            dmax = fmax(dmax, fmax(hypot(n1.x - uo[k].x, uo[k].y), hypot(n2.x - uo2[k].x, uo2[k].y)));
+          // real points n' (Re c) and n' + N/2 (Im c), stored real
+          const double n1 = overwrite ? c.x : uo[k].x + c.x;
+          const double n2 = overwrite ? c.y : uo2[k].x + c.y;
+          double *ur = (double *)u + (size_t)m * g.N + n0 + (size_t)l * lstride + t;
+          ur[0] = n1;
+          ur[g.N / 2] = n2;
+          if (l == g.L - 1) dmax = fmax(dmax, fmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
         } else {
           ub[(size_t)l * lstride + t] = overwrite ? c : cadd(uo[k], c);
           if (l == g.L - 1) {
@@ -487,63 +509,105 @@ __global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTable
   const int x0 = bx * BX, y0 = by * BY;
   const int W = BX + 2 * HW, H = BY + 2 * HW;
   const size_t plane = (size_t)M * g.N;
-  const double2 *ul = u + (size_t)l * plane;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NH = PACK ? 2 : 1;
-  for (int r = warp; r < NH * M * H; r += blockDim.x >> 5) {
-    const int hh = r / (M * H), rr = r - hh * M * H;
-    const int j = rr / H, yy = rr - j * H;
-    const int y = (y0 + hh * (g.ny / 2) + yy - HW) & (g.ny - 1);
+  const double sc = __ldg(at.scale_fwd + l);
+  if constexpr (PACK) {
+    // real storage: stage reals, real arithmetic; the CTA's block (hh = 0) and its partner ny/2
+    // rows lower (hh = 1) give Z = Re r(n') + i Re r(n' + N/2)
+    double *smr = (double *)sm;   // [2][M][H][W]
+    const double *ur = (const double *)u + (size_t)l * plane;
+    for (int r = warp; r < 2 * M * H; r += blockDim.x >> 5) {
+      const int hh = r / (M * H), rr = r - hh * M * H;
+      const int j = rr / H, yy = rr - j * H;
+      const int y = (y0 + hh * (g.ny / 2) + yy - HW) & (g.ny - 1);
+      const double *src = ur + (size_t)j * g.N + ((size_t)y << g.lognx);
+      double *dst = smr + r * W;
+      for (int xx = lane; xx < W; xx += 32) cp_async8(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
+      const int ty = pt / BX, tx = pt - ty * BX;
+      const int n = ((y0 + ty) << g.lognx) + x0 + tx;
+      double res[2][M];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int nn = n + hh * (g.N / 2);
+        // one rank: w (l = 0) or the H-term u_{l-1, M-1}
+        const double base = l == 0 ? __ldg(st.u0 + nn).x : __ldg(ur - g.N + nn);
+        double uc[M], Au[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const double *q = smr + ((hh * M + j) * H + ty + HW) * W + tx + HW;
+          const double c = q[0];
+          uc[j] = c;
+          double acc = g.wx[3] * c;
+#pragma unroll
+          for (int o = -HW; o <= HW; ++o) {
+            if (o == 0) continue;
+            acc = fma(g.wx[3 + o], q[o], acc);
+            acc = fma(g.wy[3 + o], q[o * W], acc);
+          }
+          Au[j] = acc;
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          double acc = base - uc[m];
+#pragma unroll
+          for (int j = 0; j < M; ++j) acc = fma(g.dTQ[m * M + j], Au[j], acc);
+          res[hh][m] = acc * sc;
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < M; ++m) X[((size_t)l * M + m) * (g.N / 2) + n] = make_double2(res[0][m], res[1][m]);
+    }
+    return;
+  } else {
+  const double2 *ul = u + (size_t)l * plane;
+  for (int r = warp; r < M * H; r += blockDim.x >> 5) {
+    const int j = r / H, yy = r - j * H;
+    const int y = (y0 + yy - HW) & (g.ny - 1);
     const double2 *src = ul + (size_t)j * g.N + ((size_t)y << g.lognx);
     double2 *dst = sm + r * W;
     for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
   }
   cp_async_wait_all();
   __syncthreads();
-  const double sc = __ldg(at.scale_fwd + l);
   for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
     const int ty = pt / BX, tx = pt - ty * BX;
     const int n = ((y0 + ty) << g.lognx) + x0 + tx;
-    double2 res[NH][M];
+    const double2 base = prev_value(st, l, n);
+    double2 uc[M], Au[M];
 #pragma unroll
-    for (int hh = 0; hh < NH; ++hh) {
-      const double2 base = prev_value(st, l, n + hh * (g.N / 2));
-      double2 uc[M], Au[M];
+    for (int j = 0; j < M; ++j) {
+      const double2 *q = sm + (j * H + ty + HW) * W + tx + HW;
+      const double2 c = q[0];
+      uc[j] = c;
+      double2 acc = make_double2(g.wx[3] * c.x, g.wx[3] * c.y);
 #pragma unroll
-      for (int j = 0; j < M; ++j) {
-        const double2 *s = sm + ((hh * M + j) * H + ty + HW) * W + tx + HW;
-        const double2 c = s[0];
-        uc[j] = c;
-        double2 acc = make_double2(g.wx[3] * c.x, g.wx[3] * c.y);
-#pragma unroll
-        for (int o = -HW; o <= HW; ++o) {
-          if (o == 0) continue;
-          const double2 a = s[o], d = s[o * W];
-          acc.x = fma(g.wx[3 + o], a.x, acc.x);
-          acc.y = fma(g.wx[3 + o], a.y, acc.y);
-          acc.x = fma(g.wy[3 + o], d.x, acc.x);
-          acc.y = fma(g.wy[3 + o], d.y, acc.y);
-        }
-        Au[j] = acc;
+      for (int o = -HW; o <= HW; ++o) {
+        if (o == 0) continue;
+        const double2 a = q[o], d = q[o * W];
+        acc.x = fma(g.wx[3 + o], a.x, acc.x);
+        acc.y = fma(g.wx[3 + o], a.y, acc.y);
+        acc.x = fma(g.wy[3 + o], d.x, acc.x);
+        acc.y = fma(g.wy[3 + o], d.y, acc.y);
       }
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        double2 acc = csub(base, uc[m]);
-        if (!PACK && st.v) acc = cadd(acc, __ldg(st.v + ((size_t)l * M + m) * g.N + n));   // forcing part of w
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-          const double q = g.dTQ[m * M + j];
-          acc.x = fma(q, Au[j].x, acc.x);
-          acc.y = fma(q, Au[j].y, acc.y);
-        }
-        res[hh][m] = cscale(acc, sc);
-      }
+      Au[j] = acc;
     }
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      if (PACK) X[((size_t)l * M + m) * (g.N / 2) + n] = make_double2(res[0][m].x, res[NH - 1][m].x);
-      else X[(size_t)l * plane + (size_t)m * g.N + n] = res[0][m];
+      double2 acc = csub(base, uc[m]);
+      if (st.v) acc = cadd(acc, __ldg(st.v + ((size_t)l * M + m) * g.N + n));   // forcing part of w
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const double q = g.dTQ[m * M + j];
+        acc.x = fma(q, Au[j].x, acc.x);
+        acc.y = fma(q, Au[j].y, acc.y);
+      }
+      X[(size_t)l * plane + (size_t)m * g.N + n] = cscale(acc, sc);
     }
+  }
   }
 }
 
@@ -567,6 +631,7 @@ __device__ __forceinline__ int table_line(const Geometry &g, const int *slots, i
   return __ldg(slots + line / g.M) * g.M + line % g.M;
 }
 
+template <int F>
 __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry g, AlphaTables at,
                                                                   double2 *__restrict__ X, int R, int T,
                                                                   int j_off, const double2 *__restrict__ r0,
@@ -587,8 +652,7 @@ __global__ void __launch_bounds__(kPcrThreads) pcr_classes_kernel(const Geometry
     sm[it] = r0 ? cmul(__ldg(at.sig + tline), __ldg(r0 + (size_t)q * R + rr + tt)) : xl[(size_t)q * R + rr + tt];
   }
   __syncthreads();
-  const int F = g.nfac;
-  const double2 *coef = at.pcr + (size_t)tline * g.logN * F * 2;
+  const double2 *coef = at.pcr + (size_t)tline * g.logN * F * 2;   // F == g.nfac
   for (int jf = 0; jf < lognq * F; ++jf) {   // level jj, factor f (all circulant: any order)
     const int jj = jf / F;
     const int j = j_off + jj;
@@ -900,9 +964,9 @@ __global__ void __launch_bounds__(kColThreads, 1)
 
 __global__ void direct_r0_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ u,
                                  double2 *__restrict__ r0) {
-  const double2 *ul = u + ((size_t)(g.L - 1) * g.M + (g.M - 1)) * g.N;
+  const size_t ul = ((size_t)(g.L - 1) * g.M + (g.M - 1)) * g.N;
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < g.N; n += gridDim.x * blockDim.x) {
-    const double2 a = __ldg(st.u0 + n), b = __ldg(ul + n);
+    const double2 a = __ldg(st.u0 + n), b = u_at(u, ul + n, st.packed != 0);
     r0[n] = make_double2(a.x - at.alpha * b.x, a.y - at.alpha * b.y);
   }
 }
@@ -1076,7 +1140,8 @@ __global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables s
        i += (long long)gridDim.x * blockDim.x) {
     const int l = (int)(i / g.N), n = (int)(i - (long long)l * g.N);
     double2 r[M];
-    residual_point<M>(g, st, u, l, n, r);
+    if (st.packed) residual_point<M, true>(g, st, u, l, n, r);
+    else residual_point<M, false>(g, st, u, l, n, r);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const double a2 = r[m].x * r[m].x + r[m].y * r[m].y;
@@ -1109,11 +1174,24 @@ __global__ void reduce_partials_kernel(const double *partial, int nblocks, doubl
   if (threadIdx.x == 0) { out[0] = sqrt(a); out[1] = b; }
 }
 
-__global__ void init_iterate_kernel(Geometry g, const double2 *__restrict__ u0, double2 *__restrict__ u) {
+__global__ void init_iterate_kernel(Geometry g, const double2 *__restrict__ u0, double2 *__restrict__ u, int real) {
   const long long total = (long long)g.L * g.M * g.N;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x)
-    u[i] = __ldg(u0 + (i % g.N));
+       i += (long long)gridDim.x * blockDim.x) {
+    if (real) ((double *)u)[i] = __ldg(u0 + (i % g.N)).x;
+    else u[i] = __ldg(u0 + (i % g.N));
+  }
+}
+
+// storage conversion of the iterate (pint_set_hermitian): complex <-> real through a scratch
+// vector (in-place compaction would race)
+__global__ void real_parts_kernel(const double2 *__restrict__ src, double *__restrict__ dst, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i].x;
+}
+__global__ void complex_from_real_kernel(const double *__restrict__ src, double2 *__restrict__ dst, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = make_double2(src[i], 0.0);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1216,6 +1294,17 @@ static cudaError_t set_smem(const void *fn, size_t bytes) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+static cudaError_t launch_pcr_classes(const Geometry &g, const AlphaTables &at, double2 *X, int R, int T, int jOff,
+                                      const double2 *r0, const int *slots, int grid, size_t smem, cudaStream_t s) {
+  cudaError_t e;
+#define PINT_PCRCL(F_)                                                                          \
+  if ((e = set_smem((const void *)pcr_classes_kernel<F_>, smem)) != cudaSuccess) return e;      \
+  pcr_classes_kernel<F_><<<grid, kPcrThreads, smem, s>>>(g, at, X, R, T, jOff, r0, slots);
+  if (g.nfac == 1) { PINT_PCRCL(1) } else if (g.nfac == 2) { PINT_PCRCL(2) } else { PINT_PCRCL(3) }
+#undef PINT_PCRCL
+  return cudaGetLastError();
+}
+
 template <int E>
 static cudaError_t launch_pcr_reg(const Geometry &g, const AlphaTables &at, double2 *X, int R, int T, int jOff,
                                   const double2 *r0, const int *slots, int grid, size_t smem, cudaStream_t s) {
@@ -1256,18 +1345,20 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
   const int grid = (st.packed ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
   if (g.dim == 1) {
+#define PINT_FWD1(NODE_, PACK_, HW_)                                                              \
+  e = set_smem((const void *)fwd_kernel<MM, true, NODE_, PACK_, HW_>, smem);                       \
+  if (e == cudaSuccess) fwd_kernel<MM, true, NODE_, PACK_, HW_><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+    const bool wide = g.hw > 1;   // the 5-/7-point stencils (reading R14)
     PINT_DISPATCH_M(g.M, {
       if (st.packed) {
-        e = set_smem((const void *)fwd_kernel<MM, true, true, true>, smem);
-        if (e == cudaSuccess) fwd_kernel<MM, true, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+        if (wide) { PINT_FWD1(true, true, 3) } else { PINT_FWD1(true, true, 1) }
       } else if (st.P == 1) {
-        e = set_smem((const void *)fwd_kernel<MM, true, true>, smem);
-        if (e == cudaSuccess) fwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+        if (wide) { PINT_FWD1(true, false, 3) } else { PINT_FWD1(true, false, 1) }
       } else {
-        e = set_smem((const void *)fwd_kernel<MM, true, false>, smem);
-        if (e == cudaSuccess) fwd_kernel<MM, true, false><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);
+        if (wide) { PINT_FWD1(false, false, 3) } else { PINT_FWD1(false, false, 1) }
       }
     });
+#undef PINT_FWD1
     rec(s);
   } else {
     const bool pk = st.packed != 0;   // Hermitian mode: two real points per complex time series
@@ -1276,7 +1367,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     if (pk && BY > g.ny / 2) BY = g.ny / 2;
     const int hw = g.hw < 1 ? 1 : g.hw;
     auto rbytes = [&](int bx, int by) {
-      return (size_t)(pk ? 2 : 1) * g.M * (bx + 2 * hw) * (by + 2 * hw) * sizeof(double2);
+      return (size_t)g.M * (bx + 2 * hw) * (by + 2 * hw) * (pk ? 2 * sizeof(double) : sizeof(double2));
     };
     while (rbytes(BX, BY) > 200 * 1024) {   // wide halos at large M: smaller blocks
       if (BY > 1) BY >>= 1;
@@ -1318,8 +1409,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
   if (g.dim == 1) {
     if (lc.pcr_mode == 0) {
       const size_t smem = (size_t)g.N * sizeof(double2);
-      if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-      pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, nullptr, st.slots);
+      if ((e = launch_pcr_classes(g, at, b.X, 1, 1, 0, nullptr, st.slots, lines, smem, s)) != cudaSuccess) return e;
       rec(s);
       *out = b.X;
     } else {
@@ -1334,8 +1424,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
         if ((e = launch_pcr_reg<E>(g, at, b.X, R, Tr, jOff, nullptr, st.slots, lines * (R / Tr), smr, s)) != cudaSuccess)
           return e;
       } else {
-        if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-        pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, nullptr, st.slots);
+        if ((e = launch_pcr_classes(g, at, b.X, R, T, jOff, nullptr, st.slots, lines * (R / T), smem, s)) != cudaSuccess) return e;
       }
       rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1537,8 +1626,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   }
   if (lc.pcr_mode == 0) {
     const size_t smem = (size_t)g.N * sizeof(double2);
-    if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-    pcr_classes_kernel<<<lines, kPcrThreads, smem, s>>>(g, at, b.X, 1, 1, 0, r0, st.slots);
+    if ((e = launch_pcr_classes(g, at, b.X, 1, 1, 0, r0, st.slots, lines, smem, s)) != cudaSuccess) return e;
     rec(s);
     *out = b.X;
     return cudaGetLastError();
@@ -1554,8 +1642,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
       return e;
   } else {
     const size_t smem = (size_t)nq * T * sizeof(double2);
-    if ((e = set_smem((const void *)pcr_classes_kernel, smem)) != cudaSuccess) return e;
-    pcr_classes_kernel<<<lines * (R / T), kPcrThreads, smem, s>>>(g, at, b.X, R, T, jOff, r0, st.slots);
+    if ((e = launch_pcr_classes(g, at, b.X, R, T, jOff, r0, st.slots, lines * (R / T), smem, s)) != cudaSuccess) return e;
   }
   rec(s);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1629,7 +1716,23 @@ cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const
   const long long total = (long long)g.L * g.M * g.N;
   long long blocks = (total + 255) / 256;
   if (blocks > num_sms() * 32) blocks = num_sms() * 32;
-  init_iterate_kernel<<<(int)blocks, 256, 0, s>>>(g, st.u0, b.u);
+  init_iterate_kernel<<<(int)blocks, 256, 0, s>>>(g, st.u0, b.u, st.packed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_storage_convert(const Geometry &g, const Buffers &b, bool to_real, cudaStream_t s) {
+  const long long n = (long long)g.L * g.M * g.N;
+  const int blocks = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  double *tmp = (double *)b.X;   // scratch: X holds >= L M N complex values
+  if (to_real) {
+    real_parts_kernel<<<blocks, 256, 0, s>>>(b.u, tmp, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync((void *)b.u, tmp, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  }
+  cudaError_t e = cudaMemcpyAsync(tmp, (const void *)b.u, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return e;
+  complex_from_real_kernel<<<blocks, 256, 0, s>>>(tmp, b.u, n);
   return cudaGetLastError();
 }
 

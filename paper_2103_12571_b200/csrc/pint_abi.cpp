@@ -785,6 +785,16 @@ pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf) {
 pint_status pint_get_iterate(pint_ctx *c, double *u_host) {
   if (!c || !u_host) return fail(PINT_ERR_INVALID, "NULL argument");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (c->hermitian) {   // real storage: the first L M N doubles, expanded to (re, 0)
+    const size_t n = (size_t)c->g.L * c->g.M * c->g.N;
+    CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = n; i-- > 0;) {   // back to front: u_host[2i] never overwrites an unread u_host[j > i]
+      u_host[2 * i] = u_host[i];
+      u_host[2 * i + 1] = 0.0;
+    }
+    return PINT_OK;
+  }
   CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u, c->lay.vec_bytes, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PINT_OK;
@@ -794,6 +804,17 @@ pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
   if (!c || !u_host) return fail(PINT_ERR_INVALID, "NULL argument");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const size_t off = ((size_t)(c->g.L - 1) * c->g.M + (c->g.M - 1)) * c->g.N;
+  if (c->hermitian) {
+    const size_t n = (size_t)c->g.N;
+    CUDA_TRY(c, cudaMemcpyAsync(u_host, (const double *)c->u + off, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = n; i-- > 0;) {
+      u_host[2 * i] = u_host[i];
+      u_host[2 * i + 1] = 0.0;
+    }
+    return PINT_OK;
+  }
   CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u + off, (size_t)c->g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PINT_OK;
@@ -819,23 +840,19 @@ pint_status pint_next_window(pint_ctx *c) {
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (c->P != 1) return fail(PINT_ERR_INVALID, "windowed stepping is single-rank only");
   const Geometry &g = c->g;
-  const double2 *last = c->u + ((size_t)(g.L - 1) * g.M + (g.M - 1)) * g.N;
-  CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToDevice,
-                              c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->u0.data(), last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  if (c->hermitian) {   // real storage: u0 := (u_{L-1, M-1}, 0) through the host copy
+    pint_status st = pint_get_final_value(c, c->u0.data());
+    if (st != PINT_OK) return st;
+    CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, c->u0.data(), (size_t)g.N * sizeof(double2),
+                                cudaMemcpyHostToDevice, c->stream));
+  } else {
+    const double2 *last = c->u + ((size_t)(g.L - 1) * g.M + (g.M - 1)) * g.N;
+    CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->u0.data(), last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+  }
   CUDA_TRY(c, launch_init_iterate(c->g, c->st, buffers(c), c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (c->hermitian) {   // the projection keeps the final value real up to roundoff: make it exact
-    bool changed = false;
-    for (int n = 0; n < g.N; ++n)
-      if (c->u0[2 * n + 1] != 0.0) { c->u0[2 * n + 1] = 0.0; changed = true; }
-    if (changed) {
-      CUDA_TRY(c, cudaMemcpyAsync((void *)c->st.u0, c->u0.data(), (size_t)g.N * sizeof(double2),
-                                  cudaMemcpyHostToDevice, c->stream));
-      CUDA_TRY(c, launch_init_iterate(c->g, c->st, buffers(c), c->stream));
-      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    }
-  }
   c->k = 0;
   return PINT_OK;
 }
@@ -934,6 +951,12 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->st.nsolve = ns;
   c->st.packed = on ? 1 : 0;
+  if ((on != 0) != c->hermitian) {
+    // iterate storage: real fp64 in the Hermitian mode (its imaginary parts are zero in exact
+    // arithmetic; roundoff-level ones are dropped), complex128 otherwise
+    CUDA_TRY(c, launch_storage_convert(g, buffers(c), on != 0, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
   c->hermitian = on != 0;
   return PINT_OK;
 }
@@ -992,6 +1015,7 @@ pint_status pint_sequential(pint_ctx *c) {
   const Geometry &g = c->g;
   if (g.dim != 2 || !reg2d_path(g) || c->P != 1)
     return fail(PINT_ERR_INVALID, "sequential baseline: 2-D grids of the spatial pipeline, one rank");
+  if (c->hermitian) return fail(PINT_ERR_INVALID, "sequential baseline: complex storage only (pint_set_hermitian(0))");
   const int M = g.M;
   // Q = V diag(lambda) V^{-1} (Radau IIA): step l solves (I - dT Q (x) A) U_l = 1 (x) u_{l-1,M-1}
   // as z_m = (V^{-1} 1)_m (I - dT lambda_m A)^{-1} u_{l-1,M-1}, U_l = (V (x) I) z

@@ -225,8 +225,18 @@ class Solver:
         _check(self.lib.pint_sequential(self.ctx))
 
     def set_hermitian(self, on: bool = True):
-        """Real-data fast path: solve only the frequencies k <= L/2 (y_{L-k} = conj(y_k))."""
+        """Real-data fast path: solve only the frequencies k <= L/2 (y_{L-k} = conj(y_k)); while on,
+        the device iterate is stored as real fp64 (see iterate_view)."""
         _check(self.lib.pint_set_hermitian(self.ctx, 1 if on else 0))
+        self.hermitian = bool(on)
+
+    def iterate_view(self):
+        """The device iterate as a torch view: complex128 (L, M, N), or float64 (L, M, N) in the
+        Hermitian mode (real storage in the first L*M*N doubles of the buffer)."""
+        import torch
+        if getattr(self, "hermitian", False):
+            return self.u.view(-1).view(torch.float64)[: self.L * self.M * self.N].view(self.L, self.M, self.N)
+        return self.u
 
     # -- iteration
     def iterate(self, n: int = 1, want_diff: bool = False):

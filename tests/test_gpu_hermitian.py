@@ -78,3 +78,35 @@ def test_hermitian_full_size_config5_sampled_modes():
         errs.append(float(np.linalg.norm((g - uh).ravel()) / np.linalg.norm(uh.ravel())))
     s.close()
     assert max(errs) <= TOL, errs
+
+
+def test_real_storage_roundtrip():
+    """Hermitian mode stores the iterate as real fp64 (first L M N doubles of u_dev): switching on
+    converts, get_iterate expands to (re, 0), switching off restores complex128 storage, and the
+    iteration continues identically in both storages."""
+    import paper_2103_12571_b200 as PB
+    p = W.reduced(5)
+    u0 = np.ascontiguousarray(p.u0().real.astype(np.complex128))
+    a = [1e-3] * 4
+    ref = PB.Solver(p, u0)
+    ref.set_alpha_schedule(a)
+    ref.iterate(2)
+    s = PB.Solver(p, u0)
+    s.set_alpha_schedule(a)
+    s.iterate(1)
+    before = s.get_iterate()
+    s.set_hermitian(True)
+    after = s.get_iterate()
+    assert np.array_equal(after.real, before.real) and np.all(after.imag == 0)
+    v = s.iterate_view()
+    assert v.dtype.is_floating_point and not v.dtype.is_complex and tuple(v.shape) == (p.L, p.M, p.N)
+    np.testing.assert_array_equal(v.cpu().numpy(), before.real)
+    s.iterate(1)
+    assert relative_l2(s.get_iterate(), ref.get_iterate()) < 1e-12
+    s.set_hermitian(False)
+    np.testing.assert_array_equal(s.iterate_view().cpu().numpy(), s.get_iterate())
+    ref.iterate(1)
+    s.iterate(1)
+    assert relative_l2(s.get_iterate(), ref.get_iterate()) < 1e-12
+    s.close()
+    ref.close()

@@ -145,7 +145,7 @@ def _gpu_project(s, p, kx, ky):
     """uhat[l, m, j] = sum_n u[l, m, n] e^{-2 pi i (kx x/nx + ky y/ny)} of the device iterate, via
     torch matmuls on the GPU (test-side measurement only)."""
     import torch
-    dev = s.u.device
+    dev = s.iterate_view().device
     xs = torch.arange(p.nx, device=dev, dtype=torch.int64)
     ys = torch.arange(p.ny, device=dev, dtype=torch.int64)
     kxt = torch.as_tensor(np.asarray(kx), device=dev, dtype=torch.int64)
@@ -154,10 +154,10 @@ def _gpu_project(s, p, kx, ky):
     ey = torch.exp(-2j * np.pi * ((ys[:, None] * kyt[None, :]) % p.ny).to(torch.float64) / p.ny)  # (ny, K)
     L, M = p.L, p.M
     out = torch.empty((L * M, len(kx)), dtype=torch.complex128, device=dev)
-    U = s.u.view(L * M, p.ny, p.nx)
+    U = s.iterate_view().view(L * M, p.ny, p.nx)        # float64 in the Hermitian mode (real storage)
     chunk = max(1, (1 << 27) // (p.N * 4))
     for i in range(0, L * M, chunk):
-        a = torch.matmul(U[i:i + chunk], ex)              # (c, ny, K)
+        a = torch.matmul(U[i:i + chunk].to(torch.complex128), ex)   # (c, ny, K)
         out[i:i + chunk] = (a * ey[None]).sum(1)
     torch.cuda.synchronize()
     return out.view(L, M, len(kx)).cpu().numpy()
