@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 // HW: halo width (1 for the 3-point operators, up to 3 for the kappa-6 / upwind-5 stencils);
 // weights outside [-hx0, hx1] x [-hy0, hy1] are zero in g.wx / g.wy.
 template <int M, bool PACK, int HW>
-__global__ void __launch_bounds__(256) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
+__global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
                                                          const double2 *__restrict__ u,
                                                          double2 *__restrict__ X, int BX, int BY) {
   extern __shared__ double2 sm[];  // [1 + PACK][M][BY+2HW][BX+2HW]
@@ -1289,9 +1289,12 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i) {
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 
-static cudaError_t set_smem(const void *fn, size_t bytes) {
+static cudaError_t set_smem(const void *fn, size_t bytes, bool max_carveout = false) {
   // always opt in: static shared memory (reduction scratch) adds to the dynamic bytes
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess || !max_carveout) return e;
+  // largest shared-memory carveout (residual tiles: 4 CTAs of 42 KB per SM)
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
 }
 
 static cudaError_t launch_pcr_classes(const Geometry &g, const AlphaTables &at, double2 *X, int R, int T, int jOff,
@@ -1376,7 +1379,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     const size_t rs = rbytes(BX, BY);
     const int rgrid = g.L * (g.nx / BX) * ((pk ? g.ny / 2 : g.ny) / BY);
 #define PINT_RES2D(MM_, PK_, HW_)                                                                   \
-  e = set_smem((const void *)residual2d_kernel<MM_, PK_, HW_>, rs);                                  \
+  e = set_smem((const void *)residual2d_kernel<MM_, PK_, HW_>, rs, true);                            \
   if (e == cudaSuccess) residual2d_kernel<MM_, PK_, HW_><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY);
     PINT_DISPATCH_M(g.M, {
       if (pk) {
