@@ -119,6 +119,44 @@ __device__ __forceinline__ void node_transform(double2 *sm, int ls, int M, int r
   }
 }
 
+// Copy-out of the I item with the node matrix applied: for every (row yy, column x) the M lines'
+// values (tile[(yy M + j) NX + F(x)]) -> out_m = sum_j A[m][j] v_j -> xp[m N + (y0 + yy) NX + x].
+// A (M x M, shared memory) is held in registers for M <= 4 (the FFT's registers are free here).
+template <class PX, int MM>
+__device__ __forceinline__ void node_copyout(const double2 *tile, const double2 *A, int YR,
+                                             double2 *__restrict__ xp, int N, int y0) {
+  constexpr int LX = PX::LOGN, NX = 1 << LX;
+  double2 ar[MM <= 4 ? MM * MM : 1];
+  if constexpr (MM <= 4) {
+#pragma unroll
+    for (int i = 0; i < MM * MM; ++i) ar[i] = A[i];
+  }
+  for (int i = threadIdx.x; i < YR * NX; i += blockDim.x) {
+    const int x = i & (NX - 1), yy = i >> LX;
+    const double2 *base = tile + (size_t)yy * MM * NX + rfft::F<PX>(x);
+    double2 v[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) v[j] = base[j * NX];
+    double2 *dst = xp + ((size_t)(y0 + yy) << LX) + x;
+#pragma unroll (MM <= 4 ? MM : 1)
+    for (int m = 0; m < MM; ++m) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < MM; ++j) {
+        double2 a;
+        if constexpr (MM <= 4) {
+          a = ar[m * MM + j];
+        } else {
+          const volatile double2 *av = (const volatile double2 *)(A + m * MM + j);
+          a = make_double2(av->x, av->y);
+        }
+        acc = cfma(a, v[j], acc);
+      }
+      dst[(size_t)m * N] = acc;
+    }
+  }
+}
+
 // ---- R item: rows y0 .. y0 + YR - 1 of slot p, all M nodes ---------------------------------
 template <class PX>
 __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at, double2 *tile, double2 *nt,
@@ -159,6 +197,13 @@ __device__ __forceinline__ void r_item(const Geometry &g, const AlphaTables &at,
           tile[(size_t)l * NX + rfft::F<PX>(x)] = v;
         }
       }
+    }
+  } else if (NX >= kSpThreads) {
+    for (int l = 0; l < nl; ++l) {   // line-major: the (row, node) split once per line
+      const int yy = l / M, m = l - yy * M;
+      const double2 *src = xp + (size_t)m * g.N + ((size_t)(y0 + yy) << LX);
+      double2 *dst = tile + (size_t)l * NX;
+      for (int x = threadIdx.x; x < NX; x += kSpThreads) cp_async16(dst + rfft::F<PX>(x), src + x);
     }
   } else {
     for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
@@ -218,9 +263,18 @@ __device__ __forceinline__ void i_item(const Geometry &g, const AlphaTables &at,
   }
   if (node && threadIdx.x < M * M) nt[threadIdx.x] = __ldg(at.SG + (size_t)p * M * M + threadIdx.x);
   __syncthreads();
-  if (node) {
-    node_transform<PX>(tile, NX, M, YR, nt);
-    __syncthreads();
+  if (node) {   // y = G_p^{-1} S_p x2 applied on the way out (one smem pass and barrier fewer)
+    switch (M) {
+      case 1: node_copyout<PX, 1>(tile, nt, YR, xp, g.N, y0); break;
+      case 2: node_copyout<PX, 2>(tile, nt, YR, xp, g.N, y0); break;
+      case 3: node_copyout<PX, 3>(tile, nt, YR, xp, g.N, y0); break;
+      case 4: node_copyout<PX, 4>(tile, nt, YR, xp, g.N, y0); break;
+      case 5: node_copyout<PX, 5>(tile, nt, YR, xp, g.N, y0); break;
+      case 6: node_copyout<PX, 6>(tile, nt, YR, xp, g.N, y0); break;
+      case 7: node_copyout<PX, 7>(tile, nt, YR, xp, g.N, y0); break;
+      default: node_copyout<PX, 8>(tile, nt, YR, xp, g.N, y0); break;
+    }
+    return;
   }
   for (int i = threadIdx.x; i < nl * NX; i += blockDim.x) {
     const int x = i & (NX - 1), li = i >> LX;
@@ -313,7 +367,7 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
   // before it by CTAs that are running (cooperative launch), so the waits cannot deadlock.  The
   // next claim is issued at the start of an item and consumed at its end (latency hidden).
   unsigned *claim = sync + 3 * sp.nbatch;
-  __shared__ unsigned s_next;
+  __shared__ unsigned s_next[2];   // double-buffered: consecutive items use alternate slots
   auto round_count = [&](int j) {
     const int slo = j - (sp.nbatch - 1) > 0 ? j - (sp.nbatch - 1) : 0;
     const int shi = j < sp.nstage - 1 ? j : sp.nstage - 1;
@@ -321,9 +375,10 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
     for (int si = slo; si <= shi; ++si) rn += (first + si == kStC) ? sp.nC : sp.nRI;
     return rn;
   };
-  if (threadIdx.x == 0) s_next = sp.claim ? atomicAdd(claim, 1u) : blockIdx.x;
+  if (threadIdx.x == 0) s_next[0] = sp.claim ? atomicAdd(claim, 1u) : blockIdx.x;
   __syncthreads();
-  unsigned t = s_next;
+  unsigned t = s_next[0];
+  int par = 1;
   int j = 0;
   long long rs = 0;            // sequence number of round j's first item
   int rn = round_count(0);
@@ -376,10 +431,12 @@ __global__ void __launch_bounds__(kSpThreads, MB == 4 ? 2 : 1)
           i_item<PX>(g, at, tile, nt, twx, xp, slot, y0, sp.YR, node);
         }
       }
-      if (threadIdx.x == 0) s_next = nxt;
-      publish(sync + stage * sp.nbatch + b);   // its barrier also publishes s_next to the CTA
-      t = s_next;
-      __syncthreads();   // every thread has read s_next before thread 0 may overwrite it
+      // slot par was last read before the previous item's publish barrier, which thread 0 has
+      // passed: no thread can still be reading it
+      if (threadIdx.x == 0) s_next[par] = nxt;
+      publish(sync + stage * sp.nbatch + b);   // its barrier also publishes s_next[par] to the CTA
+      t = s_next[par];
+      par ^= 1;
     }
   }
 }
