@@ -87,6 +87,11 @@ __device__ __forceinline__ double2 inv_symbol(const StaticTables &st, double2 s,
 template <class PX, int MM>
 __device__ __forceinline__ void node_transform_m(double2 *sm, int ls, int rows, const double2 *A) {
   constexpr int LX = PX::LOGN, NX = 1 << LX;
+  double2 ar[MM <= 4 ? MM * MM : 1];   // M <= 4: A in registers (nothing else is live here)
+  if constexpr (MM <= 4) {
+#pragma unroll
+    for (int i = 0; i < MM * MM; ++i) ar[i] = A[i];
+  }
   for (int i = threadIdx.x; i < rows * NX; i += blockDim.x) {
     const int x = i & (NX - 1), r = i >> LX;
     double2 *base = sm + (size_t)r * MM * ls + rfft::F<PX>(x);
@@ -98,8 +103,14 @@ __device__ __forceinline__ void node_transform_m(double2 *sm, int ls, int rows, 
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int j = 0; j < MM; ++j) {
-        const volatile double2 *a = (const volatile double2 *)(A + m * MM + j);
-        acc = cfma(make_double2(a->x, a->y), v[j], acc);
+        double2 a;
+        if constexpr (MM <= 4) {
+          a = ar[m * MM + j];
+        } else {
+          const volatile double2 *av = (const volatile double2 *)(A + m * MM + j);
+          a = make_double2(av->x, av->y);
+        }
+        acc = cfma(a, v[j], acc);
       }
       base[m * ls] = acc;
     }
