@@ -80,7 +80,8 @@ __host__ __device__ inline double2 *unit_planes(const Geometry &g, double2 *X) {
 // ---- launch wrappers (kernels.cu) -----------------------------------------------------------
 // All return cudaGetLastError() after enqueueing on `st`.
 struct LaunchCfg {
-  int fwd_T;                  // spatial points per forward/backward tile (all l x all m, 1-D)
+  int fwd_T;                  // spatial points per forward tile (all l x all m, 1-D; <= 64 KB, 3 CTAs/SM)
+  int bwd_T;                  // spatial points per backward tile (<= 100 KB: 128-byte rows at 2 CTAs/SM)
   int tfft_T;                 // spatial points per 2-D time-FFT tile (all l x one m)
   int pcr_mode;               // 0: single-pass line PCR; 1: two-pass (classes + chunks)
   int pcr_R;                  // residue-class modulus of the two-pass scheme

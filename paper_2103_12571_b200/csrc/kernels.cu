@@ -1241,6 +1241,13 @@ LaunchCfg choose_launch(const Geometry &g) {
   if (const char *e = getenv("PINT_FWD_T")) T = atoi(e);   // tuning experiments only
   while (T > g.N) T >>= 1;
   lc.fwd_T = T;
+  // backward tile: measured on config 3 (L = 256, M = 3): T = 8 (96 KB) 0.63 ms vs T = 4 0.75 ms
+  // (the forward tile, which also evaluates the stencil, prefers T = 4 at 3 CTAs per SM)
+  int TB = 16;
+  while (TB > 1 && fwd_smem_bytes(g, TB) > 100 * 1024) TB >>= 1;
+  if (const char *e = getenv("PINT_BWD_T")) TB = atoi(e);   // tuning experiments only
+  while (TB > g.N) TB >>= 1;
+  lc.bwd_T = TB;
   int T2 = 32;
   while (T2 > 1 && (size_t)g.L * T2 * sizeof(double2) > 64 * 1024) T2 >>= 1;
   while (T2 > g.N) T2 >>= 1;
@@ -1487,7 +1494,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
 cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                             const AlphaTables &at, const Buffers &b, const double2 *x2,
                             double *diff_slot, cudaStream_t s, int overwrite) {
-  int T = lc.fwd_T;
+  int T = lc.bwd_T;
   if (st.packed) while (T > g.N / 2) T >>= 1;
   const size_t smem = fwd_smem_bytes(g, T);
   const int grid = (st.packed && g.dim == 1 ? g.N / 2 : g.N) / T;
