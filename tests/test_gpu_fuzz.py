@@ -1,0 +1,69 @@
+"""Randomised GPU parity sweep (seeded): small problems drawn over every operator, dimension,
+grid shape, step count, node count, iteration form and the real-data mode, two iterations each
+against the oracle.  Complements the hand-picked cases with shapes nobody chose (ragged tiles,
+L = 1 / 2, M up to 6, 2-D shapes served by both spatial engines)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle.paralpha import Oracle, relative_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+OPS = ["heat", "advection", "heat4", "heat6", "upwind1", "upwind3", "upwind5"]
+
+
+def _cases(n=96, seed=2103):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        dim = int(rng.integers(1, 3))
+        op = OPS[int(rng.integers(len(OPS)))]
+        nx = int(2 ** rng.integers(3, 7 if dim == 2 else 9))
+        ny = int(2 ** rng.integers(2, 7)) if dim == 2 else 1
+        L = int(2 ** rng.integers(0, 6))
+        M = int(rng.integers(1, 7))
+        heat = op.startswith("heat")
+        nu = float(rng.uniform(0.05, 1.0)) if heat else 0.0
+        cx = 0.0 if heat else float(rng.uniform(-1.0, 1.0))
+        cy = 0.0 if heat or dim == 1 else float(rng.uniform(-1.0, 1.0))
+        T = float(10 ** rng.uniform(-3, -1))
+        alpha = float(10 ** rng.uniform(-4, -2))
+        form = "direct" if rng.random() < 0.3 else "correction"
+        herm = bool(rng.random() < 0.3)
+        p = W.Problem(f"fz{i}_{dim}d_{op}_{nx}x{ny}_L{L}_M{M}_{form}{'_h' if herm else ''}", dim, nx, ny, op,
+                      nu, cx, cy, T, L, M, "random", "fixed", alpha, 2)
+        out.append((p, form, herm))
+    return out
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0].name)
+def test_fuzz_parity(case):
+    import paper_2103_12571_b200 as PB
+    p, form, herm = case
+    u0 = p.u0()
+    if herm:
+        u0 = np.ascontiguousarray(u0.real.astype(np.complex128))
+    s = PB.Solver(p, u0)
+    if herm:
+        try:
+            s.set_hermitian(True)
+        except PB.PintError:
+            s.close()
+            pytest.skip("real-data mode not available for this shape (documented requirement)")
+    if form == "direct":
+        s.set_form("direct")
+    a = [p.alpha_fixed] * 2
+    try:
+        s.set_alpha_schedule(a)
+    except PB.PintError as e:
+        s.close()
+        pytest.skip(f"alpha tables rejected by the documented guard: {e}")
+    o = Oracle(p, u0, "dense" if p.M * p.N <= 1024 else "fourier")
+    u = o.initial()
+    for k in range(2):
+        u = o.iterate(u, a[k]) if form == "correction" else o.iterate_direct(u, a[k])
+        s.iterate(1)
+        e = relative_l2(s.get_iterate(), u)
+        assert e <= TOL, (k, e)
+    s.close()
