@@ -67,3 +67,42 @@ def test_fuzz_parity(case):
         e = relative_l2(s.get_iterate(), u)
         assert e <= TOL, (k, e)
     s.close()
+
+
+def _sharded_cases(n=24, seed=12571):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        P = int(rng.choice([2, 4]))
+        L = int(2 ** rng.integers(2, 6))
+        M = int(rng.integers(1, 5))
+        if (L // P) % P or L < P * P or M * P > 32:
+            continue
+        dim = int(rng.integers(1, 3))
+        op = OPS[int(rng.integers(len(OPS)))]
+        heat = op.startswith("heat")
+        nx = int(2 ** rng.integers(3, 6 if dim == 2 else 8))
+        ny = int(2 ** rng.integers(3, 6)) if dim == 2 else 1
+        p = W.Problem(f"fzs{len(out)}_P{P}_{dim}d_{op}_{nx}x{ny}_L{L}_M{M}", dim, nx, ny, op,
+                      0.5 if heat else 0.0, 0.0 if heat else 0.7, 0.0 if heat or dim == 1 else -0.4,
+                      float(10 ** rng.uniform(-3, -1)), L, M, "random", "fixed", 1e-3, 2)
+        out.append((p, P))
+    return out
+
+
+@pytest.mark.parametrize("case", _sharded_cases(), ids=lambda c: c[0].name)
+def test_fuzz_sharded_parity(case):
+    """Time-sharded path (P virtual ranks on one GPU) on random shapes."""
+    import paper_2103_12571_b200 as PB
+    p, P = case
+    u0 = p.u0()
+    grp = PB.Group(p, u0, P)
+    grp.set_alpha_schedule([p.alpha_fixed] * 2)
+    o = Oracle(p, u0, "dense" if p.M * p.N <= 1024 else "fourier")
+    u = o.initial()
+    for k in range(2):
+        u = o.iterate(u, p.alpha_fixed)
+        grp.iterate(1)
+        e = relative_l2(grp.get_iterate(), u)
+        assert e <= TOL, (k, e)
+    grp.close()
