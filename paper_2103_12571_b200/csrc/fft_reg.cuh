@@ -238,9 +238,12 @@ __device__ __forceinline__ void lane_dit(double2 (&v)[P::E], int tau) {
 template <class P>
 __device__ __forceinline__ void forward_regs(double2 (&v)[P::E], double2 *line, int l, int tau,
                                              const double2 *tw) {
+  // Exchanges need one barrier each: every thread writes pass i's values back to exactly the
+  // positions pos<i>(tau, .) it read them from (from_smem<P, i>), so a write can never clobber a
+  // position another thread of the line has still to read (the position sets of the threads are
+  // disjoint); only the read of pass i + 1 must wait for all writes (RAW).
   dif<P, 0>(v, tau, tw);
   if constexpr (P::NP >= 2) {
-    line_sync<P>(l);
     to_smem<P, 0>(v, line, tau);
     line_sync<P>(l);
     from_smem<P, 1>(v, line, tau);
@@ -249,14 +252,15 @@ __device__ __forceinline__ void forward_regs(double2 (&v)[P::E], double2 *line, 
   if constexpr (P::NP >= 3 && P::SHL) {
     lane_dif<P>(v, tau);
   } else if constexpr (P::NP >= 3) {
-    line_sync<P>(l);
     to_smem<P, 1>(v, line, tau);
     line_sync<P>(l);
     from_smem<P, 2>(v, line, tau);
     dif<P, 2>(v, tau, tw);
   }
 }
-// forward_regs starting from pass-0 values that sit (natural order, swizzled) in `line`
+// forward_regs starting from pass-0 values that sit (natural order, swizzled) in `line`; the
+// values must have been read from pos<0> positions of this thread (from_smem<P, 0> below), which
+// is what makes the write-back of pass 0 barrier-free
 template <class P>
 __device__ __forceinline__ void forward_from_smem(double2 (&v)[P::E], double2 *line, int l, int tau,
                                                   const double2 *tw) {
@@ -266,7 +270,10 @@ __device__ __forceinline__ void forward_from_smem(double2 (&v)[P::E], double2 *l
 
 // Inverse transform starting from the last pass's positions in registers; ends with the values
 // of pass 0 (natural positions tau + TPL t) in registers.  Uses `line` for the exchanges: the
-// caller must make sure nobody still reads it (barrier) before calling.
+// caller must make sure nobody still reads it, or that every thread's values came from its own
+// last-pass positions of `line` (the forward transform), so that the first write-back clobbers
+// nothing another thread still reads.  The last read (pass 0) is not followed by a barrier: a
+// caller that writes `line` afterwards must write pos<P, 0> positions (to_smem<P, 0>) or sync.
 template <class P>
 __device__ __forceinline__ void inverse_in_regs(double2 (&v)[P::E], double2 *line, int l, int tau,
                                                 const double2 *tw) {
@@ -277,14 +284,12 @@ __device__ __forceinline__ void inverse_in_regs(double2 (&v)[P::E], double2 *lin
     to_smem<P, 2>(v, line, tau);
     line_sync<P>(l);
     from_smem<P, 1>(v, line, tau);
-    line_sync<P>(l);
   }
   if constexpr (P::NP >= 2) {
     dit<P, 1>(v, tau, tw);
-    to_smem<P, 1>(v, line, tau);
+    to_smem<P, 1>(v, line, tau);   // pos<1> positions: the ones this thread just read
     line_sync<P>(l);
     from_smem<P, 0>(v, line, tau);
-    line_sync<P>(l);
   }
   dit<P, 0>(v, tau, tw);
 }

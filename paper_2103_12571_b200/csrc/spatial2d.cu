@@ -341,7 +341,6 @@ __device__ __forceinline__ void c_item(const Geometry &g, const StaticTables &st
           const int P = rfft::last_pos<PY>(tau, u, t);
           v[u * R + t] = cmul(v[u * R + t], inv_symbol(st, s, inv_n, kx, brev(P, LY)));
         }
-      rfft::line_sync<PY>(lc);   // every thread of the line has read its last-pass values
     }
   }
   if (wrun) {
