@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   const size_t plane = (size_t)M * g.N;
   const int rows = L * M;
   const int all = rows * T;
+  for (int i = threadIdx.x; i < g.L; i += blockDim.x) sm[all + i] = __ldg(st.twL + i);   // time twiddles
   if (RESID) {
     // (i) residual + alpha^{l/L} scale, one (l, t) per work item
     const int items = L * T;
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   }
   __syncthreads();
   // (ii) L-point DIF FFT along l for the M*T columns
-  fft_dif<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  fft_dif<3, false>(sm, M * T, 1, M * T, L, g.logL, sm + all);   // twiddles staged behind the tile
   if (PACK) {
     // (iii) unpack X_k (k <= L/2) from the slots of k and L - k, then S_k^{-1}; one (unit, m) per item
     for (int it = threadIdx.x; it < st.nsolve * M; it += blockDim.x) {
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     __syncthreads();
   }
   // (v-b) inverse DIT FFT from bit-reversed p to natural l
-  fft_dit_inv<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);
+  fft_dit_inv<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);   // (staging measured slower here)
   // (v-c) u += alpha^{-l/L}/L c, loads batched for memory-level parallelism
   double dmax = 0.0;
   constexpr int kB = 4;
@@ -352,13 +353,14 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   const size_t lstride = (size_t)g.M * g.N;
   double2 *base = X + (size_t)m * g.N + n0;
   const int all = g.L * T;
+  for (int i = threadIdx.x; i < g.L; i += blockDim.x) sm[all + i] = __ldg(st.twL + i);   // time twiddles
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
     const int t = idx & (T - 1), l = idx >> lT;
     cp_async16(sm + sidx<false>(idx), base + (size_t)l * lstride + t);
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_dif<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
+  fft_dif<3, false>(sm, T, 1, T, g.L, g.logL, sm + all);   // twiddles staged behind the tile
   for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
     const int t = idx & (T - 1), p = idx >> lT;
     double2 v = sm[sidx<false>(idx)];
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       sm[sidx<false>(idx)] = cmulc(sm[sidx<false>(idx)], __ldg(st.twr + (idx >> lT)));
     __syncthreads();
   }
-  fft_dit_inv<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
+  fft_dit_inv<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);   // (staging measured slower here)
   double dmax = 0.0;
   constexpr int kB = 4;
   for (int b0 = threadIdx.x; b0 < all; b0 += kB * blockDim.x) {
@@ -1351,7 +1353,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
                            const AlphaTables &at, const Buffers &b, cudaStream_t s) {
   int T = lc.fwd_T;
   if (st.packed) while (T > g.N / 2) T >>= 1;
-  const size_t smem = fwd_smem_bytes(g, T);
+  const size_t smem = fwd_smem_bytes(g, T) + (size_t)g.L * sizeof(double2);   // + staged twiddles
   const int grid = (st.packed ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
   if (g.dim == 1) {
@@ -1403,7 +1405,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     if (pk) gt.N = g.N / 2;
     int T2 = lc.tfft_T;
     while (T2 > gt.N) T2 >>= 1;
-    const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
+    const size_t sm2 = (size_t)g.L * (T2 + 1) * sizeof(double2);   // tile + staged twiddles
     e = set_smem((const void *)tfft_fwd_kernel, sm2);
     if (e == cudaSuccess) tfft_fwd_kernel<<<g.M * (gt.N / T2), kTileThreads, sm2, s>>>(gt, st, b.X, T2);
     rec(s);
