@@ -622,6 +622,22 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
 // applies the large strides (closed on residue classes mod R) first, then the small strides on
 // contiguous chunks with halos.
 
+// One PCR level update y - p y_{i-h} - q y_{i+h}.  The level coefficients of the heat family are
+// symmetric (q = p at every level: a' = -a^2/b, c' = -c^2/b keep a = c) and those of centred
+// advection antisymmetric at level 0 (q = -p) and symmetric after; sym = +1 / -1 then needs one
+// complex product instead of two (used by the chunk pass; the register class pass measured
+// slower with the extra branch).
+__device__ __forceinline__ int pcr_sym(double2 p, double2 q) {
+  if (p.x == q.x && p.y == q.y) return 1;
+  if (p.x == -q.x && p.y == -q.y) return -1;
+  return 0;
+}
+__device__ __forceinline__ double2 pcr_update(int sym, double2 p, double2 q, double2 lv, double2 rv, double2 y) {
+  if (sym > 0) return cfms(p, cadd(lv, rv), y);
+  if (sym < 0) return cfms(p, csub(lv, rv), y);
+  return cfms(q, rv, cfms(p, lv, y));
+}
+
 constexpr int kPcrThreads = 256;
 constexpr int kPcrIPT = 16;   // items per thread held in registers per level
 
@@ -827,12 +843,13 @@ __global__ void __launch_bounds__(kChunkThreads) pcr_chunk_kernel(const Geometry
     const int h = 1 << (jf / F);
     lo += h;  // valid region after this (level, factor): [lo, S - lo)
     const double2 pj = __ldg(coef + 2 * jf), qj = __ldg(coef + 2 * jf + 1);
+    const int sym = pcr_sym(pj, qj);
     const int cnt = S - 2 * lo;
     double2 nv[kChunkIPT];
 #pragma unroll
     for (int k = 0; k < kChunkIPT; ++k) {
       const int i = lo + threadIdx.x + k * kChunkThreads;
-      if (i < lo + cnt) nv[k] = csub(csub(sm[i], cmul(pj, sm[i - h])), cmul(qj, sm[i + h]));
+      if (i < lo + cnt) nv[k] = pcr_update(sym, pj, qj, sm[i - h], sm[i + h], sm[i]);
     }
     __syncthreads();
 #pragma unroll
