@@ -5,7 +5,8 @@
  *
  * Citations: "P:n" = PAPER.md line n (LaTeX source of arXiv 2103.12571).
  *
- * Problem statement: u_t = A u + b on [0, T], u(0) = u0, b == 0,
+ * Problem statement: u_t = A u + b on [0, T], u(0) = u0, b == 0 (b != 0:
+ * pint_set_forcing),
  * L equal steps dT = T/L, M right-included Gauss-Radau (Radau IIA) nodes.
  * The all-at-once system is C u = w with (block matrix P:115-135)
  *     C = I_L (x) (I_MN - dT Q (x) A) + E (x) (H_M (x) I_N),  E = -1 on the sub-diagonal,
@@ -30,7 +31,8 @@
  * one factor; wider stencils are factored on the host per (alpha, k, m); pint_set_alpha_schedule
  * fails with PINT_ERR_NUMERIC if a factor cannot be formed).  2-D solves are diagonal in Fourier.
  *
- * Data layout: complex128, interleaved (re, im) doubles, u[l][m][n], n fastest.
+ * Data layout: complex128, interleaved (re, im) doubles, u[l][m][n], n fastest (the real-data
+ * mode of pint_set_hermitian stores u as real fp64 u[l][m][n] in the same buffer instead).
  *
  * Ownership: the caller owns all device memory (u_dev, work_dev); the context keeps
  * non-owning pointers and carves its small tables out of work_dev.  Host inputs are copied
