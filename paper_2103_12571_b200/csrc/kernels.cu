@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   }
   fft_dit_inv<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);   // (staging measured slower here)
   double dmax = 0.0;
-  constexpr int kB = 4;
+  constexpr int kB = 8;
   for (int b0 = threadIdx.x; b0 < all; b0 += kB * blockDim.x) {
     double2 uo[kB], uo2[kB];
     double sc[kB];
