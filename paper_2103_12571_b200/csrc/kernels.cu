@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   fft_dit_inv<3, false>(sm, M * T, 1, M * T, L, g.logL, st.twL);   // (staging measured slower here)
   // (v-c) u += alpha^{-l/L}/L c, loads batched for memory-level parallelism
   double dmax = 0.0;
-  constexpr int kB = 4;
+  constexpr int kB = 8;
   for (int base = threadIdx.x; base < all; base += kB * blockDim.x) {
     double2 uo[kB], uo2[kB];
     double sc[kB];
