@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
     cp_async_wait_all();
     __syncthreads();
     for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
-      const int ty = pt / BX, tx = pt - ty * BX;
+      const int ty = pt >> (31 - __clz(BX)), tx = pt & (BX - 1);   // BX: power of two
       const int n = ((y0 + ty) << g.lognx) + x0 + tx;
       double res[2][M];
 #pragma unroll
