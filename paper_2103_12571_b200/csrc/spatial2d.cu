@@ -3,19 +3,20 @@
 //
 // Spatial solves: for every line q = (slot p, node m) x2 = F^{-1}[F x1 / (1 - s_q lambda)] as
 // three plane passes over the frequency batch of slot p (all M nodes):
-//   R  rows:    x1 = S_p^{-1} x (node transform), x-DIF; spectral rows stored in the
-//               S-layout of fft_reg.cuh (coalesced)
+//   R  rows:    x1 = S_p^{-1} x (node transform in shared memory), x-DIF; spectral rows
+//               stored in the S-layout of fft_reg.cuh (coalesced)
 //   C  columns: y-DIF, x2 = x1 / ((1 - s_q (lambda_x + lambda_y)) nx ny), y-DIT, in registers
-//   I  rows:    x-DIT, y = G_p^{-1} S_p x2
+//   I  rows:    x-DIT, y = G_p^{-1} S_p x2 applied while copying the rows out
 // run as ONE persistent kernel that software-pipelines the batches (round j: R(j), C(j-1),
 // I(j-2)) so intermediate planes are re-read while they are still in L2.
 //
 // Work distribution: the global item sequence (round by round, stage segments in the order
-// R, C, I) is dealt round-robin to the co-resident CTAs of a cooperative launch.  An item of
-// C(b) waits until all items of R(b) have been counted done (I(b): all of C(b)); every
-// dependency points to an item that comes earlier in the sequence and each CTA walks its items
-// in sequence order, so the earliest unfinished item can always run (no deadlock while all CTAs
-// are resident, which the cooperative launch guarantees).  Producers publish with bar.sync +
+// R, C, I) is claimed item by item from one device counter by the co-resident CTAs of a
+// cooperative launch (the next claim is issued when an item starts and read when it ends).  An
+// item of C(b) waits until all items of R(b) have been counted done (I(b): all of C(b)); every
+// dependency points to an item that comes earlier in the sequence, already claimed by a running
+// CTA, so the earliest unfinished item can always run (no deadlock while all CTAs are resident,
+// which the cooperative launch guarantees).  Producers publish with bar.sync +
 // red.release.gpu; consumers acquire with ld.acquire.gpu and then load with cp.async.cg /
 // ld.global.cg (L2; never a stale L1 line).
 //
