@@ -10,9 +10,10 @@
 //   bwd_kernel        (v): G_k^{-1} S_k, inverse DIT FFT along time from
 //                     bit-reversed order, alpha^{-l/L}/L, u += c    X -> u
 //
-// Design notes: everything is HBM-bandwidth bound (AI < 4 flop/B, fp64), so the
+// Design notes: the arithmetic intensity is low (< 4 flop/B, fp64), so the
 // kernels are organised around full-tile shared-memory staging with 16-byte coalesced global
-// accesses; no tensor cores (no dense contraction on this path).
+// accesses and are measured against the HBM roof; the FFT-heavy ones end up latency bound on
+// shared memory and fp64 dependencies (§5b).  No tensor cores: no dense contraction on this path.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
