@@ -67,7 +67,7 @@ typedef enum {
   PINT_ERR_INVALID = 1,             /* bad argument / unsupported size; nothing was changed   */
   PINT_ERR_SCHEDULE = 2,            /* alpha outside (0,1), schedule exhausted, m_k < 4 gamma */
   PINT_ERR_NOT_DIAGONALIZABLE = 3,  /* cond(S_k) > 1e8 or eigenvalue gap < 1e-8 rho(B_k)     */
-  PINT_ERR_NUMERIC = 4,             /* non-finite residual norm                                */
+  PINT_ERR_NUMERIC = 4,             /* non-finite u0, residual norm or last-step difference     */
   PINT_ERR_CUDA = 5,                /* CUDA runtime error (context poisoned)                   */
   PINT_ERR_NCCL = 6,                /* communication error (context poisoned)                  */
   PINT_ERR_STATE = 7                /* context poisoned by an earlier CUDA/NCCL error          */
@@ -119,8 +119,11 @@ size_t pint_workspace_bytes(const pint_problem *p, const pint_dist *d);
  * over all (l, m).  work_dev/work_bytes: caller-owned
  * device scratch (256-byte aligned, >= pint_workspace_bytes).  u0_host: 2N doubles (re, im),
  * copied.  forcing_host must be NULL (b == 0 at creation; a forcing is attached with
- * pint_set_forcing).
- * Errors: PINT_ERR_INVALID (sizes, alignment, NULL), PINT_ERR_CUDA. */
+ * pint_set_forcing).  This call and every later one that enqueues work first make dist->device
+ * the calling thread's current CUDA device (cudaSetDevice), so one thread may drive contexts on
+ * several devices.
+ * Errors: PINT_ERR_INVALID (sizes, alignment, NULL), PINT_ERR_NUMERIC (u0 not finite),
+ * PINT_ERR_CUDA / PINT_ERR_NCCL (nothing is leaked: the context and its communicator are freed). */
 pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, void *work_dev,
                         size_t work_bytes, const double *u0_host, const double *forcing_host,
                         pint_ctx **out);
@@ -131,13 +134,20 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
 pint_status pint_adaptive_schedule(int32_t L, double w_inf, double m0, double eps, double tau,
                                    int32_t K, double *alpha_out, double *m_out);
 
-/* ||w||_inf = ||u0||_inf of the context's initial value (b == 0), for pint_adaptive_schedule. */
+/* ||w||_inf of the assembled w (Alg. 2's gamma), for pint_adaptive_schedule: ||u0||_inf
+ * when b == 0 (host copy, no device work); with a forcing attached (pint_set_forcing)
+ * max(||u0 + v_0||_inf, max_l ||v_l||_inf) reduced on the device (and over ranks with NCCL;
+ * synchronises the stream).  Errors: PINT_ERR_INVALID, PINT_ERR_NUMERIC (non-finite),
+ * PINT_ERR_STATE (loopback ranks with a forcing), PINT_ERR_CUDA / PINT_ERR_NCCL. */
 pint_status pint_w_inf(pint_ctx *c, double *w_inf);
 
 /* Copies K alphas (each in (0,1)), builds their per-alpha factor tables on the host in long
  * double (d_k, r_k, S_k, S_k^{-1}, G_k^{-1} S_k, d_km, PCR level coefficients) and uploads them;
- * resets the iteration counter to 0.  Errors: PINT_ERR_SCHEDULE, PINT_ERR_NOT_DIAGONALIZABLE,
- * PINT_ERR_INVALID (K > PINT_MAX_SCHEDULE), PINT_ERR_CUDA. */
+ * resets the iteration counter to 0.  Every entry is built and validated before anything is
+ * uploaded: on PINT_ERR_SCHEDULE / _NOT_DIAGONALIZABLE / _NUMERIC / _INVALID the context keeps
+ * its previous schedule untouched.  Errors: PINT_ERR_SCHEDULE, PINT_ERR_NOT_DIAGONALIZABLE,
+ * PINT_ERR_NUMERIC (1-D factorisation), PINT_ERR_INVALID (K > PINT_MAX_SCHEDULE), PINT_ERR_CUDA
+ * (then the context holds no schedule). */
 pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K);
 
 /* Iteration form.  PINT_FORM_CORRECTION (default; north star, reading R1):
@@ -173,8 +183,8 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
  * steps l = rank + P j of this rank), 16-byte aligned, read by every iteration's residual (never
  * written; the caller keeps it alive); NULL removes the forcing.  The residual norms include it.
  * Not combinable with the direct form, the Hermitian mode or pint_sequential (the direct form's
- * single non-zero block and the packed real data assume b == 0).  The Algorithm 2 driver keeps
- * gamma = L (3 eps + tau) ||u0||_inf.  Errors: PINT_ERR_INVALID. */
+ * single non-zero block and the packed real data assume b == 0).  The Algorithm 2 driver takes
+ * gamma = L (3 eps + tau) ||w||_inf of this w (pint_w_inf).  Errors: PINT_ERR_INVALID. */
 pint_status pint_set_forcing(pint_ctx *c, const void *v_dev);
 
 /* Algorithm 2 of the paper, the stopping driver: gamma = L (3 eps + tau) ||w||_inf;
@@ -201,7 +211,9 @@ pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double to
 
 /* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:
  * nullable; if given, n_iter doubles receive ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf (Alg. 2 line 7,
- * P:421) and the call synchronises the stream.  PINT_ERR_SCHEDULE if the schedule would run out. */
+ * P:421) and the call synchronises the stream; a non-finite difference (diverged or NaN iterate:
+ * the device max propagates NaN) returns PINT_ERR_NUMERIC after filling the array.
+ * PINT_ERR_SCHEDULE if the schedule would run out. */
 pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf);
 
 /* ||w - C u||_2 and ||w - C u||_inf of the current (global) iterate (synchronises; with NCCL ranks

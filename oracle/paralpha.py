@@ -57,6 +57,12 @@ def d_values(L: int, alpha: float) -> np.ndarray:
     return -(alpha ** (1.0 / L)) * (np.cos(ang) - 1j * np.sin(ang))
 
 
+def time_apply(T: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """(T (x) I) v for an L x L matrix T acting on the leading (time) axis of v[l][...]: one complex
+    GEMM (L x L) . (L x M*N) — the naive DFT of SURVEY §8(c) O2/O4 (no FFT)."""
+    return (T @ v.reshape(v.shape[0], -1)).reshape((T.shape[0],) + v.shape[1:])
+
+
 def E_matrix(L: int, alpha: float | None = None) -> np.ndarray:
     """E (alpha None): -1 on the sub-diagonal; E_alpha: plus -alpha in the corner."""
     E = np.zeros((L, L))
@@ -87,7 +93,7 @@ def forcing_vector(p, tab: Tableau, b) -> np.ndarray:
 def apply_C(p, tab: Tableau, u: np.ndarray) -> np.ndarray:
     """C u = (I_L (x) C_coll + E (x) H) u, block by block."""
     Au = apply_A(p, u)                                       # (L, M, N)
-    QAu = np.einsum("mj,ljn->lmn", tab.Q, Au)
+    QAu = np.matmul(tab.Q, Au)                               # Q (x) I over the node axis
     Cu = u - p.dT * QAu
     Hu_prev = np.zeros_like(u)
     Hu_prev[1:, :, :] = u[:-1, p.M - 1, :][:, None, :]       # H u_{l-1}: last node to every node
@@ -170,9 +176,9 @@ class Oracle:
     def iterate(self, u: np.ndarray, alpha: float) -> np.ndarray:
         p = self.p
         r = residual(p, self.tab, u, self.u0, self.v)                       # (i)
-        x = np.einsum("kl,lmn->kmn", V_inverse(p.L, alpha), r)              # (ii)  eq. s1
+        x = time_apply(V_inverse(p.L, alpha), r)              # (ii)  eq. s1
         y = self.solver.solve(alpha, x)                                     # (iii)-(iv) eq. s2
-        c = np.einsum("lk,kmn->lmn", V_matrix(p.L, alpha), y)               # (v)   eq. s3
+        c = time_apply(V_matrix(p.L, alpha), y)               # (v)   eq. s3
         return u + c
 
     def iterate_direct(self, u: np.ndarray, alpha: float) -> np.ndarray:
@@ -181,9 +187,9 @@ class Oracle:
         p = self.p
         r = w_vector(p, self.u0, self.v)
         r[0, :, :] -= alpha * u[p.L - 1, p.M - 1, :][None, :]
-        x = np.einsum("kl,lmn->kmn", V_inverse(p.L, alpha), r)
+        x = time_apply(V_inverse(p.L, alpha), r)
         y = self.solver.solve(alpha, x)
-        return np.einsum("lk,kmn->lmn", V_matrix(p.L, alpha), y)
+        return time_apply(V_matrix(p.L, alpha), y)
 
     def residual_norms(self, u: np.ndarray):
         r = residual(self.p, self.tab, u, self.u0, self.v)
@@ -226,7 +232,7 @@ class ModeOracle:
         p, tab = self.p, self.tab
         w = np.zeros_like(uh)
         w[0] = self.u0hat[None, :]
-        Cu = uh - p.dT * self.lam[None, None, :] * np.einsum("mj,ljk->lmk", tab.Q, uh)
+        Cu = uh - p.dT * self.lam[None, None, :] * np.matmul(tab.Q, uh)
         Cu[1:] -= uh[:-1, p.M - 1, :][:, None, :]
         return w - Cu
 
@@ -239,26 +245,26 @@ class ModeOracle:
 
     def _solve_ca(self, r: np.ndarray, alpha: float) -> np.ndarray:
         p, tab = self.p, self.tab
-        x = np.einsum("kl,lmj->kmj", V_inverse(p.L, alpha), r)
+        x = time_apply(V_inverse(p.L, alpha), r)
         d = d_values(p.L, alpha)
         y = np.empty_like(x)
         for k in range(p.L):
             G = np.eye(p.M) + d[k] * tab.H
             B = G[None, :, :] - p.dT * self.lam[:, None, None] * tab.Q[None, :, :]
             y[k] = np.linalg.solve(B, x[k].T[:, :, None])[:, :, 0].T
-        return np.einsum("lk,kmj->lmj", V_matrix(p.L, alpha), y)
+        return time_apply(V_matrix(p.L, alpha), y)
 
     def iterate(self, uh: np.ndarray, alpha: float) -> np.ndarray:
         p, tab = self.p, self.tab
         r = self.residual(uh)
-        x = np.einsum("kl,lmj->kmj", V_inverse(p.L, alpha), r)
+        x = time_apply(V_inverse(p.L, alpha), r)
         d = d_values(p.L, alpha)
         y = np.empty_like(x)
         for k in range(p.L):
             G = np.eye(p.M) + d[k] * tab.H
             B = G[None, :, :] - p.dT * self.lam[:, None, None] * tab.Q[None, :, :]
             y[k] = np.linalg.solve(B, x[k].T[:, :, None])[:, :, 0].T
-        c = np.einsum("lk,kmj->lmj", V_matrix(p.L, alpha), y)
+        c = time_apply(V_matrix(p.L, alpha), y)
         return uh + c
 
 

@@ -1,6 +1,8 @@
-"""Builds libpint.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension machinery)."""
+"""Builds libpint.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension machinery).
+Each translation unit compiles to its own object in parallel; one nvcc call links the library."""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
@@ -8,31 +10,47 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libpint.so")
 SOURCES = ["kernels.cu", "spatial2d.cu", "pint_abi.cpp", "host_numerics.cpp"]
+HEADERS = ["internal.h", "host_numerics.h", "fft_reg.cuh", "device_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 LIBS = ["-lnccl"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
+def _compile(src: str) -> tuple[str, subprocess.CompletedProcess]:
+    obj = os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
+    cmd = [NVCC, *FLAGS, "-c", "-o", obj, src, "-I", os.path.join(ROOT, "include")]
+    return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "host_numerics.h"), os.path.join(CSRC, "fft_reg.cuh"),
-                   os.path.join(CSRC, "device_common.cuh"),
-                   os.path.join(ROOT, "include", "pint.h")]
+    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pint.h")]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
-    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB, *srcs, "-I", os.path.join(ROOT, "include"), *LIBS]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    os.makedirs(OBJ, exist_ok=True)
     log = os.path.join(HERE, "build.log")
+    with cf.ThreadPoolExecutor(len(srcs)) as ex:
+        results = list(ex.map(_compile, srcs))
+    text = "".join(" ".join(r.args) + "\n" + r.stdout + r.stderr for _, r in results)
+    failed = [r for _, r in results if r.returncode != 0]
+    if not failed:
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB,
+               *[o for o, _ in results], *LIBS]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        text += " ".join(cmd) + "\n" + res.stdout + res.stderr
+        if res.returncode != 0:
+            failed = [res]
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        f.write(text)
+    if failed:
+        sys.stderr.write("".join(r.stdout + r.stderr for r in failed))
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stdout.write(res.stderr)
+        sys.stdout.write(text)
     return LIB
 
 

@@ -142,6 +142,8 @@ cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, cons
                                  double *out2, cudaStream_t s);
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,
                                 cudaStream_t s);
+// ||w||_inf of w = (u0 + v_0, v_1, ...) with the forcing st.v attached (one double at `out`)
+cudaError_t launch_w_inf(const Geometry &g, const StaticTables &st, double *out, cudaStream_t s);
 // Hermitian mode storage switch of the iterate u: complex128 <-> real fp64 (first L M N doubles)
 cudaError_t launch_storage_convert(const Geometry &g, const Buffers &b, bool to_real, cudaStream_t s);
 cudaError_t launch_square_first(const double *in, double *out, cudaStream_t s);

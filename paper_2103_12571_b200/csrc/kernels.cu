@@ -316,24 +316,24 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
           double *ur = (double *)u + (size_t)row * g.N + n0 + t;
           ur[0] = n1;
           ur[g.N / 2] = n2;
-          if (row / M == L - 1) dmax = fmax(dmax, fmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
+          if (row / M == L - 1) dmax = nanmax(dmax, nanmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
         } else {
           u[(size_t)row * g.N + n0 + t] = overwrite ? c : cadd(uo[k], c);   // direct form: u = C_a^{-1} r
           if (row / M == L - 1) {
             const double2 dd = overwrite ? csub(c, uo[k]) : c;
-            dmax = fmax(dmax, hypot(dd.x, dd.y));
+            dmax = nanmax(dmax, hypot(dd.x, dd.y));
           }
         }
       }
     }
   }
   if (diff_slot) {
-    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    for (int o = 16; o > 0; o >>= 1) dmax = nanmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
     __syncthreads();
     if (threadIdx.x == 0) {
       double v = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = nanmax(v, red[w]);
       atomicMax(diff_slot, dbl_bits(v));  // non-negative doubles order like their bit patterns
     }
   }
@@ -467,24 +467,24 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
           double *ur = (double *)u + (size_t)m * g.N + n0 + (size_t)l * lstride + t;
           ur[0] = n1;
           ur[g.N / 2] = n2;
-          if (l == g.L - 1) dmax = fmax(dmax, fmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
+          if (l == g.L - 1) dmax = nanmax(dmax, nanmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
         } else {
           ub[(size_t)l * lstride + t] = overwrite ? c : cadd(uo[k], c);
           if (l == g.L - 1) {
             const double2 dd = overwrite ? csub(c, uo[k]) : c;
-            dmax = fmax(dmax, hypot(dd.x, dd.y));
+            dmax = nanmax(dmax, hypot(dd.x, dd.y));
           }
         }
       }
     }
   }
   if (diff_slot) {
-    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    for (int o = 16; o > 0; o >>= 1) dmax = nanmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
     __syncthreads();
     if (threadIdx.x == 0) {
       double v = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = nanmax(v, red[w]);
       atomicMax(diff_slot, dbl_bits(v));
     }
   }
@@ -1166,18 +1166,18 @@ __global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables s
     for (int m = 0; m < M; ++m) {
       const double a2 = r[m].x * r[m].x + r[m].y * r[m].y;
       acc2 += a2;
-      accm = fmax(accm, sqrt(a2));
+      accm = nanmax(accm, sqrt(a2));
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
     acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
-    accm = fmax(accm, __shfl_xor_sync(0xffffffffu, accm, o));
+    accm = nanmax(accm, __shfl_xor_sync(0xffffffffu, accm, o));
   }
   if ((threadIdx.x & 31) == 0) { s2[threadIdx.x >> 5] = acc2; sm_[threadIdx.x >> 5] = accm; }
   __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0.0, b = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s2[w]; b = fmax(b, sm_[w]); }
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += s2[w]; b = nanmax(b, sm_[w]); }
     partial[2 * blockIdx.x] = a;
     partial[2 * blockIdx.x + 1] = b;
   }
@@ -1186,10 +1186,10 @@ __global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables s
 __global__ void reduce_partials_kernel(const double *partial, int nblocks, double *out) {
   // one warp, fixed order -> deterministic
   double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < nblocks; i += 32) { a += partial[2 * i]; b = fmax(b, partial[2 * i + 1]); }
+  for (int i = threadIdx.x; i < nblocks; i += 32) { a += partial[2 * i]; b = nanmax(b, partial[2 * i + 1]); }
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);
-    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    b = nanmax(b, __shfl_xor_sync(0xffffffffu, b, o));
   }
   if (threadIdx.x == 0) { out[0] = sqrt(a); out[1] = b; }
 }
@@ -1200,6 +1200,27 @@ __global__ void init_iterate_kernel(Geometry g, const double2 *__restrict__ u0, 
        i += (long long)gridDim.x * blockDim.x) {
     if (real) ((double *)u)[i] = __ldg(u0 + (i % g.N)).x;
     else u[i] = __ldg(u0 + (i % g.N));
+  }
+}
+
+// ||w||_inf with a forcing attached (Alg. 2's gamma): w_0 = u0 + v_0 on every node of global
+// step 0 (rank 0's local step 0), w_l = v_l otherwise; NaN-propagating max into out (as bits)
+__global__ void __launch_bounds__(256) w_inf_kernel(Geometry g, StaticTables st, unsigned long long *out) {
+  __shared__ double red[8];
+  double m = 0.0;
+  const long long total = (long long)g.L * g.M * g.N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 v = __ldg(st.v + i);
+    if (st.rank == 0 && i < (long long)g.M * g.N) v = cadd(v, __ldg(st.u0 + (i % g.N)));
+    m = nanmax(m, hypot(v.x, v.y));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = nanmax(m, red[w]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));   // non-negative: bit order = value order
   }
 }
 
@@ -1280,13 +1301,14 @@ LaunchCfg choose_launch(const Geometry &g) {
     } else {
       lc.pcr_mode = 1;
       int jA = g.logN / 2;            // R = 2^jA classes of length N/R
-      lc.pcr_chunk = 4096;
-      if (g.nfac > 1) {
-        // chunk halo F R: keep C + 2 F R within the chunk kernel's register capacity
-        // (kChunkThreads * kChunkIPT) and the class length N/R within the class pass's (4096)
-        lc.pcr_chunk = 2048;
-        while (jA > 1 && lc.pcr_chunk + 2 * g.nfac * (1 << jA) > kChunkThreads * kChunkIPT) --jA;
-      }
+      lc.pcr_chunk = g.nfac > 1 ? 2048 : 4096;
+      // The chunk kernel updates at most kChunkThreads * kChunkIPT values per level, so the tile
+      // C + 2 F R (chunk + halos) must fit it (every nfac: N = 2^20 with F = 1 gives R = 1024 and
+      // a 6144-value tile at C = 4096).  Lower jA while the class length N/R stays <= 4096 (the
+      // class pass's tile), then shrink the chunk.
+      const int cap = kChunkThreads * kChunkIPT;
+      while (jA > 1 && lc.pcr_chunk + 2 * g.nfac * (1 << jA) > cap && (g.N >> (jA - 1)) <= 4096) --jA;
+      while (lc.pcr_chunk > 256 && lc.pcr_chunk + 2 * g.nfac * (1 << jA) > cap) lc.pcr_chunk >>= 1;
       lc.pcr_R = 1 << jA;
       int nq = g.N / lc.pcr_R;
       int t = 4096 / nq;
@@ -1459,6 +1481,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       rec(s);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       const int C = lc.pcr_chunk, H = R * g.nfac;
+      if (C + 2 * H > kChunkThreads * kChunkIPT) return cudaErrorInvalidConfiguration;   // see choose_launch
       smem = (size_t)(C + 2 * H) * sizeof(double2);
       if ((e = set_smem((const void *)pcr_chunk_kernel, smem)) != cudaSuccess) return e;
       pcr_chunk_kernel<<<lines * (g.N / C), kChunkThreads, smem, s>>>(g, at, b.X, b.Y, C, H, jOff, st.slots);
@@ -1739,6 +1762,13 @@ cudaError_t launch_square_first(const double *in, double *out, cudaStream_t s) {
 }
 cudaError_t launch_sqrt_into(const double *in, double *out, cudaStream_t s) {
   sqrt_into_kernel<<<1, 1, 0, s>>>(in, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_w_inf(const Geometry &g, const StaticTables &st, double *out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  w_inf_kernel<<<num_sms() * 4, 256, 0, s>>>(g, st, (unsigned long long *)out);
   return cudaGetLastError();
 }
 

@@ -180,6 +180,27 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
     }                                                                                     \
   } while (0)
 
+// pint_create error paths: free the half-built context and its communicator (nothing leaks)
+static pint_status create_abort(pint_ctx *c, pint_status st) {
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return st;
+}
+#define CREATE_TRY(c, expr)                                                                       \
+  do {                                                                                            \
+    cudaError_t _e = (expr);                                                                      \
+    if (_e != cudaSuccess)                                                                        \
+      return create_abort(c, fail(PINT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
+  } while (0)
+
+// entry points that enqueue work bind the context's device first (cheap when already current), so
+// a thread driving contexts on several devices never launches on the wrong one
+#define BIND_DEVICE(c)                                                                            \
+  do {                                                                                            \
+    cudaError_t _e = cudaSetDevice((c)->dist.device);                                             \
+    if (_e != cudaSuccess) return fail(PINT_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
 extern "C" {
 
 int32_t pint_abi_version(void) { return PINT_ABI_VERSION; }
@@ -222,6 +243,8 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   if (s != PINT_OK) return s;
   if (!d) return fail(PINT_ERR_INVALID, "dist is NULL");
   if (!u_dev || !work_dev || !u0_host) return fail(PINT_ERR_INVALID, "NULL buffer");
+  for (size_t i = 0; i < 2 * (size_t)p->nx * (p->dim == 2 ? p->ny : 1); ++i)
+    if (!std::isfinite(u0_host[i])) return fail(PINT_ERR_NUMERIC, "u0 has a non-finite entry");
   if (forcing_host) return fail(PINT_ERR_INVALID, "forcing_host must be NULL (attach a forcing with pint_set_forcing)");
   if (((uintptr_t)u_dev) % 16) return fail(PINT_ERR_INVALID, "u_dev must be 16-byte aligned");
   if (((uintptr_t)work_dev) % 256) return fail(PINT_ERR_INVALID, "work_dev must be 256-byte aligned");
@@ -297,7 +320,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   size_t o_px = o; ptw(g.lognx);
   size_t o_py = o; ptw(g.logny);
   double2 *sbase = (double2 *)(c->work + lay.off_static);
-  CUDA_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+  CREATE_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
   c->st.twL = sbase + o_twL;
   c->st.twx = sbase + o_twx;
   c->st.twy = sbase + o_twy;
@@ -325,8 +348,8 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
       std::memcpy(&id, d->nccl_unique_id, sizeof id);
       ncclResult_t r = ncclCommInitRank(&c->comm, P, id, rank);
       if (r != ncclSuccess) {
-        delete c;
-        return fail(PINT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        c->comm = nullptr;
+        return create_abort(c, fail(PINT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
       }
     } else {
       c->loopback = true;
@@ -336,7 +359,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     std::vector<int> sym(2 * (size_t)g.L);
     for (int q = 0; q < g.L; ++q) { sym[q] = q; sym[g.L + q] = q; }
     int *dsym = (int *)(c->work + lay.off_sym);
-    CUDA_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CREATE_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     c->st.slots = dsym;
     c->st.unitof = dsym + g.L;
     c->st.nsolve = g.L;
@@ -345,8 +368,8 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
             (double *)(c->work + lay.off_red), (unsigned *)(c->work + lay.off_sync)};
-  CUDA_TRY(c, launch_init_iterate(c->g, c->st, b, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // host staging buffer goes out of scope
+  CREATE_TRY(c, launch_init_iterate(c->g, c->st, b, c->stream));
+  CREATE_TRY(c, cudaStreamSynchronize(c->stream));  // host staging buffer goes out of scope
   *out = c;
   return PINT_OK;
 }
@@ -358,14 +381,33 @@ static Buffers buffers(pint_ctx *c) {
 
 pint_status pint_w_inf(pint_ctx *c, double *w_inf) {
   if (!c || !w_inf) return fail(PINT_ERR_INVALID, "NULL argument");
-  double m = 0;
-  for (int n = 0; n < c->g.N; ++n) m = std::fmax(m, std::hypot(c->u0[2 * n], c->u0[2 * n + 1]));
-  *w_inf = m;
+  if (!c->st.v) {   // b == 0: w = (u0 replicated, 0, ..., 0)
+    double m = 0;
+    for (int n = 0; n < c->g.N; ++n) m = std::fmax(m, std::hypot(c->u0[2 * n], c->u0[2 * n + 1]));
+    *w_inf = m;
+    return PINT_OK;
+  }
+  // forcing attached: w = (u0 + v_0, v_1, ..., v_{L-1}) reduced on the device
+  BIND_DEVICE(c);
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  double *slot = (double *)(c->work + c->lay.off_red) + 148 * 8 * 2 + 64 + PINT_MAX_SCHEDULE;
+  CUDA_TRY(c, launch_w_inf(c->g, c->st, slot, c->stream));
+  if (c->P > 1) {
+    if (!c->comm) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: ||w|| needs every rank");
+    ncclResult_t r = ncclAllReduce(slot, slot, 1, ncclDouble, ncclMax, c->comm, c->stream);
+    if (r != ncclSuccess) { c->poisoned = true; return fail(PINT_ERR_NCCL, ncclGetErrorString(r)); }
+  }
+  double h = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&h, slot, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (!std::isfinite(h)) return fail(PINT_ERR_NUMERIC, "non-finite ||w||_inf");
+  *w_inf = h;
   return PINT_OK;
 }
 
 pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (K < 0 || K > PINT_MAX_SCHEDULE || (K > 0 && !alpha))
     return fail(PINT_ERR_INVALID, "K must be in [0, PINT_MAX_SCHEDULE]");
@@ -381,9 +423,12 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
   const int F = g.nfac;
   std::vector<AlphaTables> tabs(K);
   std::vector<std::vector<cld>> hS(K), hSi(K), hD(K), hdk(K);
-  std::vector<char> blob(c->lay.alpha_bytes_each);
+  // every blob is built and validated on the host before any upload: a failing entry leaves the
+  // context's current schedule and its device tables untouched
+  std::vector<std::vector<char>> blobs(K, std::vector<char>(c->lay.alpha_bytes_each, 0));
+  std::vector<size_t> offs_pcr(K, 0), offs_inv(K, 0);
   for (int a = 0; a < K; ++a) {
-    std::memset(blob.data(), 0, blob.size());
+    std::vector<char> &blob = blobs[a];
     const ld al = alpha[a];
     double *sf = (double *)blob.data();
     double *sb = sf + L;
@@ -487,9 +532,17 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
         }
       }
     }
+    offs_pcr[a] = off_pcr;
+    offs_inv[a] = off_inv;
+  }
+  // commit: the old schedule is dropped first, so a failed upload leaves no schedule (ERR_SCHEDULE)
+  c->at.clear();
+  c->alphas.clear();
+  for (int a = 0; a < K; ++a) {
+    const ld al = alpha[a];
+    const size_t off_pcr = offs_pcr[a], off_inv = offs_inv[a];
     char *dst = c->work + c->lay.off_alpha + (size_t)a * c->lay.alpha_bytes_each;
-    CUDA_TRY(c, cudaMemcpyAsync(dst, blob.data(), blob.size(), cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(dst, blobs[a].data(), blobs[a].size(), cudaMemcpyHostToDevice, c->stream));
     AlphaTables &t = tabs[a];
     t.scale_fwd = (const double *)dst;
     t.scale_bwd = (const double *)dst + L;
@@ -502,6 +555,7 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
     t.pcr = g.dim == 1 ? (const double2 *)(dst + off_pcr) : nullptr;
     t.inv_e = g.dim == 1 ? (const double2 *)(dst + off_inv) : nullptr;
   }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // host blobs go out of scope
   c->at = tabs;
   c->alphas.assign(alpha, alpha + K);
   c->h_S = hS;
@@ -620,6 +674,7 @@ static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
 
 pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (n_iter < 0) return fail(PINT_ERR_INVALID, "n_iter < 0");
   if (c->loopback) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: use pint_group_iterate");
@@ -643,6 +698,8 @@ pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf
     }
     CUDA_TRY(c, cudaMemcpyAsync(last_step_diff_inf, slots, n_iter * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < n_iter; ++i)   // the device max propagates NaN (nanmax): a diverged iterate
+      if (!std::isfinite(last_step_diff_inf[i])) return fail(PINT_ERR_NUMERIC, "non-finite last-step difference");
   }
   return PINT_OK;
 }
@@ -753,6 +810,7 @@ pint_status pint_group_residual_norm(pint_ctx *const *ctxs, int32_t P, double *l
 
 pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   Buffers b = buffers(c);
   double *out2 = (double *)(c->work + c->lay.off_red) + 148 * 8 * 2;
@@ -784,6 +842,7 @@ pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf) {
 
 pint_status pint_get_iterate(pint_ctx *c, double *u_host) {
   if (!c || !u_host) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (c->hermitian) {   // real storage: the first L M N doubles, expanded to (re, 0)
     const size_t n = (size_t)c->g.L * c->g.M * c->g.N;
@@ -802,6 +861,7 @@ pint_status pint_get_iterate(pint_ctx *c, double *u_host) {
 
 pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
   if (!c || !u_host) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const size_t off = ((size_t)(c->g.L - 1) * c->g.M + (c->g.M - 1)) * c->g.N;
   if (c->hermitian) {
@@ -822,7 +882,10 @@ pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
 
 pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t reset_iterate) {
   if (!c || !u0_host) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  for (size_t i = 0; i < 2 * (size_t)c->g.N; ++i)
+    if (!std::isfinite(u0_host[i])) return fail(PINT_ERR_NUMERIC, "u0 has a non-finite entry");
   if (c->hermitian)
     for (int n = 0; n < c->g.N; ++n)
       if (u0_host[2 * n + 1] != 0.0) return fail(PINT_ERR_INVALID, "Hermitian mode needs a real u0");
@@ -837,6 +900,7 @@ pint_status pint_set_initial_value(pint_ctx *c, const double *u0_host, int32_t r
 
 pint_status pint_next_window(pint_ctx *c) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (c->P != 1) return fail(PINT_ERR_INVALID, "windowed stepping is single-rank only");
   const Geometry &g = c->g;
@@ -865,6 +929,7 @@ pint_status pint_destroy(pint_ctx *c) {
 
 pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms) {
   if (!c || !kernel_ms) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
   if (c->P > 1) return fail(PINT_ERR_INVALID, "per-launch profiling is single-rank only");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   if (c->k + n_iter > (int)c->alphas.size())
@@ -918,6 +983,7 @@ pint_status pint_set_form(pint_ctx *c, int32_t form) {
 
 pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
   if (on) {
@@ -966,8 +1032,11 @@ pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double to
   if (!c || !iters) return fail(PINT_ERR_INVALID, "NULL argument");
   if (!(m0 > 0) || !(tol > 0) || max_iter < 1 || max_iter > PINT_MAX_SCHEDULE || !(eps >= 0) || !(tau >= 0))
     return fail(PINT_ERR_INVALID, "need m0 > 0, tol > 0, eps, tau >= 0, 1 <= max_iter <= PINT_MAX_SCHEDULE");
-  double w_inf = 0;
-  for (int n = 0; n < c->g.N; ++n) w_inf = std::fmax(w_inf, std::hypot(c->u0[2 * n], c->u0[2 * n + 1]));
+  double w_inf = 0;   // ||w||_inf of the assembled w, forcing included
+  {
+    pint_status sw = pint_w_inf(c, &w_inf);
+    if (sw != PINT_OK) return sw;
+  }
   const ld gam = (ld)c->prob.L * (3.0L * eps + tau) * w_inf;          // Alg. 2 line 1
   if (!(gam > 0)) return fail(PINT_ERR_INVALID, "gamma = L(3 eps + tau)||w||_inf must be > 0");
   std::vector<double> alphas, ms{m0};
@@ -1010,6 +1079,7 @@ pint_status pint_set_forcing(pint_ctx *c, const void *v_dev) {
 
 pint_status pint_sequential(pint_ctx *c) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
   if (c->st.v) return fail(PINT_ERR_INVALID, "the sequential baseline assumes b == 0");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
@@ -1073,6 +1143,7 @@ pint_status pint_get_factors(pint_ctx *c, int32_t a, int32_t k, double *d_k, dou
 
 pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s) {
   if (!c || a < 0 || a >= (int)c->at.size()) return fail(PINT_ERR_INVALID, "bad schedule entry");
+  BIND_DEVICE(c);
   if (c->P > 1) return fail(PINT_ERR_INVALID, "debug stages are single-rank only");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   Buffers b = buffers(c);
@@ -1089,6 +1160,7 @@ pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s) {
 
 pint_status pint_debug_get_work(pint_ctx *c, int32_t which, double *host) {
   if (!c || !host) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
   Buffers b = buffers(c);
   const double2 *src = which == 0 ? b.X : ((c->g.dim == 1 && c->lc.pcr_mode == 1) ? b.Y : b.X);
   CUDA_TRY(c, cudaMemcpyAsync(host, src, c->lay.vec_bytes, cudaMemcpyDeviceToHost, c->stream));

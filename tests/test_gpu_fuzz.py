@@ -37,6 +37,18 @@ def _cases(n=96, seed=2103):
     return out
 
 
+def _max_cond(p, alpha):
+    from oracle.collocation import Tableau
+    from oracle.paralpha import d_values
+    tab = Tableau(p.M)
+    worst = 0.0
+    for d in d_values(p.L, alpha):
+        r = d / (1 + d)
+        _, V = np.linalg.eig(tab.Q - r * tab.Dt @ tab.H)
+        worst = max(worst, np.linalg.cond(V))
+    return worst
+
+
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0].name)
 def test_fuzz_parity(case):
     import paper_2103_12571_b200 as PB
@@ -58,7 +70,11 @@ def test_fuzz_parity(case):
         s.set_alpha_schedule(a)
     except PB.PintError as e:
         s.close()
-        pytest.skip(f"alpha tables rejected by the documented guard: {e}")
+        # the guard may only fire where the frequency blocks really are near-defective: check the
+        # eigenvector conditioning of Q - r_k D_t H_M independently (numpy) before accepting it
+        assert e.status == 3, str(e)
+        assert _max_cond(p, a[0]) > 1e6, f"guard fired on a well-conditioned alpha: {e}"
+        pytest.skip(f"alpha tables rejected by the documented guard (near-defective): {e}")
     o = Oracle(p, u0, "dense" if p.M * p.N <= 1024 else "fourier")
     u = o.initial()
     for k in range(2):

@@ -30,8 +30,8 @@ CASES = [W.CONFIGS[1], W.CONFIGS[2], W.reduced(3), W.reduced(4), W.reduced(5),
 def test_hermitian_parity(p, form):
     import paper_2103_12571_b200 as PB
     u0 = p.u0()
-    if np.iscomplexobj(u0) and np.abs(u0.imag).max() > 0:
-        pytest.skip("complex initial value")
+    if np.abs(u0.imag).max() > 0:   # edge cases draw complex u0: the real-data mode takes its real part
+        u0 = np.ascontiguousarray(u0.real.astype(np.complex128))
     a = _alphas(p, u0)
     s = PB.Solver(p, u0)
     s.set_form(form)
