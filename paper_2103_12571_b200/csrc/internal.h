@@ -3,8 +3,21 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace pint {
+
+// A/B experiment switches read from the environment (PINT_LEGACY2D, PINT_LEGACY_PIPE, PINT_FWD_T,
+// PINT_BWD_T, PINT_SP_SKIP, PINT_SP_CLAIM).  Compiled in only with -DPINT_EXPERIMENTS: the product
+// library ignores the environment (pint_experiments_enabled() == 0; bench.py refuses otherwise).
+inline const char *experiment_env(const char *name) {
+#ifdef PINT_EXPERIMENTS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // Per-alpha device tables (pointers into work_dev).  Frequency index p is BIT-REVERSED:
 // slot p holds frequency k = bitrev_L(p) (the time FFT leaves its output in that order).
@@ -109,7 +122,15 @@ size_t spatial_sync_bytes(int lines);
 cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
                              const double2 *spec, unsigned *sync, int lines, cudaStream_t s);
 bool spatial2d_supported(const Geometry &g);
-bool reg2d_path(const Geometry &g);   // the 2-D path runs spatial2d (else the generic row/column kernels)
+// Pipelined per-stage plane passes (spatial2d.cu): the default for the grids and
+// modes they serve (2-D, 512..4096 per axis, M <= 4, complex storage)
+bool spatial_pipe_geometry(const Geometry &g);                          // grid/M served (needs a 2nd vector)
+bool spatial_pipe_supported(const Geometry &g, const StaticTables &st);  // ... and the current mode
+// X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector
+cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                                double2 *Yb, cudaStream_t s);
+bool reg2d_path(const Geometry &g);
+bool pipe2d_geometry(const Geometry &g);   // the 2-D path can run the pipelined passes (2 work vectors)   // the 2-D path runs spatial2d (else the generic row/column kernels)
 size_t fwd_smem_bytes(const Geometry &g, int T);
 
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
@@ -155,8 +176,8 @@ cudaError_t launch_halo_pack(const Geometry &g, const Buffers &b, double2 *hsend
 // send chunks by destination.
 cudaError_t launch_xdft(const Geometry &g, const StaticTables &st, const AlphaTables &at,
                         const double2 *in, double2 *out, bool inverse, cudaStream_t s);
-int launches_per_iteration(const Geometry &g, const LaunchCfg &lc);
-const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i);
+int launches_per_iteration(const Geometry &g, const LaunchCfg &lc, const StaticTables &st);
+const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i);
 
 // Optional per-launch event recorder (pint_iterate_profiled): when set, every launch wrapper
 // records ev[n++] on the launch stream right after each kernel it enqueues.
@@ -165,5 +186,6 @@ struct Recorder {
   int n, cap;
 };
 void set_recorder(Recorder *r);
+void record_launch(cudaStream_t s);   // records the recorder's next event (no-op when unset)
 
 }  // namespace pint

@@ -1240,6 +1240,9 @@ __global__ void complex_from_real_kernel(const double *__restrict__ src, double2
 
 static thread_local Recorder *g_rec = nullptr;
 void set_recorder(Recorder *r) { g_rec = r; }
+void record_launch(cudaStream_t s) {
+  if (g_rec && g_rec->n < g_rec->cap) cudaEventRecord(g_rec->ev[g_rec->n++], s);
+}
 static inline void rec(cudaStream_t s) {
   if (g_rec && g_rec->n < g_rec->cap) cudaEventRecord(g_rec->ev[g_rec->n++], s);
 }
@@ -1259,10 +1262,18 @@ size_t fwd_smem_bytes(const Geometry &g, int T) { return (size_t)g.L * g.M * T *
 
 // 2-D path selection: default = all-node time tiles + the persistent spatial pipeline
 // (spatial2d.cu); PINT_LEGACY2D=1 selects the six-pass path (A/B measurements only).
+static bool legacy_pipe() {   // A/B: the fused persistent spatial2d kernel instead of the pipelined passes
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_LEGACY_PIPE");
+    v = (e && atoi(e)) ? 1 : 0;
+  }
+  return v == 1;
+}
 static bool legacy2d() {
   static int v = -1;
   if (v < 0) {
-    const char *e = getenv("PINT_LEGACY2D");
+    const char *e = experiment_env("PINT_LEGACY2D");
     v = (e && atoi(e)) ? 1 : 0;
   }
   return v == 1;
@@ -1279,14 +1290,14 @@ LaunchCfg choose_launch(const Geometry &g) {
   // forward/backward tile: as many spatial points as fit ~100 KB (2 CTAs per SM), <= 16
   int T = 16;
   while (T > 1 && fwd_smem_bytes(g, T) > 64 * 1024) T >>= 1;
-  if (const char *e = getenv("PINT_FWD_T")) T = atoi(e);   // tuning experiments only
+  if (const char *e = experiment_env("PINT_FWD_T")) T = atoi(e);   // tuning experiments only
   while (T > g.N) T >>= 1;
   lc.fwd_T = T;
   // backward tile: measured on config 3 (L = 256, M = 3): T = 8 (96 KB) 0.63 ms vs T = 4 0.75 ms
   // (the forward tile, which also evaluates the stencil, prefers T = 4 at 3 CTAs per SM)
   int TB = 16;
   while (TB > 1 && fwd_smem_bytes(g, TB) > 100 * 1024) TB >>= 1;
-  if (const char *e = getenv("PINT_BWD_T")) TB = atoi(e);   // tuning experiments only
+  if (const char *e = experiment_env("PINT_BWD_T")) TB = atoi(e);   // tuning experiments only
   while (TB > g.N) TB >>= 1;
   lc.bwd_T = TB;
   int T2 = 32;
@@ -1321,20 +1332,27 @@ LaunchCfg choose_launch(const Geometry &g) {
   return lc;
 }
 
-int launches_per_iteration(const Geometry &g, const LaunchCfg &lc) {
-  if (g.dim == 2) return reg2d(g) ? 4 : 6;
+static bool pipe2d(const Geometry &g, const StaticTables &st) {
+  return reg2d(g) && spatial_pipe_supported(g, st) && !legacy_pipe();
+}
+bool pipe2d_geometry(const Geometry &g) { return reg2d(g) && spatial_pipe_geometry(g); }
+
+int launches_per_iteration(const Geometry &g, const LaunchCfg &lc, const StaticTables &st) {
+  if (g.dim == 2) return pipe2d(g, st) ? 6 : (reg2d(g) ? 4 : 6);
   return lc.pcr_mode == 0 ? 3 : 4;
 }
 
-const char *kernel_name(const Geometry &g, const LaunchCfg &lc, int i) {
+const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i) {
   static const char *k1a[] = {"fwd_kernel", "pcr_classes_kernel", "bwd_kernel"};
   static const char *k1b[] = {"fwd_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
   static const char *k2[] = {"residual2d_kernel", "tfft_fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
                              "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
   static const char *k2p[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial2d_kernel", "tfft_bwd_kernel"};
-  const int n = launches_per_iteration(g, lc);
+  static const char *k2q[] = {"residual2d_kernel", "tfft_fwd_kernel", "rows_pipe_kernel<fwd>", "cols_pipe_kernel",
+                              "rows_pipe_kernel<inv>", "tfft_bwd_kernel"};
+  const int n = launches_per_iteration(g, lc, st);
   if (i < 0 || i >= n) return "";
-  if (g.dim == 2) return reg2d(g) ? k2p[i] : k2[i];
+  if (g.dim == 2) return pipe2d(g, st) ? k2q[i] : (reg2d(g) ? k2p[i] : k2[i]);
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 
@@ -1488,6 +1506,11 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       rec(s);
       *out = b.Y;
     }
+  } else if (pipe2d(g, st)) {
+    e = launch_spatial_pipe(g, st, at, b.X, b.Y, s);   // R, C, I: three launches, each recorded
+    *out = b.X;
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
   } else if (reg2d(g)) {
     e = launch_spatial2d(g, st, at, b.X, nullptr, b.sync, st.nsolve * g.M, s);
     rec(s);

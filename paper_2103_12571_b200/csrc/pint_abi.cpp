@@ -128,7 +128,7 @@ static Geometry make_geometry(const pint_problem *p, int P) {
 static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   Layout L{};
   L.vec_bytes = (size_t)g.L * g.M * g.N * sizeof(double2);
-  L.two_vectors = (g.dim == 1 && lc.pcr_mode == 1) || P > 1;
+  L.two_vectors = (g.dim == 1 && lc.pcr_mode == 1) || P > 1 || pipe2d_geometry(g);
   size_t off = 0;
   L.off_X = off;
   // 2-D: one extra M x N unit plane group (Hermitian packed mode: units 0..L/2 after Z)
@@ -963,13 +963,13 @@ pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms
 const char *pint_kernel_name(pint_ctx *c, int32_t i) {
   if (!c) return "";
   if (c->form == PINT_FORM_DIRECT) return kernel_name_direct(c->g, c->lc, i);
-  return kernel_name(c->g, c->lc, i);
+  return kernel_name(c->g, c->lc, c->st, i);
 }
 
 int32_t pint_launches_per_iteration(pint_ctx *c) {
   if (!c) return -1;
   if (c->form == PINT_FORM_DIRECT) return launches_per_iteration_direct(c->g, c->lc);
-  return launches_per_iteration(c->g, c->lc);
+  return launches_per_iteration(c->g, c->lc, c->st);
 }
 
 pint_status pint_set_form(pint_ctx *c, int32_t form) {

@@ -26,12 +26,15 @@
 // Units: st.slots[0 .. nsolve) (every slot; Hermitian mode: the L/2 + 1 slots with k <= L/2,
 // whose R stage unpacks X_k from the packed real-data spectra Z_k, Z_{L-k} and whose planes live in
 // the unit area of X, internal.h).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
 
 #include "device_common.cuh"
 #include "fft_reg.cuh"
+#include "host_numerics.h"
 #include "internal.h"
 
 namespace pint {
@@ -486,9 +489,9 @@ SpatialPlan make_spatial_plan(const Geometry &g, int lines, bool synth) {
   sp.nC = sp.B * g.M * (g.nx / sp.TC);
   sp.synth = synth ? 1 : 0;
   sp.nstage = synth ? 2 : 3;
-  const char *sk = getenv("PINT_SP_SKIP");   // timing experiments only: bit s skips stage s (R, C, I)
+  const char *sk = experiment_env("PINT_SP_SKIP");   // timing experiments only: bit s skips stage s (R, C, I)
   sp.skip = sk ? atoi(sk) : 0;
-  const char *cl = getenv("PINT_SP_CLAIM");  // A/B experiments: 0 = static round-robin assignment
+  const char *cl = experiment_env("PINT_SP_CLAIM");  // A/B experiments: 0 = static round-robin assignment
   sp.claim = cl ? atoi(cl) : 1;
   sp.rounds = sp.nbatch + sp.nstage - 1;
   return sp;
@@ -546,6 +549,417 @@ cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const Al
   PINT_SP3(11) PINT_SP3(12)
 #undef PINT_SP3
 #undef PINT_SP
+  return cudaErrorInvalidValue;
+}
+
+// =============================================================================================
+// Pipelined plane passes (one persistent launch per stage; the default 2-D solve for the large
+// grids).  Same arithmetic as the R / C / I items above, restructured so that the
+// memory stream never waits for the FFT arithmetic and DRAM only sees whole 128-byte lines:
+//   * every CTA (one per SM) runs G consumer groups (one item each) over a ring of NS
+//     shared-memory slots filled by the TMA unit (1-D cp.async.bulk of contiguous rows for R,
+//     tensor-map tiles for C and I) that complete on one mbarrier per slot;
+//   * the group that finishes reading slot s refills it with the CTA's item k + NS at once (ring
+//     order = item order, every wait points to an earlier item: no deadlock);
+//   * the spectral planes between R, C and I are stored COLUMN-BLOCKED: S-slot q of row y of a
+//     plane lives at blk(q) ny 8 + y 8 + (q mod 8), blocks of 8 S-slot columns (128 bytes per
+//     row).  R writes whole 128-byte block rows, C reads and writes block columns (a CTA takes
+//     both 4-column halves of a block back to back, so the two 64-byte halves of every line meet
+//     in L2), I reads a row as one tensor-map box of all blocks;
+//   * results leave from registers (R, coalesced) or through the slot (I: node transform on the
+//     way out; C: the column transpose).
+// Items are assigned statically: CTA b takes b, b + grid, ... (grid = one CTA per SM).
+
+namespace {
+
+constexpr int kBW = 8;   // S-slot columns per block of the blocked spectral layout (128 bytes)
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+// first 1024-byte aligned address (shared window) at or after p
+__device__ __forceinline__ unsigned char *align_smem_1024(unsigned char *p) {
+  const unsigned a = smem_u32(p);
+  return p + (((a + 1023u) & ~1023u) - a);
+}
+
+// blocked offset of S-slot q in row y of a plane with ny rows
+__device__ __forceinline__ size_t blocked(int q, int y, int logny) {
+  return ((size_t)(q >> 3) << (logny + 3)) + ((size_t)y << 3) + (q & 7);
+}
+
+// y_m = sum_j A[m][j] x_j over the MM lines (stride NX) of each of the `rows` row groups of a
+// natural-order tile, in place (A: M x M complex, global, L1-resident broadcast reads)
+template <int MM>
+__device__ __forceinline__ void node_natural(double2 *tile, const double2 *__restrict__ A, int rows, int NX, int t,
+                                             int GT) {
+  double2 ar[MM * MM];
+#pragma unroll
+  for (int i = 0; i < MM * MM; ++i) ar[i] = __ldg(A + i);
+  for (int i = t; i < rows * NX; i += GT) {
+    const int r = i / NX, x = i - r * NX;
+    double2 *base = tile + (size_t)r * MM * NX + x;
+    double2 v[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) v[j] = base[j * NX];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < MM; ++j) acc = cfma(ar[m * MM + j], v[j], acc);
+      base[m * NX] = acc;
+    }
+  }
+}
+
+// R (INV = false) and I (INV = true) stage.  Item = YR rows y0.. of all MM node planes of one
+// unit (frequency slot p): LINES = YR MM lines of NX points, TPL threads per line, GT = LINES TPL
+// threads per group.  R loads natural rows of X (1-D bulk copies) and stores blocked spectral
+// rows into Yb (a second vector: a blocked row is spread over the whole plane, so R cannot work
+// in place); I loads blocked rows of Yb through the tensor map `tmi` (box: all blocks of one
+// row) and stores natural rows into X.  Named barriers: 1 + line id (exchanges, TPL > 32), then
+// one per group.
+template <class PX, int MM, bool INV, bool NODE>
+__global__ void __launch_bounds__(512, 1)
+    rows_pipe_kernel(const __grid_constant__ CUtensorMap tmi, const Geometry g, StaticTables st, AlphaTables at,
+                     double2 *__restrict__ X, double2 *__restrict__ Yb, int YR, int G, int NS, int nitems) {
+  constexpr int NX = PX::N, TPL = PX::TPL, E = PX::E, R = 1 << PX::BL, TW = PX::twsize();
+  constexpr int NBLK = NX / kBW, IBOX = NBLK < 256 ? NBLK : 256;
+  extern __shared__ __align__(1024) unsigned char smraw_[];
+  unsigned char *smraw = align_smem_1024(smraw_);   // the launch adds 1 KB of slack
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  double2 *twx = reinterpret_cast<double2 *>(smraw + 128);
+  double2 *ring = reinterpret_cast<double2 *>(smraw + 1024 + (((size_t)TW * sizeof(double2) + 1023) & ~(size_t)1023));
+  const int LINES = YR * MM, GT = LINES * TPL, slot_elems = LINES * NX;
+  const int gid = threadIdx.x / GT, t = threadIdx.x - gid * GT;
+  const int l = t / TPL, tau = t - l * TPL;
+  const int lid = gid * LINES + l;
+  const int gbar = 1 + (TPL > 32 ? G * LINES : 0) + gid;   // after the line barriers (TPL > 32)
+  const int ygroups = g.ny / YR;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
+    mbar_init_fence();
+    if (INV) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmi) : "memory");
+  }
+  copy_table(twx, st.ptwx, TW);
+  __syncthreads();
+  // fill the ring slot of CTA-local item k (one elected thread)
+  auto issue = [&](int k) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= nitems) return;
+    const int un = it / ygroups, y0 = (it - un * ygroups) * YR;
+    const int p = __ldg(st.slots + un);
+    uint64_t *bar = full + k % NS;
+    double2 *dst = ring + (size_t)(k % NS) * slot_elems;
+    mbar_arrive_expect_tx(bar, (unsigned)(slot_elems * sizeof(double2)));
+    for (int yy = 0; yy < YR; ++yy)
+      for (int m = 0; m < MM; ++m) {
+        double2 *d = dst + (size_t)(yy * MM + m) * NX;
+        if constexpr (INV) {
+          for (int b = 0; b < NBLK; b += IBOX)
+            tma_load_3d(d + b * kBW, &tmi, 0, y0 + yy, (p * MM + m) * NBLK + b, bar);
+        } else {
+          bulk_g2s(d, X + ((size_t)p * MM + m) * g.N + ((size_t)(y0 + yy) << PX::LOGN), NX * sizeof(double2), bar);
+        }
+      }
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NS; ++k) issue(k);
+  for (int k = gid;; k += G) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= nitems) break;
+    const int s = k % NS;
+    double2 *tile = ring + (size_t)s * slot_elems;
+    double2 *line = tile + (size_t)l * NX;
+    const int un = it / ygroups, y0 = (it - un * ygroups) * YR;
+    const int p = __ldg(st.slots + un);
+    double2 *xp = X + (size_t)p * MM * g.N;
+    const int yy = l / MM, m = l - yy * MM;
+    mbar_wait(full + s, (unsigned)((k / NS) & 1));
+    double2 v[E];
+    if constexpr (!INV) {
+      if constexpr (NODE) {   // x1 = S_p^{-1} x on the natural rows, in place
+        node_natural<MM>(tile, at.Sinv + (size_t)p * MM * MM, YR, NX, t, GT);
+        named_sync(gbar, GT);
+      }
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = line[rfft::natural_pos<PX>(tau, i)];
+      rfft::line_sync<PX>(lid);   // the engine's exchanges write swizzled positions
+      rfft::forward_regs<PX>(v, line, lid, tau, twx);
+      fence_proxy_async_smem();   // this thread's generic smem accesses before the refill's async ones
+      named_sync(gbar, GT);       // every line of the slot has done its last read
+      if (t == 0) issue(k + NS);
+      double2 *dst = Yb + ((size_t)p * MM + m) * g.N;
+#pragma unroll
+      for (int u = 0; u < E / R; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[blocked(rfft::s_slot<PX>(tau, u, r), y0 + yy, g.logny)] = v[u * R + r];
+    } else {
+#pragma unroll
+      for (int u = 0; u < E / R; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[u * R + r] = line[rfft::s_slot<PX>(tau, u, r)];
+      rfft::line_sync<PX>(lid);
+      rfft::inverse_in_regs<PX>(v, line, lid, tau, twx);
+      rfft::to_smem<PX, 0>(v, line, tau);
+      named_sync(gbar, GT);
+      if constexpr (NODE) {   // y = G_p^{-1} S_p x2 on the way out
+        const double2 *A = at.SG + (size_t)p * MM * MM;
+        double2 ar[MM * MM];
+#pragma unroll
+        for (int i = 0; i < MM * MM; ++i) ar[i] = __ldg(A + i);
+        for (int i = t; i < YR * NX; i += GT) {
+          const int x = i & (NX - 1), r2 = i >> PX::LOGN;
+          const double2 *base = tile + (size_t)r2 * MM * NX + rfft::F<PX>(x);
+          double2 w[MM];
+#pragma unroll
+          for (int j = 0; j < MM; ++j) w[j] = base[j * NX];
+          double2 *o = xp + ((size_t)(y0 + r2) << PX::LOGN) + x;
+#pragma unroll
+          for (int mm = 0; mm < MM; ++mm) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < MM; ++j) acc = cfma(ar[mm * MM + j], w[j], acc);
+            o[(size_t)mm * g.N] = acc;
+          }
+        }
+      } else {
+        for (int i = t; i < LINES * NX; i += GT) {
+          const int x = i & (NX - 1), li = i >> PX::LOGN;
+          const int y2 = li / MM, m2 = li - y2 * MM;
+          xp[(size_t)m2 * g.N + ((size_t)(y0 + y2) << PX::LOGN) + x] = tile[(size_t)li * NX + rfft::F<PX>(x)];
+        }
+      }
+      fence_proxy_async_smem();
+      named_sync(gbar, GT);
+      if (t == 0) issue(k + NS);
+    }
+  }
+}
+
+// C stage, in place on the blocked planes Yb.  Item = TC consecutive S-slot columns (one half of
+// a block, or the whole block when TC = 8) of one plane (unit, node), loaded by the tensor map `tmc` (box {2 TC doubles, BR rows,
+// 1 block}, 16-byte swizzle of the TC*16-byte rows: conflict-free column reads).  One group of
+// TC TPL threads; the CTA's items k, k+1 are the two halves of one block.  Then lines of stride
+// ls for the engine's exchanges: y-DIF, x2 = x1 / ((1 - s lambda) nx ny) with the y-symbol table
+// staged in shared memory, y-DIT; the transpose back to block rows goes through the slot.
+template <class PX, class PY>
+__global__ void __launch_bounds__(256, 1)
+    cols_pipe_kernel(const __grid_constant__ CUtensorMap tmc, const Geometry g, StaticTables st, AlphaTables at,
+                     double2 *__restrict__ Yb, int lT, int NS, int ls, int BR, int nitems) {
+  constexpr int NY = PY::N, TPL = PY::TPL, E = PY::E, R = 1 << PY::BL, TW = PY::twsize();
+  constexpr int LX = PX::LOGN, LY = PY::LOGN, NX = PX::N, NBLK = NX / kBW;
+  extern __shared__ __align__(1024) unsigned char smraw_[];
+  unsigned char *smraw = align_smem_1024(smraw_);   // swizzled TMA tiles need 1 KB-aligned slots
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  double2 *twy = reinterpret_cast<double2 *>(smraw + 128);
+  double2 *lamy = twy + TW;
+  double2 *ring = reinterpret_cast<double2 *>(
+      smraw + 1024 + (((size_t)(TW + NY) * sizeof(double2) + 1023) & ~(size_t)1023));
+  const int TC = 1 << lT, NH = kBW >> lT;   // columns per item, items per block
+  const int slot_elems = ((TC * ls * (int)sizeof(double2) + 1023) & ~1023) / (int)sizeof(double2);
+  const int t = threadIdx.x, c = t / TPL, tau = t - c * TPL;
+  const int GT = TC * TPL;
+  const int M = g.M;
+  const double inv_n = 1.0 / ((double)NX * (double)NY);
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
+    mbar_init_fence();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmc) : "memory");
+  }
+  copy_table(twy, st.ptwy, TW);
+  copy_table(lamy, st.lamy, NY);
+  __syncthreads();
+  // CTA-local item k: block pair b = blockIdx + (k / NH) grid, half k mod NH
+  auto item_of = [&](int k) { return (blockIdx.x + (k / NH) * gridDim.x) * NH + (k % NH); };
+  auto issue = [&](int k) {
+    const int it = item_of(k);
+    if (it >= nitems) return;
+    const int bi = it / NH, half = it - bi * NH;
+    const int li = bi / NBLK, blk = bi - li * NBLK;
+    const int un = li / M, mm = li - un * M;
+    const int plane = __ldg(st.slots + un) * M + mm;
+    uint64_t *bar = full + k % NS;
+    double2 *dst = ring + (size_t)(k % NS) * slot_elems;
+    mbar_arrive_expect_tx(bar, (unsigned)(NY * TC * sizeof(double2)));
+    for (int b = 0; b < NY; b += BR) tma_load_3d(dst + (size_t)b * TC, &tmc, 2 * TC * half, b, plane * NBLK + blk, bar);
+  };
+  if (t == 0)
+    for (int k = 0; k < NS; ++k) issue(k);
+  for (int k = 0;; ++k) {
+    const int it = item_of(k);
+    if (it >= nitems) break;
+    const int s = k % NS;
+    double2 *tile = ring + (size_t)s * slot_elems;
+    const int bi = it / NH, half = it - bi * NH;
+    const int li = bi / NBLK, blk = bi - li * NBLK;
+    const int un = li / M, mm = li - un * M;
+    const int q = __ldg(st.slots + un) * M + mm;   // table line (slot, node) == plane index
+    const int q0 = blk * kBW + half * TC;          // first S-slot column of the item
+    double2 *xb = Yb + (size_t)q * g.N + ((size_t)blk << (LY + 3)) + half * TC;
+    const double2 sh = __ldg(at.shift + q);
+    const double2 lx = __ldg(st.lamx + brev(rfft::slot_to_pos<PX>(q0 + c), LX));
+    mbar_wait(full + s, (unsigned)((k / NS) & 1));
+    double2 v[E];
+    // column c, row y of the swizzled TMA tile: 16-byte chunk c ^ ((y TC / 8) mod TC) of row y
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int y = rfft::natural_pos<PY>(tau, i);
+      v[i] = tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))];
+    }
+    named_sync(1, GT);   // the slot is re-used as TC exchange lines of stride ls
+    double2 *line = tile + (size_t)c * ls;
+    rfft::forward_regs<PY>(v, line, 1 + c, tau, twy);
+#pragma unroll
+    for (int u = 0; u < E / R; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        // 1 / ((1 - s lambda) nx ny), lambda = lambda_x + lambda_y (|1 - s lambda| >= 7.7e-4)
+        const double2 lam = cadd(lx, lamy[brev(rfft::last_pos<PY>(tau, u, r), LY)]);
+        const double2 sl = cmul(sh, lam);
+        const double dr = 1.0 - sl.x, di = -sl.y;
+        const double qq = dr * dr + di * di;
+        double rq = __drcp_rn(qq);
+        rq = fma(rq, fma(-qq, rq, 1.0), rq);
+        const double den = inv_n * rq;
+        v[u * R + r] = cmul(v[u * R + r], make_double2(dr * den, -di * den));
+      }
+    rfft::inverse_in_regs<PY>(v, line, 1 + c, tau, twy);
+    rfft::to_smem<PY, 0>(v, line, tau);
+    named_sync(1, GT);
+    for (int i = t; i < (NY << lT); i += GT) {
+      const int cc = i & (TC - 1), y = i >> lT;
+      xb[((size_t)y << 3) + cc] = tile[(size_t)cc * ls + rfft::F<PY>(y)];
+    }
+    fence_proxy_async_smem();
+    named_sync(1, GT);
+    if (t == 0) issue(k + NS);
+  }
+}
+
+struct PipePlan {
+  int YR, G, NS;           // R / I: rows per item, groups, slots
+  int lT, NSC, ls, BR;     // C: log2 columns per item, slots, line stride, TMA box rows
+  size_t rsmem, csmem;
+};
+
+bool pipe_plan(const Geometry &g, PipePlan &pp) {
+  if (g.dim != 2 || g.lognx < 9 || g.logny < 9 || g.lognx > 11 || g.logny > 11) return false;
+  if (g.lognx - g.logny > 1 || g.logny - g.lognx > 1 || g.M > 4) return false;
+  const int tplx = g.nx / 16, tply = g.ny / 16;
+  // R / I: items of YR rows x M nodes, <= 256 threads and <= 64 KB, two groups, three slots
+  int YR = 1;
+  while (2 * YR * g.M * tplx <= 256 && 2 * YR * g.M * g.nx * 16 <= 64 * 1024 && g.ny % (2 * YR) == 0) YR *= 2;
+  if (YR * g.M * tplx > 256 || (size_t)YR * g.M * g.nx * 16 > 64 * 1024) return false;
+  pp.YR = YR;
+  pp.G = 512 / (YR * g.M * tplx);
+  if (pp.G > 2) pp.G = 2;
+  pp.NS = pp.G + 1;
+  const size_t tw_r = ((size_t)pass_twiddle_count(g.lognx, 4) * 16 + 1023) & ~(size_t)1023;
+  pp.rsmem = 1024 + 1024 + tw_r + (size_t)pp.NS * YR * g.M * g.nx * 16;
+  // C: a whole 8-column block per item if it fits 256 threads and 64 KB, else half blocks
+  int lT = 3;
+  while (lT > 2 && ((1 << lT) * tply > 256 || (size_t)(1 << lT) * g.ny * 16 > 64 * 1024)) --lT;
+  const int TC = 1 << lT;
+  if (TC * tply > 256) return false;
+  pp.lT = lT;
+  pp.NSC = 3;
+  pp.ls = g.ny + (TC >= 8 ? 1 : 8 / TC);
+  pp.BR = g.ny < 256 ? g.ny : 256;
+  const size_t tw_c = ((size_t)(pass_twiddle_count(g.logny, 4) + g.ny) * 16 + 1023) & ~(size_t)1023;
+  const size_t cslot = ((size_t)TC * pp.ls * 16 + 1023) & ~(size_t)1023;
+  pp.csmem = 1024 + 1024 + tw_c + (size_t)pp.NSC * cslot;
+  const int lbr = tplx > 32 ? pp.G * YR * g.M : 0, lbc = tply > 32 ? TC : 0;   // named barrier ids
+  if (lbr + pp.G + 1 > 16 || lbc + 2 > 16) return false;
+  return pp.rsmem <= 227 * 1024 && pp.csmem <= 227 * 1024;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+  }
+  return fn;
+}
+
+// tensor map over the blocked spectral planes Yb: dims {16 doubles (one block row), ny rows,
+// planes * nx/8 blocks}
+bool blocked_map(const Geometry &g, double2 *Yb, unsigned box0, unsigned box1, unsigned box2, CUtensorMapSwizzle swz,
+                 CUtensorMap &tm) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * kBW, (cuuint64_t)g.ny, (cuuint64_t)g.L * g.M * (g.nx / kBW)};
+  const cuuint64_t strides[2] = {(cuuint64_t)kBW * 16, (cuuint64_t)kBW * 16 * g.ny};
+  const cuuint32_t box[3] = {box0, box1, box2};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)Yb, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int LX, int LY, int MM>
+cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, const PipePlan &pp,
+                        double2 *X, double2 *Yb, int units, bool node, cudaStream_t s) {
+  using PX = rfft::Plan<LX, 4>;
+  using PY = rfft::Plan<LY, 4>;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e;
+  const int TC = 1 << pp.lT;
+  const unsigned nblk = g.nx / kBW;
+  CUtensorMap tmi, tmc;
+  if (!blocked_map(g, Yb, 2 * kBW, 1, nblk < 256 ? nblk : 256, CU_TENSOR_MAP_SWIZZLE_NONE, tmi) ||
+      !blocked_map(g, Yb, 2 * TC, pp.BR, 1, TC == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, tmc))
+    return cudaErrorNotSupported;
+  const int rthreads = pp.G * pp.YR * MM * PX::TPL;
+  const int ritems = units * (g.ny / pp.YR);
+  auto rows = [&](auto fn) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.rsmem);
+    if (e2 != cudaSuccess) return e2;
+    fn<<<sms, rthreads, pp.rsmem, s>>>(tmi, g, st, at, X, Yb, pp.YR, pp.G, pp.NS, ritems);
+    record_launch(s);
+    return cudaGetLastError();
+  };
+  e = node ? rows(rows_pipe_kernel<PX, MM, false, true>) : rows(rows_pipe_kernel<PX, MM, false, false>);
+  if (e != cudaSuccess) return e;
+  {
+    const void *fn = (const void *)cols_pipe_kernel<PX, PY>;
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.csmem)) != cudaSuccess)
+      return e;
+    const int cthreads = TC * PY::TPL;
+    const int citems = units * g.M * (g.nx / TC);
+    cols_pipe_kernel<PX, PY><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls, pp.BR, citems);
+    record_launch(s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return node ? rows(rows_pipe_kernel<PX, MM, true, true>) : rows(rows_pipe_kernel<PX, MM, true, false>);
+}
+
+}  // namespace
+
+bool spatial_pipe_geometry(const Geometry &g) {
+  PipePlan pp;
+  return pipe_plan(g, pp);
+}
+
+bool spatial_pipe_supported(const Geometry &g, const StaticTables &st) { return !st.packed && spatial_pipe_geometry(g); }
+
+cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                                double2 *Yb, cudaStream_t s) {
+  PipePlan pp;
+  if (st.packed || !pipe_plan(g, pp) || Yb == X) return cudaErrorInvalidValue;
+  const bool node = st.P == 1;
+  const int units = st.nsolve;
+#define PINT_PIPE(LXX, LYY, MMM) \
+  if (g.lognx == LXX && g.logny == LYY && g.M == MMM) return launch_pipe<LXX, LYY, MMM>(g, st, at, pp, X, Yb, units, node, s);
+#define PINT_PIPE_M(LXX, LYY) PINT_PIPE(LXX, LYY, 1) PINT_PIPE(LXX, LYY, 2) PINT_PIPE(LXX, LYY, 3) PINT_PIPE(LXX, LYY, 4)
+  PINT_PIPE_M(9, 9) PINT_PIPE_M(10, 10) PINT_PIPE_M(9, 10) PINT_PIPE_M(10, 9) PINT_PIPE_M(11, 11) PINT_PIPE_M(10, 11)
+  PINT_PIPE_M(11, 10)
+#undef PINT_PIPE_M
+#undef PINT_PIPE
   return cudaErrorInvalidValue;
 }
 
