@@ -33,7 +33,9 @@ ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32
               "fft2d_cols_kernel": 32, "fft2d_rows_kernel<inv>": 32, "bwd_kernel": 48, "residual2d_kernel": 32,
               "tfft_fwd_kernel": 32, "tfft_bwd_kernel": 48,
               # persistent 2-D spatial pipeline: the three plane passes' compulsory traffic (3 x 32 B)
-              "spatial2d_kernel": 96}
+              "spatial2d_kernel": 96,
+              # pipelined plane passes (same 3 x 32 B, one launch each)
+              "rows_pipe_kernel<fwd>": 32, "cols_pipe_kernel": 32, "rows_pipe_kernel<inv>": 32}
 # direct form (u = C_a^{-1}((C_a - C)u + w)): no read of u, input synthesized from one N-vector
 ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
                      "cols_direct_kernel": 16, "fft2d_rows_kernel<inv>": 32, "tfft_bwd_kernel": 32,
@@ -199,6 +201,8 @@ def main():
     ap.add_argument("--no-sequential", action="store_true", help="skip the sequential Radau IIA baseline")
     ap.add_argument("--hermitian", action="store_true",
                     help="real-data fast path (SURVEY 8(f) row 1): solve only frequencies k <= L/2")
+    ap.add_argument("--allow-experiments", action="store_true",
+                    help="A/B only: accept a library built with -DPINT_EXPERIMENTS (PINT_LIBRARY)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     p = W.CONFIGS[args.config]
@@ -213,6 +217,10 @@ def main():
 
     import torch
     import paper_2103_12571_b200 as P
+    experiments = P.experiments_enabled()
+    if experiments and not args.allow_experiments:
+        sys.exit("bench.py: the loaded libpint was built with -DPINT_EXPERIMENTS (environment switches); "
+                 "refusing to report it (pass --allow-experiments for A/B runs)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -385,6 +393,7 @@ def main():
                 "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
                            "unknowns": p.U, "bytes_per_vector": 16 * p.U, "form": args.form,
                            "hermitian": bool(args.hermitian),
+                           "library": "experiments (A/B build)" if experiments else "product",
                            "l2": "inputs larger than L2 (no flush)" if 16 * p.U > 126e6 else "L2-resident",
                            "parallelism": "single GPU" if world == 1 else
                            f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},

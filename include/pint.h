@@ -262,6 +262,10 @@ const char *pint_last_error(void);
 
 int32_t pint_abi_version(void);
 
+/* 1 if the library was built with -DPINT_EXPERIMENTS (A/B builds that read the PINT_* environment
+ * switches of csrc/internal.h), 0 for the product library, which ignores the environment. */
+int32_t pint_experiments_enabled(void);
+
 /* ---- introspection (tests / benchmarks) ------------------------------------------------- */
 
 /* Number of kernel launches one iteration enqueues, and the names of the kernels. */

@@ -12,6 +12,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libpint.so")
+# A/B experiment library (-DPINT_EXPERIMENTS: reads the PINT_* switches of internal.h); never the
+# product: bench.py refuses it unless --allow-experiments, and records it
+LIB_EXP = os.path.join(HERE, "libpint_exp.so")
 SOURCES = ["kernels.cu", "spatial2d.cu", "pint_abi.cpp", "host_numerics.cpp"]
 HEADERS = ["internal.h", "host_numerics.h", "fft_reg.cuh", "device_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -20,25 +23,28 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
-def _compile(src: str) -> tuple[str, subprocess.CompletedProcess]:
-    obj = os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
-    cmd = [NVCC, *FLAGS, "-c", "-o", obj, src, "-I", os.path.join(ROOT, "include")]
+def _compile(src: str, objdir: str, extra: list[str]) -> tuple[str, subprocess.CompletedProcess]:
+    obj = os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")
+    cmd = [NVCC, *FLAGS, *extra, "-c", "-o", obj, src, "-I", os.path.join(ROOT, "include")]
     return obj, subprocess.run(cmd, capture_output=True, text=True)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, experiments: bool = False) -> str:
+    lib = LIB_EXP if experiments else LIB
+    objdir = OBJ + ("_exp" if experiments else "")
+    extra = ["-DPINT_EXPERIMENTS"] if experiments else []
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pint.h")]
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
-    log = os.path.join(HERE, "build.log")
+    if not force and os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(d) for d in deps):
+        return lib
+    os.makedirs(objdir, exist_ok=True)
+    log = os.path.join(HERE, "build_exp.log" if experiments else "build.log")
     with cf.ThreadPoolExecutor(len(srcs)) as ex:
-        results = list(ex.map(_compile, srcs))
+        results = list(ex.map(lambda src: _compile(src, objdir, extra), srcs))
     text = "".join(" ".join(r.args) + "\n" + r.stdout + r.stderr for _, r in results)
     failed = [r for _, r in results if r.returncode != 0]
     if not failed:
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB,
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib,
                *[o for o, _ in results], *LIBS]
         res = subprocess.run(cmd, capture_output=True, text=True)
         text += " ".join(cmd) + "\n" + res.stdout + res.stderr
@@ -51,9 +57,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stdout.write(text)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="-v" in sys.argv, force=True, experiments="--experiments" in sys.argv))

@@ -67,6 +67,7 @@ struct StaticTables {
   int P, rank;
   // per-pass twiddle tables of the register FFT engine (fft_reg.cuh) for nx, ny
   const double2 *ptwx, *ptwy;
+  const double2 *ptwx5, *ptwy5;   // nx / ny plans with radix-32 passes (pipelined plane stages)
   // Frequency units of the 2-D spatial solves: unit q < nsolve solves slot slots[q].  Default:
   // every slot (slots[q] = q), X holds the planes.  Hermitian (packed) mode (real data,
   // pint_set_hermitian): two real spatial points n' and n' + N/2 share one complex time series

@@ -145,7 +145,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   L.off_static = off;
   const int mb = g.dim == 2 ? spatial_maxb(g) : 4;
   L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8 + pass_twiddle_count(g.lognx, mb) +
-                            pass_twiddle_count(g.logny, mb)) * sizeof(double2);
+                            pass_twiddle_count(g.logny, mb) + pass_twiddle_count(g.lognx, 5) +
+                            pass_twiddle_count(g.logny, 5)) * sizeof(double2);
   off = align_up(off + L.static_bytes, 256);
   L.off_alpha = off;
   const size_t LM = (size_t)g.L * g.M;
@@ -204,6 +205,14 @@ static pint_status create_abort(pint_ctx *c, pint_status st) {
 extern "C" {
 
 int32_t pint_abi_version(void) { return PINT_ABI_VERSION; }
+
+int32_t pint_experiments_enabled(void) {
+#ifdef PINT_EXPERIMENTS
+  return 1;
+#else
+  return 0;
+#endif
+}
 
 const char *pint_last_error(void) { return g_err.c_str(); }
 
@@ -319,6 +328,13 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   };
   size_t o_px = o; ptw(g.lognx);
   size_t o_py = o; ptw(g.logny);
+  auto ptw5 = [&](int logn) {   // radix-32 plans of the pipelined plane passes
+    std::vector<cld> v;
+    pass_twiddles(logn, 5, v);
+    for (const cld &w : v) host[o++] = make_double2((double)w.real(), (double)w.imag());
+  };
+  size_t o_px5 = o; ptw5(g.lognx);
+  size_t o_py5 = o; ptw5(g.logny);
   double2 *sbase = (double2 *)(c->work + lay.off_static);
   CREATE_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
   c->st.twL = sbase + o_twL;
@@ -329,6 +345,8 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   c->st.u0 = sbase + o_u0;
   c->st.ptwx = sbase + o_px;
   c->st.ptwy = sbase + o_py;
+  c->st.ptwx5 = sbase + o_px5;
+  c->st.ptwy5 = sbase + o_py5;
   c->st.P = P;
   c->st.rank = rank;
   if (P == 1) {

@@ -619,7 +619,7 @@ __device__ __forceinline__ void node_natural(double2 *tile, const double2 *__res
 // row) and stores natural rows into X.  Named barriers: 1 + line id (exchanges, TPL > 32), then
 // one per group.
 template <class PX, int MM, bool INV, bool NODE>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
     rows_pipe_kernel(const __grid_constant__ CUtensorMap tmi, const Geometry g, StaticTables st, AlphaTables at,
                      double2 *__restrict__ X, double2 *__restrict__ Yb, int YR, int G, int NS, int nitems) {
   constexpr int NX = PX::N, TPL = PX::TPL, E = PX::E, R = 1 << PX::BL, TW = PX::twsize();
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init_fence();
     if (INV) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmi) : "memory");
   }
-  copy_table(twx, st.ptwx, TW);
+  copy_table(twx, PX::E == 32 ? st.ptwx5 : st.ptwx, TW);
   __syncthreads();
   // fill the ring slot of CTA-local item k (one elected thread)
   auto issue = [&](int k) {
@@ -737,13 +737,15 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 // C stage, in place on the blocked planes Yb.  Item = TC consecutive S-slot columns (one half of
-// a block, or the whole block when TC = 8) of one plane (unit, node), loaded by the tensor map `tmc` (box {2 TC doubles, BR rows,
-// 1 block}, 16-byte swizzle of the TC*16-byte rows: conflict-free column reads).  One group of
-// TC TPL threads; the CTA's items k, k+1 are the two halves of one block.  Then lines of stride
-// ls for the engine's exchanges: y-DIF, x2 = x1 / ((1 - s lambda) nx ny) with the y-symbol table
-// staged in shared memory, y-DIT; the transpose back to block rows goes through the slot.
-template <class PX, class PY>
-__global__ void __launch_bounds__(256, 1)
+// a block, or the whole block when TC = 8) of one plane (unit, node), loaded by the tensor map
+// `tmc` (box {2 TC doubles, BR rows, 1 block}, 16-byte swizzle of the TC*16-byte rows:
+// conflict-free column reads).  GC groups of TC TPL threads over a ring of NS slots; the CTA's
+// items k, k+1 are the two halves of one block (with two groups they run side by side).  Then
+// lines of stride ls for the engine's exchanges: y-DIF, x2 = x1 / ((1 - s lambda) nx ny) with the
+// y-symbol table staged in shared memory, y-DIT; the transpose back to block rows goes through
+// the slot.  Named barriers: 1 + group, then 1 + GC + line (TPL > 32).
+template <class PX, class PY, int GC>
+__global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 : 1), 1)
     cols_pipe_kernel(const __grid_constant__ CUtensorMap tmc, const Geometry g, StaticTables st, AlphaTables at,
                      double2 *__restrict__ Yb, int lT, int NS, int ls, int BR, int nitems) {
   constexpr int NY = PY::N, TPL = PY::TPL, E = PY::E, R = 1 << PY::BL, TW = PY::twsize();
@@ -757,17 +759,22 @@ __global__ void __launch_bounds__(256, 1)
       smraw + 1024 + (((size_t)(TW + NY) * sizeof(double2) + 1023) & ~(size_t)1023));
   const int TC = 1 << lT, NH = kBW >> lT;   // columns per item, items per block
   const int slot_elems = ((TC * ls * (int)sizeof(double2) + 1023) & ~1023) / (int)sizeof(double2);
-  const int t = threadIdx.x, c = t / TPL, tau = t - c * TPL;
   const int GT = TC * TPL;
+  const int gid = threadIdx.x / GT, t = threadIdx.x - gid * GT, c = t / TPL, tau = t - c * TPL;
+  const int gbar = 1 + gid, lid = GC + gid * TC + c;   // line_sync uses barrier 1 + lid
   const int M = g.M;
   const double inv_n = 1.0 / ((double)NX * (double)NY);
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
     mbar_init_fence();
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmc) : "memory");
   }
-  copy_table(twy, st.ptwy, TW);
-  copy_table(lamy, st.lamy, NY);
+  copy_table(twy, PY::E == 32 ? st.ptwy5 : st.ptwy, TW);
+  // y symbols by spectral position P (frequency bitrev(P)), stored at P ^ ((P >> SH) & 7): the last
+  // pass reads positions R_L g + r with lanes on consecutive g, which this XOR spreads over the
+  // eight 16-byte bank slots (a plain bit-reversed table read was 8-way conflicted)
+  constexpr int SH = PY::BL > 3 ? PY::BL : 3;
+  for (int P = threadIdx.x; P < NY; P += blockDim.x) lamy[P ^ ((P >> SH) & 7)] = __ldg(st.lamy + brev(P, LY));
   __syncthreads();
   // CTA-local item k: block pair b = blockIdx + (k / NH) grid, half k mod NH
   auto item_of = [&](int k) { return (blockIdx.x + (k / NH) * gridDim.x) * NH + (k % NH); };
@@ -783,9 +790,9 @@ __global__ void __launch_bounds__(256, 1)
     mbar_arrive_expect_tx(bar, (unsigned)(NY * TC * sizeof(double2)));
     for (int b = 0; b < NY; b += BR) tma_load_3d(dst + (size_t)b * TC, &tmc, 2 * TC * half, b, plane * NBLK + blk, bar);
   };
-  if (t == 0)
+  if (threadIdx.x == 0)
     for (int k = 0; k < NS; ++k) issue(k);
-  for (int k = 0;; ++k) {
+  for (int k = gid;; k += GC) {
     const int it = item_of(k);
     if (it >= nitems) break;
     const int s = k % NS;
@@ -806,15 +813,16 @@ __global__ void __launch_bounds__(256, 1)
       const int y = rfft::natural_pos<PY>(tau, i);
       v[i] = tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))];
     }
-    named_sync(1, GT);   // the slot is re-used as TC exchange lines of stride ls
+    named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
     double2 *line = tile + (size_t)c * ls;
-    rfft::forward_regs<PY>(v, line, 1 + c, tau, twy);
+    rfft::forward_regs<PY>(v, line, lid, tau, twy);
 #pragma unroll
     for (int u = 0; u < E / R; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         // 1 / ((1 - s lambda) nx ny), lambda = lambda_x + lambda_y (|1 - s lambda| >= 7.7e-4)
-        const double2 lam = cadd(lx, lamy[brev(rfft::last_pos<PY>(tau, u, r), LY)]);
+        const int P = rfft::last_pos<PY>(tau, u, r);
+        const double2 lam = cadd(lx, lamy[P ^ ((P >> SH) & 7)]);
         const double2 sl = cmul(sh, lam);
         const double dr = 1.0 - sl.x, di = -sl.y;
         const double qq = dr * dr + di * di;
@@ -823,29 +831,34 @@ __global__ void __launch_bounds__(256, 1)
         const double den = inv_n * rq;
         v[u * R + r] = cmul(v[u * R + r], make_double2(dr * den, -di * den));
       }
-    rfft::inverse_in_regs<PY>(v, line, 1 + c, tau, twy);
+    rfft::inverse_in_regs<PY>(v, line, lid, tau, twy);
     rfft::to_smem<PY, 0>(v, line, tau);
-    named_sync(1, GT);
+    named_sync(gbar, GT);
     for (int i = t; i < (NY << lT); i += GT) {
       const int cc = i & (TC - 1), y = i >> lT;
       xb[((size_t)y << 3) + cc] = tile[(size_t)cc * ls + rfft::F<PY>(y)];
     }
     fence_proxy_async_smem();
-    named_sync(1, GT);
+    named_sync(gbar, GT);
     if (t == 0) issue(k + NS);
   }
 }
 
 struct PipePlan {
   int YR, G, NS;           // R / I: rows per item, groups, slots
-  int lT, NSC, ls, BR;     // C: log2 columns per item, slots, line stride, TMA box rows
+  int lT, GC, NSC, ls, BR; // C: log2 columns per item, groups (1: 255 registers, 2: 128), slots, line stride, box rows
+  int rx32, ry32;          // radix-32 plans for the 1024-point x (R, I) / y (C) axes
   size_t rsmem, csmem;
 };
 
 bool pipe_plan(const Geometry &g, PipePlan &pp) {
   if (g.dim != 2 || g.lognx < 9 || g.logny < 9 || g.lognx > 11 || g.logny > 11) return false;
   if (g.lognx - g.logny > 1 || g.logny - g.lognx > 1 || g.M > 4) return false;
-  const int tplx = g.nx / 16, tply = g.ny / 16;
+  // radix-32 row plan for the R / I passes (1024^2 grids; the C pass must use the same x plan):
+  // R 16.3 -> 13.8 ms, I 13.1 -> 11.8 ms on config 5
+  pp.rx32 = g.lognx == 10 && g.logny == 10 ? 1 : 0;
+  if (const char *e = experiment_env("PINT_R_RADIX32")) pp.rx32 = atoi(e) && g.lognx == 10 && g.logny == 10 ? 1 : 0;
+  const int tplx = pp.rx32 ? 32 : g.nx / 16, tply = g.ny / 16;
   // R / I: items of YR rows x M nodes, <= 256 threads and <= 64 KB, two groups, three slots
   int YR = 1;
   while (2 * YR * g.M * tplx <= 256 && 2 * YR * g.M * g.nx * 16 <= 64 * 1024 && g.ny % (2 * YR) == 0) YR *= 2;
@@ -854,7 +867,7 @@ bool pipe_plan(const Geometry &g, PipePlan &pp) {
   pp.G = 512 / (YR * g.M * tplx);
   if (pp.G > 2) pp.G = 2;
   pp.NS = pp.G + 1;
-  const size_t tw_r = ((size_t)pass_twiddle_count(g.lognx, 4) * 16 + 1023) & ~(size_t)1023;
+  const size_t tw_r = ((size_t)pass_twiddle_count(g.lognx, pp.rx32 ? 5 : 4) * 16 + 1023) & ~(size_t)1023;
   pp.rsmem = 1024 + 1024 + tw_r + (size_t)pp.NS * YR * g.M * g.nx * 16;
   // C: a whole 8-column block per item if it fits 256 threads and 64 KB, else half blocks
   int lT = 3;
@@ -862,14 +875,21 @@ bool pipe_plan(const Geometry &g, PipePlan &pp) {
   const int TC = 1 << lT;
   if (TC * tply > 256) return false;
   pp.lT = lT;
-  pp.NSC = 3;
+  pp.GC = 1;
+  if (const char *e = experiment_env("PINT_C_GROUPS")) pp.GC = atoi(e) == 2 ? 2 : 1;
+  // radix-32 column plan (32 threads x 32 values per line, one exchange per transform, two groups
+  // of 128 threads at <= 255 registers): C 31 -> 24 ms on config 5
+  pp.ry32 = g.logny == 10 && g.lognx == 10 ? 1 : 0;
+  if (const char *e = experiment_env("PINT_C_RADIX32")) pp.ry32 = atoi(e) && g.logny == 10 && g.lognx == 10 ? 1 : 0;
+  if (pp.ry32) pp.GC = 2;
+  pp.NSC = pp.GC + 1 > 3 ? pp.GC + 1 : 3;
   pp.ls = g.ny + (TC >= 8 ? 1 : 8 / TC);
   pp.BR = g.ny < 256 ? g.ny : 256;
-  const size_t tw_c = ((size_t)(pass_twiddle_count(g.logny, 4) + g.ny) * 16 + 1023) & ~(size_t)1023;
+  const size_t tw_c = ((size_t)(pass_twiddle_count(g.logny, pp.ry32 ? 5 : 4) + g.ny) * 16 + 1023) & ~(size_t)1023;
   const size_t cslot = ((size_t)TC * pp.ls * 16 + 1023) & ~(size_t)1023;
   pp.csmem = 1024 + 1024 + tw_c + (size_t)pp.NSC * cslot;
-  const int lbr = tplx > 32 ? pp.G * YR * g.M : 0, lbc = tply > 32 ? TC : 0;   // named barrier ids
-  if (lbr + pp.G + 1 > 16 || lbc + 2 > 16) return false;
+  const int lbr = tplx > 32 && !pp.rx32 ? pp.G * YR * g.M : 0, lbc = tply > 32 && !pp.ry32 ? pp.GC * TC : 0;   // named barrier ids
+  if (lbr + pp.G + 1 > 16 || lbc + pp.GC + 1 > 16) return false;
   return pp.rsmem <= 227 * 1024 && pp.csmem <= 227 * 1024;
 }
 
@@ -899,11 +919,9 @@ bool blocked_map(const Geometry &g, double2 *Yb, unsigned box0, unsigned box1, u
              swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int LX, int LY, int MM>
+template <class PX, class PY, int MM, int GC>
 cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, const PipePlan &pp,
                         double2 *X, double2 *Yb, int units, bool node, cudaStream_t s) {
-  using PX = rfft::Plan<LX, 4>;
-  using PY = rfft::Plan<LY, 4>;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -926,16 +944,34 @@ cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTa
   e = node ? rows(rows_pipe_kernel<PX, MM, false, true>) : rows(rows_pipe_kernel<PX, MM, false, false>);
   if (e != cudaSuccess) return e;
   {
-    const void *fn = (const void *)cols_pipe_kernel<PX, PY>;
+    const void *fn = (const void *)cols_pipe_kernel<PX, PY, GC>;
     if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.csmem)) != cudaSuccess)
       return e;
-    const int cthreads = TC * PY::TPL;
+    const int cthreads = GC * TC * PY::TPL;
     const int citems = units * g.M * (g.nx / TC);
-    cols_pipe_kernel<PX, PY><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls, pp.BR, citems);
+    cols_pipe_kernel<PX, PY, GC><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls, pp.BR,
+                                                                 citems);
     record_launch(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return node ? rows(rows_pipe_kernel<PX, MM, true, true>) : rows(rows_pipe_kernel<PX, MM, true, false>);
+}
+
+// plans: radix-32 passes (Plan<10, 5>: 32 values per thread, one exchange per transform) for
+// 1024-point axes when selected, radix-16 (Plan<L, 4>) otherwise
+template <int LX, int LY, int MM>
+cudaError_t launch_pipe_dispatch(const Geometry &g, const StaticTables &st, const AlphaTables &at, const PipePlan &pp,
+                                 double2 *X, double2 *Yb, int units, bool node, cudaStream_t s) {
+  using PX4 = rfft::Plan<LX, 4>;
+  using PY4 = rfft::Plan<LY, 4>;
+  if constexpr (LX == 10 && LY == 10) {
+    using P5 = rfft::Plan<10, 5>;
+    if (pp.rx32 && pp.ry32) return launch_pipe<P5, P5, MM, 2>(g, st, at, pp, X, Yb, units, node, s);
+    if (pp.ry32) return launch_pipe<PX4, P5, MM, 2>(g, st, at, pp, X, Yb, units, node, s);
+    if (pp.rx32) return launch_pipe<P5, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s);
+  }
+  return pp.GC == 2 ? launch_pipe<PX4, PY4, MM, 2>(g, st, at, pp, X, Yb, units, node, s)
+                    : launch_pipe<PX4, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s);
 }
 
 }  // namespace
@@ -954,7 +990,7 @@ cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const
   const bool node = st.P == 1;
   const int units = st.nsolve;
 #define PINT_PIPE(LXX, LYY, MMM) \
-  if (g.lognx == LXX && g.logny == LYY && g.M == MMM) return launch_pipe<LXX, LYY, MMM>(g, st, at, pp, X, Yb, units, node, s);
+  if (g.lognx == LXX && g.logny == LYY && g.M == MMM) return launch_pipe_dispatch<LXX, LYY, MMM>(g, st, at, pp, X, Yb, units, node, s);
 #define PINT_PIPE_M(LXX, LYY) PINT_PIPE(LXX, LYY, 1) PINT_PIPE(LXX, LYY, 2) PINT_PIPE(LXX, LYY, 3) PINT_PIPE(LXX, LYY, 4)
   PINT_PIPE_M(9, 9) PINT_PIPE_M(10, 10) PINT_PIPE_M(9, 10) PINT_PIPE_M(10, 9) PINT_PIPE_M(11, 11) PINT_PIPE_M(10, 11)
   PINT_PIPE_M(11, 10)

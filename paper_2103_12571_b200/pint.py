@@ -13,7 +13,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpint.so")
+# PINT_LIBRARY selects another build of the same ABI (A/B runs against libpint_exp.so only);
+# bench.py records pint_experiments_enabled() and refuses an experiments build by default
+LIB_PATH = os.environ.get("PINT_LIBRARY") or os.path.join(HERE, "libpint.so")
 
 PINT_OK = 0
 STATUS = {0: "PINT_OK", 1: "PINT_ERR_INVALID", 2: "PINT_ERR_SCHEDULE", 3: "PINT_ERR_NOT_DIAGONALIZABLE",
@@ -29,7 +31,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
            "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential", "pint_set_forcing",
-           "pint_next_window"]
+           "pint_next_window", "pint_experiments_enabled"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -79,6 +81,7 @@ def load_library(path: str = LIB_PATH):
         "pint_destroy": (i32, [vp]),
         "pint_last_error": (ctypes.c_char_p, []),
         "pint_abi_version": (i32, []),
+        "pint_experiments_enabled": (i32, []),
         "pint_launches_per_iteration": (i32, [vp]),
         "pint_get_factors": (i32, [vp, i32, i32, dp, dp, dp, dp]),
         "pint_tableau": (i32, [i32, dp, dp]),
@@ -104,6 +107,11 @@ def load_library(path: str = LIB_PATH):
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def experiments_enabled() -> bool:
+    """True for an A/B build with the PINT_* environment switches compiled in (never the product)."""
+    return bool(load_library().pint_experiments_enabled())
 
 
 def _check(st: int):

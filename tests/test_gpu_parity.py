@@ -181,3 +181,55 @@ def test_parity_full_size_sampled_modes(cfg):
         errs.append(float(np.linalg.norm((g - uh).ravel()) / np.linalg.norm(uh.ravel())))
     s.close()
     assert max(errs) <= TOL, errs
+
+
+# ---- the pipelined plane passes (rows_pipe / cols_pipe) at production plans -------
+
+PIPE_CASES = [
+    W.CONFIGS[5].replace(name="pipe_1024sq_M4_L4", L=4, iters=3),
+    W.CONFIGS[4].replace(name="pipe_512sq_M3_L8", L=8, iters=3),
+    W.CONFIGS[5].replace(name="pipe_1024x512_M2_L4", ny=512, M=2, L=4, iters=3),
+    W.CONFIGS[4].replace(name="pipe_512x1024_M1_L8", ny=1024, M=1, L=8, iters=3),
+    W.CONFIGS[5].replace(name="pipe_2048x1024_heat_M2_L2", nx=2048, op="heat", nu=1e-2, M=2, L=2, iters=2),
+]
+
+
+@pytest.mark.parametrize("p", PIPE_CASES, ids=lambda p: p.name)
+def test_parity_pipe_plans_random(p):
+    """Seeded random complex u0 (every spatial mode excited) through the R / C / I passes; the
+    kernel list proves the pipelined passes ran."""
+    import paper_2103_12571_b200 as PB
+    rng = np.random.default_rng(p.nx + p.ny + p.M)
+    u0 = rng.standard_normal(p.N) + 1j * rng.standard_normal(p.N)
+    s = PB.Solver(p, u0)
+    assert "cols_pipe_kernel" in s.kernel_names(), s.kernel_names()
+    a = [1e-3, 2e-2, 0.2][:p.iters]
+    s.set_alpha_schedule(a)
+    o = Oracle(p, u0, "fourier")
+    u = o.initial()
+    for k in range(p.iters):
+        u = o.iterate(u, a[k])
+        s.iterate(1)
+        assert relative_l2(s.get_iterate(), u) <= TOL, k
+    s.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_parity_pipe_plans_sharded(P):
+    """Time-sharded loopback ranks on a pipelined plan: the node transforms live in the cross-rank
+    DFT kernels and the plane passes run without them (NODE = false instantiations)."""
+    import paper_2103_12571_b200 as PB
+    p = W.CONFIGS[5].replace(name=f"pipe_sharded_P{P}", L=16, M=2, iters=2)
+    rng = np.random.default_rng(P)
+    u0 = rng.standard_normal(p.N) + 1j * rng.standard_normal(p.N)
+    g = PB.Group(p, u0, P)
+    assert "cols_pipe_kernel" in g.ranks[0].kernel_names()
+    a = [1e-3, 5e-2]
+    g.set_alpha_schedule(a)
+    o = Oracle(p, u0, "fourier")
+    u = o.initial()
+    for k in range(2):
+        u = o.iterate(u, a[k])
+        g.iterate(1)
+        assert relative_l2(g.get_iterate(), u) <= TOL, k
+    g.close()
