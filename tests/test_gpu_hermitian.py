@@ -21,7 +21,7 @@ def _alphas(p, u0):
 
 CASES = [W.CONFIGS[1], W.CONFIGS[2], W.reduced(3), W.reduced(4), W.reduced(5),
          W.CONFIGS[3].replace(name="twopass_N16384_L8", nx=16384, L=8, iters=4)] + [
-    p for p in W.edge_cases() if p.N >= 8] + [
+    p for p in W.edge_cases() if p.N >= 8 and p.L >= 2] + [   # documented: N >= 8, L >= 2 (pint.h)
     W.reduced(5).replace(name="red5_adv2d_32x64_M2_L8", nx=32, ny=64, M=2, L=8)]
 
 

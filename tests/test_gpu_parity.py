@@ -82,7 +82,9 @@ def test_last_step_diff_and_residual_norm():
         un = o.iterate(u, a[k])
         d = s.iterate(1, want_diff=True)[0]
         ref = float(np.abs(un[-1] - u[-1]).max())
-        assert d == pytest.approx(ref, rel=1e-6, abs=1e-14)
+        # the difference of two iterates inherits the parity error of each (north star: 1e-9
+        # relative to the iterate), so the absolute bound scales with max|u|, not with d
+        assert d == pytest.approx(ref, rel=1e-6, abs=2e-9 * float(np.abs(un).max()))
         l2, linf = s.residual_norm()
         rl2, rlinf = o.residual_norms(un)
         assert l2 == pytest.approx(rl2, rel=1e-3, abs=1e-13) and linf == pytest.approx(rlinf, rel=1e-3, abs=1e-13)
