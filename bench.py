@@ -35,12 +35,14 @@ ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32
               # persistent 2-D spatial pipeline: the three plane passes' compulsory traffic (3 x 32 B)
               "spatial2d_kernel": 96,
               # pipelined plane passes (same 3 x 32 B, one launch each)
-              "rows_pipe_kernel<fwd>": 32, "cols_pipe_kernel": 32, "rows_pipe_kernel<inv>": 32}
+              "rows_pipe_kernel<fwd>": 32, "cols_pipe_kernel": 32, "rows_pipe_kernel<inv>": 32,
+              # pipelined time transforms (forward in place, inverse x2 + u -> u)
+              "tfft_pipe_kernel<fwd>": 32, "tfft_pipe_kernel<inv>": 48}
 # direct form (u = C_a^{-1}((C_a - C)u + w)): no read of u, input synthesized from one N-vector
 ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
                      "cols_direct_kernel": 16, "fft2d_rows_kernel<inv>": 32, "tfft_bwd_kernel": 32,
                      "pcr_classes_kernel": 16, "pcr_chunk_kernel": 32, "bwd_kernel": 32,
-                     "spatial2d_kernel": 48}
+                     "spatial2d_kernel": 48, "tfft_pipe_kernel<inv>": 32}
 
 
 def env_rank():

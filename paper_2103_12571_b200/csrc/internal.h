@@ -68,6 +68,7 @@ struct StaticTables {
   // per-pass twiddle tables of the register FFT engine (fft_reg.cuh) for nx, ny
   const double2 *ptwx, *ptwy;
   const double2 *ptwx5, *ptwy5;   // nx / ny plans with radix-32 passes (pipelined plane stages)
+  const double2 *ptwL;            // L plan with radix-32 passes (pipelined time transforms)
   // Frequency units of the 2-D spatial solves: unit q < nsolve solves slot slots[q].  Default:
   // every slot (slots[q] = q), X holds the planes.  Hermitian (packed) mode (real data,
   // pint_set_hermitian): two real spatial points n' and n' + N/2 share one complex time series
@@ -125,6 +126,12 @@ cudaError_t launch_spatial2d(const Geometry &g, const StaticTables &st, const Al
 bool spatial2d_supported(const Geometry &g);
 // Pipelined per-stage plane passes (spatial2d.cu): the default for the grids and
 // modes they serve (2-D, 512..4096 per axis, M <= 4, complex storage)
+// Pipelined 2-D time transforms (spatial2d.cu): forward X in place (residual output -> slot order),
+// inverse x2 -> u (+= or overwrite) with the last-step difference; L = 128 .. 1024, complex storage
+bool tfft_pipe_supported(const Geometry &g, const StaticTables &st);
+cudaError_t launch_tfft_pipe(const Geometry &g, const StaticTables &st, const AlphaTables *at, double2 *X,
+                             const double2 *x2, double2 *u, bool inverse, unsigned long long *diff_slot, int overwrite,
+                             cudaStream_t s);
 bool spatial_pipe_geometry(const Geometry &g);                          // grid/M served (needs a 2nd vector)
 bool spatial_pipe_supported(const Geometry &g, const StaticTables &st);  // ... and the current mode
 // X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector
@@ -154,7 +161,7 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
                                 const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
                                 double2 **out);
 int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc);
-const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, int i);
+const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i);
 // Sequential Radau IIA baseline (2-D, one step): the spectrum of r0 (in place), then the direct-form
 // synthesized spatial pipeline with the Q-eigen tables `at` (sig, shift, SG = V) writing the M
 // stage planes of the step at `out`.

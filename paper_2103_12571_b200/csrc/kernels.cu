@@ -1270,6 +1270,17 @@ static bool legacy_pipe() {   // A/B: the fused persistent spatial2d kernel inst
   }
   return v == 1;
 }
+// The pipelined (TMA ring) time transforms measured slower than the one-tile-per-CTA kernels on
+// config 5 (forward 16.2 vs 14.9 ms, inverse 31.9 vs 21.2 ms: a third of the threads per SM keep
+// fewer u loads in flight); they stay an A/B option (PINT_TFFT_PIPE=1, experiments build).
+static bool legacy_tfft() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_TFFT_PIPE");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
 static bool legacy2d() {
   static int v = -1;
   if (v < 0) {
@@ -1350,9 +1361,19 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
   static const char *k2p[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial2d_kernel", "tfft_bwd_kernel"};
   static const char *k2q[] = {"residual2d_kernel", "tfft_fwd_kernel", "rows_pipe_kernel<fwd>", "cols_pipe_kernel",
                               "rows_pipe_kernel<inv>", "tfft_bwd_kernel"};
+  static const char *k2t[] = {"residual2d_kernel", "tfft_pipe_kernel<fwd>", "rows_pipe_kernel<fwd>", "cols_pipe_kernel",
+                              "rows_pipe_kernel<inv>", "tfft_pipe_kernel<inv>"};
   const int n = launches_per_iteration(g, lc, st);
   if (i < 0 || i >= n) return "";
-  if (g.dim == 2) return pipe2d(g, st) ? k2q[i] : (reg2d(g) ? k2p[i] : k2[i]);
+  if (g.dim == 2) {
+    if (pipe2d(g, st)) return tfft_pipe_supported(g, st) && !legacy_tfft() ? k2t[i] : k2q[i];
+    const char *nm = reg2d(g) ? k2p[i] : k2[i];
+    if (tfft_pipe_supported(g, st) && !legacy_tfft()) {   // time transforms pipelined, spatial legacy
+      if (i == 1) return "tfft_pipe_kernel<fwd>";
+      if (i == n - 1) return "tfft_pipe_kernel<inv>";
+    }
+    return nm;
+  }
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 
@@ -1459,6 +1480,12 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     rec(s);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!pk && tfft_pipe_supported(g, st) && !legacy_tfft()) {   // pipelined (TMA ring) time FFT
+      e = launch_tfft_pipe(g, st, &at, b.X, nullptr, b.u, false, nullptr, 0, s);
+      rec(s);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
     Geometry gt = g;                  // time transform over N (or N/2 packed columns)
     if (pk) gt.N = g.N / 2;
     int T2 = lc.tfft_T;
@@ -1589,6 +1616,8 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
     if (e == cudaSuccess)
       tfft_bwd_kernel<true><<<g.M * (g.N / 2 / T2), kTileThreads, sm2, s>>>(
           g, st, at, unit_planes(g, b.X), b.u, T2, (unsigned long long *)diff_slot, overwrite);
+  } else if (tfft_pipe_supported(g, st) && !legacy_tfft()) {   // pipelined (TMA ring) inverse time FFT
+    e = launch_tfft_pipe(g, st, &at, b.X, x2, b.u, true, (unsigned long long *)diff_slot, overwrite, s);
   } else {
     const int T2 = lc.tfft_T;
     const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
@@ -1607,7 +1636,7 @@ int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc) {
   return lc.pcr_mode == 0 ? 3 : 4;            // r0, pcr (1 or 2), bwd
 }
 
-const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, int i) {
+const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i) {
   static const char *k1a[] = {"direct_r0_kernel", "pcr_classes_kernel", "bwd_kernel"};
   static const char *k1b[] = {"direct_r0_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
   static const char *k2[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel",
@@ -1616,7 +1645,10 @@ const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, int i) {
                               "spatial2d_kernel", "tfft_bwd_kernel"};
   const int n = launches_per_iteration_direct(g, lc);
   if (i < 0 || i >= n) return "";
-  if (g.dim == 2) return reg2d(g) ? k2p[i] : k2[i];
+  if (g.dim == 2) {
+    if (i == n - 1 && tfft_pipe_supported(g, st) && !legacy_tfft()) return "tfft_pipe_kernel<inv>";
+    return reg2d(g) ? k2p[i] : k2[i];
+  }
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 

@@ -146,7 +146,7 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   const int mb = g.dim == 2 ? spatial_maxb(g) : 4;
   L.static_bytes = (size_t)(g.L + g.nx + g.ny + g.nx + g.ny + g.N + g.L + 8 + pass_twiddle_count(g.lognx, mb) +
                             pass_twiddle_count(g.logny, mb) + pass_twiddle_count(g.lognx, 5) +
-                            pass_twiddle_count(g.logny, 5)) * sizeof(double2);
+                            pass_twiddle_count(g.logny, 5) + pass_twiddle_count(g.logL, 5)) * sizeof(double2);
   off = align_up(off + L.static_bytes, 256);
   L.off_alpha = off;
   const size_t LM = (size_t)g.L * g.M;
@@ -335,6 +335,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   };
   size_t o_px5 = o; ptw5(g.lognx);
   size_t o_py5 = o; ptw5(g.logny);
+  size_t o_pL5 = o; ptw5(g.logL);
   double2 *sbase = (double2 *)(c->work + lay.off_static);
   CREATE_TRY(c, cudaMemcpyAsync(sbase, host.data(), o * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
   c->st.twL = sbase + o_twL;
@@ -347,6 +348,7 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
   c->st.ptwy = sbase + o_py;
   c->st.ptwx5 = sbase + o_px5;
   c->st.ptwy5 = sbase + o_py5;
+  c->st.ptwL = sbase + o_pL5;
   c->st.P = P;
   c->st.rank = rank;
   if (P == 1) {
@@ -980,7 +982,7 @@ pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms
 
 const char *pint_kernel_name(pint_ctx *c, int32_t i) {
   if (!c) return "";
-  if (c->form == PINT_FORM_DIRECT) return kernel_name_direct(c->g, c->lc, i);
+  if (c->form == PINT_FORM_DIRECT) return kernel_name_direct(c->g, c->lc, c->st, i);
   return kernel_name(c->g, c->lc, c->st, i);
 }
 

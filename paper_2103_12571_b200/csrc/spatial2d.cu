@@ -576,6 +576,17 @@ constexpr int kBW = 8;   // S-slot columns per block of the blocked spectral lay
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
+// Wait for CTA-local item k in ring slot s = k mod NS.  The slot's previous item k - NS may belong
+// to another group, and item k is only issued once that item is processed: a group that runs
+// ahead must not test item k's phase parity while the barrier still sits in item k - NS's phase
+// (equal parity two phases apart: try_wait.parity would pass at once on stale data).  The issuing
+// thread records the item it put into the slot (slot_item[s]); once that reads k, item k - NS's
+// phase has completed and the barrier's current phase is item k's, so the parity wait is exact.
+__device__ __forceinline__ void ring_wait(uint64_t *bar, volatile int *slot_item, int k, int NS) {
+  while (slot_item[k % NS] != k) __nanosleep(32);
+  mbar_wait(bar, (unsigned)((k / NS) & 1));
+}
+
 // first 1024-byte aligned address (shared window) at or after p
 __device__ __forceinline__ unsigned char *align_smem_1024(unsigned char *p) {
   const unsigned a = smem_u32(p);
@@ -627,6 +638,7 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
   extern __shared__ __align__(1024) unsigned char smraw_[];
   unsigned char *smraw = align_smem_1024(smraw_);   // the launch adds 1 KB of slack
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  volatile int *slot_item = reinterpret_cast<volatile int *>(smraw + 64);   // item held by slot s (ring_wait)
   double2 *twx = reinterpret_cast<double2 *>(smraw + 128);
   double2 *ring = reinterpret_cast<double2 *>(smraw + 1024 + (((size_t)TW * sizeof(double2) + 1023) & ~(size_t)1023));
   const int LINES = YR * MM, GT = LINES * TPL, slot_elems = LINES * NX;
@@ -636,7 +648,10 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
   const int gbar = 1 + (TPL > 32 ? G * LINES : 0) + gid;   // after the line barriers (TPL > 32)
   const int ygroups = g.ny / YR;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      slot_item[s] = -1;
+    }
     mbar_init_fence();
     if (INV) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmi) : "memory");
   }
@@ -661,6 +676,7 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
           bulk_g2s(d, X + ((size_t)p * MM + m) * g.N + ((size_t)(y0 + yy) << PX::LOGN), NX * sizeof(double2), bar);
         }
       }
+    slot_item[k % NS] = k;   // after the barrier's arm (ring_wait)
   };
   if (threadIdx.x == 0)
     for (int k = 0; k < NS; ++k) issue(k);
@@ -674,7 +690,7 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
     const int p = __ldg(st.slots + un);
     double2 *xp = X + (size_t)p * MM * g.N;
     const int yy = l / MM, m = l - yy * MM;
-    mbar_wait(full + s, (unsigned)((k / NS) & 1));
+    ring_wait(full + s, slot_item, k, NS);
     double2 v[E];
     if constexpr (!INV) {
       if constexpr (NODE) {   // x1 = S_p^{-1} x on the natural rows, in place
@@ -753,6 +769,7 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
   extern __shared__ __align__(1024) unsigned char smraw_[];
   unsigned char *smraw = align_smem_1024(smraw_);   // swizzled TMA tiles need 1 KB-aligned slots
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  volatile int *slot_item = reinterpret_cast<volatile int *>(smraw + 64);   // item held by slot s (ring_wait)
   double2 *twy = reinterpret_cast<double2 *>(smraw + 128);
   double2 *lamy = twy + TW;
   double2 *ring = reinterpret_cast<double2 *>(
@@ -765,7 +782,10 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
   const int M = g.M;
   const double inv_n = 1.0 / ((double)NX * (double)NY);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      slot_item[s] = -1;
+    }
     mbar_init_fence();
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmc) : "memory");
   }
@@ -789,6 +809,7 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
     double2 *dst = ring + (size_t)(k % NS) * slot_elems;
     mbar_arrive_expect_tx(bar, (unsigned)(NY * TC * sizeof(double2)));
     for (int b = 0; b < NY; b += BR) tma_load_3d(dst + (size_t)b * TC, &tmc, 2 * TC * half, b, plane * NBLK + blk, bar);
+    slot_item[k % NS] = k;   // after the barrier's arm (ring_wait)
   };
   if (threadIdx.x == 0)
     for (int k = 0; k < NS; ++k) issue(k);
@@ -805,7 +826,7 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
     double2 *xb = Yb + (size_t)q * g.N + ((size_t)blk << (LY + 3)) + half * TC;
     const double2 sh = __ldg(at.shift + q);
     const double2 lx = __ldg(st.lamx + brev(rfft::slot_to_pos<PX>(q0 + c), LX));
-    mbar_wait(full + s, (unsigned)((k / NS) & 1));
+    ring_wait(full + s, slot_item, k, NS);
     double2 v[E];
     // column c, row y of the swizzled TMA tile: 16-byte chunk c ^ ((y TC / 8) mod TC) of row y
 #pragma unroll
@@ -974,6 +995,224 @@ cudaError_t launch_pipe_dispatch(const Geometry &g, const StaticTables &st, cons
                     : launch_pipe<PX4, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Pipelined 2-D time transforms (north star step (ii) and the inverse of (v)): item = one node m
+// and T consecutive points n0.. over all L steps (rows at stride M N).  Tiles arrive by TMA in
+// 128-byte column boxes (8 points x up to 256 steps, 128-byte swizzle: conflict-free column
+// reads), two consumer groups run the register FFT engine on the T columns over a ring of three
+// slots, results leave through the slot in 128-byte row segments.
+//   forward: X[p][m][n] = DIF_L(alpha^{l/L} r_l)[p]  (slot p holds frequency bitrev(p); the scale
+//            was applied by the residual kernel), P > 1: times the four-step twiddle twr[p]
+//   inverse: u[l][m][n] += alpha^{-l/L} / L * DIT_L(x2)[l]  (overwrite: = instead of +=), the
+//            last-step difference, and an L2 prefetch of the u tile when the x2 tile is issued.
+template <class PL, bool INV>
+__global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
+    tfft_pipe_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmu,
+                     const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X,
+                     double2 *__restrict__ u, int lT, int G, int NS, int ls, int nitems,
+                     unsigned long long *diff_slot, int overwrite) {
+  constexpr int NL = PL::N, TPL = PL::TPL, E = PL::E, R = 1 << PL::BL, TW = PL::twsize(), NP = PL::NP;
+  constexpr int LB = NL < 256 ? NL : 256;   // steps per TMA box
+  extern __shared__ __align__(1024) unsigned char smraw_[];
+  unsigned char *smraw = align_smem_1024(smraw_);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  volatile int *slot_item = reinterpret_cast<volatile int *>(smraw + 64);   // item held by slot s (ring_wait)
+  double2 *twl = reinterpret_cast<double2 *>(smraw + 128);
+  double2 *ring = reinterpret_cast<double2 *>(smraw + 1024 + (((size_t)TW * sizeof(double2) + 1023) & ~(size_t)1023));
+  __shared__ double red[16];
+  const int T = 1 << lT, GT = T * TPL;
+  const int tile_elems = NL * T, line_elems = T * ls;
+  const int slot_elems = (((tile_elems > line_elems ? tile_elems : line_elems) * (int)sizeof(double2) + 1023) & ~1023) /
+                         (int)sizeof(double2);
+  const int gid = threadIdx.x / GT, t = threadIdx.x - gid * GT, c = t / TPL, tau = t - c * TPL;
+  const int gbar = 1 + gid, lid = G + gid * T + c;   // line_sync: barrier 1 + lid (TPL > 32)
+  const int per = g.N >> lT;
+  const size_t lstride = (size_t)g.M * g.N;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      slot_item[s] = -1;
+    }
+    mbar_init_fence();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
+  }
+  copy_table(twl, st.ptwL, TW);
+  __syncthreads();
+  auto issue = [&](int k) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= nitems) return;
+    const int m = it / per, n0 = (it - m * per) << lT;
+    uint64_t *bar = full + k % NS;
+    double2 *dst = ring + (size_t)(k % NS) * slot_elems;
+    mbar_arrive_expect_tx(bar, (unsigned)(tile_elems * sizeof(double2)));
+    for (int cb = 0; cb < T; cb += 8)
+      for (int lb = 0; lb < NL; lb += LB) {
+        tma_load_3d(dst + (size_t)cb * NL + lb * 8, &tmx, 2 * (n0 + cb), m, lb, bar);
+        if (INV && !overwrite)   // the epilogue's read of u: start it towards L2 now
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(&tmu),
+                       "r"(2 * (n0 + cb)), "r"(m), "r"(lb)
+                       : "memory");
+      }
+    slot_item[k % NS] = k;   // after the barrier's arm (ring_wait)
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NS; ++k) issue(k);
+  double dmax = 0.0;
+  for (int k = gid;; k += G) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= nitems) break;
+    const int s = k % NS;
+    double2 *tile = ring + (size_t)s * slot_elems;
+    const int m = it / per, n0 = (it - m * per) << lT;
+    // column c of the tile: box c / 8, row l, 16-byte chunk (c mod 8) ^ (l mod 8)
+    const double2 *col = tile + (size_t)(c >> 3) * NL * 8;
+    const int cc = c & 7;
+    double2 *line = tile + (size_t)c * ls;
+    ring_wait(full + s, slot_item, k, NS);
+    double2 v[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int l = rfft::natural_pos<PL>(tau, i);
+      v[i] = col[l * 8 + (cc ^ (l & 7))];
+    }
+    named_sync(gbar, GT);   // the slot becomes T exchange lines of stride ls
+    if constexpr (!INV) {
+      rfft::forward_regs<PL>(v, line, lid, tau, twl);
+      rfft::to_smem<PL, NP - 1>(v, line, tau);
+      named_sync(gbar, GT);
+      double2 *xo = X + (size_t)m * g.N + n0;
+      for (int i = t; i < (NL << lT); i += GT) {
+        const int cq = i & (T - 1), p = i >> lT;
+        double2 w = tile[(size_t)cq * ls + rfft::F<PL>(p)];
+        if (st.twr) w = cmul(w, __ldg(st.twr + p));   // P > 1: four-step twiddle
+        xo[(size_t)p * lstride + cq] = w;
+      }
+    } else {
+      // slot order in, natural steps out: place the values at their swizzled line positions,
+      // re-read them at the last pass's positions, then the inverse transform
+      rfft::to_smem<PL, 0>(v, line, tau);
+      rfft::line_sync<PL>(lid);
+#pragma unroll
+      for (int uu = 0; uu < E / R; ++uu)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int P = rfft::last_pos<PL>(tau, uu, r);
+          double2 w = line[rfft::F<PL>(P)];
+          if (st.twr) w = cmulc(w, __ldg(st.twr + P));   // P > 1: inverse four-step twiddle
+          v[uu * R + r] = w;
+        }
+      rfft::line_sync<PL>(lid);
+      rfft::inverse_in_regs<PL>(v, line, lid, tau, twl);
+      rfft::to_smem<PL, 0>(v, line, tau);
+      named_sync(gbar, GT);
+      double2 *ub = u + (size_t)m * g.N + n0;
+      constexpr int kB = 8;   // u loads in flight per thread
+      for (int b0 = t; b0 < (NL << lT); b0 += kB * GT) {
+        double2 uo[kB];
+#pragma unroll
+        for (int q = 0; q < kB; ++q) {
+          const int i = b0 + q * GT;
+          if (i < (NL << lT)) {
+            const int l = i >> lT;
+            const bool need_old = !overwrite || (diff_slot && l == NL - 1);
+            uo[q] = need_old ? ub[(size_t)l * lstride + (i & (T - 1))] : make_double2(0.0, 0.0);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kB; ++q) {
+          const int i = b0 + q * GT;
+          if (i < (NL << lT)) {
+            const int cq = i & (T - 1), l = i >> lT;
+            const double2 cv = cscale(tile[(size_t)cq * ls + rfft::F<PL>(l)], __ldg(at.scale_bwd + l));
+            ub[(size_t)l * lstride + cq] = overwrite ? cv : cadd(uo[q], cv);
+            if (l == NL - 1) {
+              const double2 dd = overwrite ? csub(cv, uo[q]) : cv;
+              dmax = nanmax(dmax, hypot(dd.x, dd.y));
+            }
+          }
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    named_sync(gbar, GT);
+    if (t == 0) issue(k + NS);
+  }
+  if (INV && diff_slot) {
+    for (int o = 16; o > 0; o >>= 1) dmax = nanmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double vmax = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) vmax = nanmax(vmax, red[w]);
+      atomicMax(diff_slot, (unsigned long long)__double_as_longlong(vmax));
+    }
+  }
+}
+
+struct TfftPlan {
+  int lT, G, NS, ls;
+  size_t smem;
+};
+
+template <class PL>
+bool tfft_plan(const Geometry &g, TfftPlan &tp) {
+  // T points per item: 64 KB tiles (L T 16 bytes), 8 <= T <= 64, 128 threads per group (E = 32)
+  // or 256 (E = 16); two groups, three slots
+  int T = (64 * 1024) / (16 * PL::N);
+  if (T > 64) T = 64;
+  if (T < 8 || g.N % T) return false;
+  tp.lT = 31 - __builtin_clz((unsigned)T);
+  tp.G = 2;
+  tp.NS = 3;
+  tp.ls = PL::N + 2;
+  if (T * PL::TPL > 256) return false;
+  if (PL::TPL > 32 && tp.G * T + tp.G + 1 > 16) return false;   // named barrier ids
+  const size_t tile = (size_t)PL::N * T * 16, lines = (size_t)T * tp.ls * 16;
+  const size_t slot = ((tile > lines ? tile : lines) + 1023) & ~(size_t)1023;
+  tp.smem = 1024 + 1024 + (((size_t)PL::twsize() * 16 + 1023) & ~(size_t)1023) + tp.NS * slot;
+  return tp.smem <= 227 * 1024;
+}
+
+// 3-D map over X[l][m][n] as doubles {2N, M, L}, box {16 doubles (8 points), 1 node, min(L, 256)}
+bool time_map(const Geometry &g, double2 *base, CUtensorMap &tm) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * g.N, (cuuint64_t)g.M, (cuuint64_t)g.L};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.N * 16, (cuuint64_t)g.M * g.N * 16};
+  const cuuint32_t box[3] = {16, 1, (cuuint32_t)(g.L < 256 ? g.L : 256)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int LL>
+cudaError_t launch_tfft_l(const Geometry &g, const StaticTables &st, const AlphaTables *at, double2 *X,
+                          const double2 *x2, double2 *u, bool inverse, unsigned long long *diff_slot, int overwrite,
+                          cudaStream_t s) {
+  using PL = rfft::Plan<LL, 5>;
+  TfftPlan tp;
+  if (!tfft_plan<PL>(g, tp)) return cudaErrorInvalidValue;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUtensorMap tmx, tmu;
+  if (!time_map(g, inverse ? (double2 *)x2 : X, tmx) || !time_map(g, u, tmu)) return cudaErrorNotSupported;
+  const void *fn = inverse ? (const void *)tfft_pipe_kernel<PL, true> : (const void *)tfft_pipe_kernel<PL, false>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp.smem);
+  if (e != cudaSuccess) return e;
+  const int threads = tp.G * (1 << tp.lT) * PL::TPL;
+  const int nitems = g.M * (g.N >> tp.lT);
+  AlphaTables a = at ? *at : AlphaTables{};
+  if (inverse)
+    tfft_pipe_kernel<PL, true><<<sms, threads, tp.smem, s>>>(tmx, tmu, g, st, a, X, u, tp.lT, tp.G, tp.NS, tp.ls,
+                                                             nitems, diff_slot, overwrite);
+  else
+    tfft_pipe_kernel<PL, false><<<sms, threads, tp.smem, s>>>(tmx, tmu, g, st, a, X, u, tp.lT, tp.G, tp.NS, tp.ls,
+                                                              nitems, nullptr, 0);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool spatial_pipe_geometry(const Geometry &g) {
@@ -997,6 +1236,29 @@ cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const
 #undef PINT_PIPE_M
 #undef PINT_PIPE
   return cudaErrorInvalidValue;
+}
+
+bool tfft_pipe_supported(const Geometry &g, const StaticTables &st) {
+  if (g.dim != 2 || st.packed || g.logL < 7 || g.logL > 10) return false;
+  TfftPlan tp;
+  switch (g.logL) {
+    case 7: return tfft_plan<rfft::Plan<7, 5>>(g, tp);
+    case 8: return tfft_plan<rfft::Plan<8, 5>>(g, tp);
+    case 9: return tfft_plan<rfft::Plan<9, 5>>(g, tp);
+    default: return tfft_plan<rfft::Plan<10, 5>>(g, tp);
+  }
+}
+
+cudaError_t launch_tfft_pipe(const Geometry &g, const StaticTables &st, const AlphaTables *at, double2 *X,
+                             const double2 *x2, double2 *u, bool inverse, unsigned long long *diff_slot, int overwrite,
+                             cudaStream_t s) {
+  switch (g.logL) {
+    case 7: return launch_tfft_l<7>(g, st, at, X, x2, u, inverse, diff_slot, overwrite, s);
+    case 8: return launch_tfft_l<8>(g, st, at, X, x2, u, inverse, diff_slot, overwrite, s);
+    case 9: return launch_tfft_l<9>(g, st, at, X, x2, u, inverse, diff_slot, overwrite, s);
+    case 10: return launch_tfft_l<10>(g, st, at, X, x2, u, inverse, diff_slot, overwrite, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace pint
