@@ -138,10 +138,10 @@ def cpu_oracle_rate(p, target_s: float, seed: int = 0):
     def run(nmodes):
         kx = rng.integers(0, p.nx, nmodes)
         ky = rng.integers(0, p.ny, nmodes)
-        uh0 = mode_coefficients(p, u0, kx, ky)       # setup (projection of u0), not timed
+        t0 = time.perf_counter()
+        uh0 = mode_coefficients(p, u0, kx, ky)       # the spatial projection of u0 (timed too)
         mo = ModeOracle(p, uh0, kx, ky)
         uh = mo.initial()
-        t0 = time.perf_counter()
         mo.iterate(uh, a)
         return time.perf_counter() - t0
 
@@ -151,7 +151,29 @@ def cpu_oracle_rate(p, target_s: float, seed: int = 0):
         n = min(p.N, n * 4)
         dt = run(n)
     rate = p.L * p.M * n / dt
-    return rate, f"{n} of {p.N} spatial Fourier modes x all L*M={p.L * p.M} (one iteration, ModeOracle)", dt
+    return rate, (f"{n} of {p.N} spatial Fourier modes x all L*M={p.L * p.M} (one iteration, ModeOracle, "
+                  f"projection of u0 onto the sampled modes included)"), dt
+
+
+def host_info():
+    """CPU model and the BLAS numpy uses (for the cpu_baseline record)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        libs = [f"{i.get('internal_api')} {i.get('version')} ({i.get('num_threads')} threads)"
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+        blas = "; ".join(libs) or None
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas": blas, "host_cores": len(os.sched_getaffinity(0))}
 
 
 def threads_used():
@@ -181,7 +203,8 @@ def run_reference(args, p, rank, world):
             "data": "synthetic (workloads.py seeded generators)", "impl": "reference",
             "config": {"workload": p.name, "cfg": args.config, "L": p.L, "M": p.M, "N": p.N,
                        "unknowns": p.U},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             **host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
 
@@ -203,6 +226,7 @@ def main():
     ap.add_argument("--no-sequential", action="store_true", help="skip the sequential Radau IIA baseline")
     ap.add_argument("--hermitian", action="store_true",
                     help="real-data fast path (SURVEY 8(f) row 1): solve only frequencies k <= L/2")
+    ap.add_argument("--graph", action="store_true", help="also time CUDA-graph replays (fixed-alpha configs)")
     ap.add_argument("--allow-experiments", action="store_true",
                     help="A/B only: accept a library built with -DPINT_EXPERIMENTS (PINT_LIBRARY)")
     args = ap.parse_args()
@@ -247,7 +271,8 @@ def main():
         from paper_2103_12571_b200.distributed import sharded_solver
         s = sharded_solver(p, u0, device=local)
     else:
-        s = P.Solver(p, u0, device=local)
+        # a dedicated (non-default) stream: the CUDA-graph leg captures the library's launches on it
+        s = P.Solver(p, u0, device=local, stream=torch.cuda.Stream(device=local))
     if args.form != "correction":
         s.set_form(args.form)
     if args.hermitian:
@@ -263,17 +288,35 @@ def main():
         s.iterate(1)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def roll(seconds):
+        """Untimed iterations of the same workload for `seconds` (clock window of short regions)."""
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end:
+            s.set_alpha_schedule(schedule_for(p, w_inf, 8))
+            s.iterate(8)
+            torch.cuda.synchronize()
+
     with ClockSampler(local) as clk:
+        # a timed region shorter than the sampler's period cannot be sampled alone: then the window
+        # is the timed region plus 0.5 s of the same iterations before and after (recorded below)
+        short = p.U < 1e9
+        if short:
+            roll(0.5)
+            s.set_alpha_schedule(schedule_for(p, w_inf, min(64, args.steps)))
+            barrier()
         ev0.record(stream)
         done = 0
         while done < args.steps:
-            n = min(args.steps - done, 64 - args.warmup if done == 0 else 64)
+            n = min(args.steps - done, (64 - args.warmup if not short else 64) if done == 0 else 64)
             if done > 0:
                 s.set_alpha_schedule(schedule_for(p, w_inf, n))  # only for K > 61 (host work, re-timed)
             s.iterate(n)
             done += n
         ev1.record(stream)
         torch.cuda.synchronize()
+        if short:
+            roll(0.5)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     value = p.U / (ms * 1e-3)          # the whole problem (all ranks together) per iteration
@@ -325,6 +368,30 @@ def main():
                     "kernel_share_of_step": float(kms[top] / kms.sum()),
                     "per_kernel_ms": {n_: float(v) for n_, v in zip(names, kms)},
                     "iteration": iteration_roof}
+
+    # ---- launch-bound configs: the same iteration replayed from a CUDA graph (fixed alpha) ---------
+    graph = None
+    if world == 1 and (args.graph or (p.alpha_mode == "fixed" and ms < 1.0)) and p.alpha_mode == "fixed":
+        ng = 16
+        s.set_alpha_schedule(schedule_for(p, w_inf, 64))
+        s.iterate(1)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            s.iterate(ng)                    # ng iterations captured on the library's stream
+        reps = max(3, args.steps)
+        gr.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(reps):
+            gr.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gus = g0.elapsed_time(g1) * 1e3 / (reps * ng)
+        graph = {"us_per_iteration": gus, "value": p.U / (gus * 1e-6), "unit": UNIT, "iterations_per_graph": ng,
+                 "replays": reps, "what": "pint_iterate x16 captured in one CUDA graph on the library stream "
+                 "(fixed alpha: every replay is the same iterations), device-timed replays"}
 
     # ---- end to end through the public API with host buffers -----------------------------------
     e2e = None
@@ -384,7 +451,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample, _ = cpu_oracle_rate(p, target_s=args.cpu_target_s)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads_used(), "kind": "oracle", "sample": sample}
+        cpu = {"value": rate, "unit": UNIT, "cores": threads_used(), "kind": "oracle", "sample": sample, **host_info()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -400,7 +467,10 @@ def main():
                            "parallelism": "single GPU" if world == 1 else
                            f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sequential_baseline": seq,
-                "gpu_launches": (nlaunch if world == 1 else nlaunch + 3) * args.steps, "clocks": clk.summary()}
+                "gpu_launches": (nlaunch if world == 1 else nlaunch + 3) * args.steps,
+                "clocks": {**clk.summary(), "window": ("timed region +- 0.5 s of the same iterations"
+                                                       if p.U < 1e9 else "timed region")},
+                "graph": graph}
         print(json.dumps(line), flush=True)
     s.close()
     if dist is not None:

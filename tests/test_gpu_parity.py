@@ -192,7 +192,7 @@ PIPE_CASES = [
     W.CONFIGS[4].replace(name="pipe_512sq_M3_L8", L=8, iters=3),
     W.CONFIGS[5].replace(name="pipe_1024x512_M2_L4", ny=512, M=2, L=4, iters=3),
     W.CONFIGS[4].replace(name="pipe_512x1024_M1_L8", ny=1024, M=1, L=8, iters=3),
-    W.CONFIGS[5].replace(name="pipe_2048x1024_heat_M2_L2", nx=2048, op="heat", nu=1e-2, M=2, L=2, iters=2),
+    W.CONFIGS[5].replace(name="pipe_2048x1024_heat_M2_L4", nx=2048, op="heat", nu=1e-2, M=2, L=4, iters=2),
 ]
 
 
