@@ -376,22 +376,21 @@ def main():
         s.set_alpha_schedule(schedule_for(p, w_inf, 64))
         s.iterate(1)
         torch.cuda.synchronize()
-        gr = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gr, stream=stream):
-            s.iterate(ng)                    # ng iterations captured on the library's stream
+        gr = s.graph_create(ng)              # ng iterations captured by the library on its stream
         reps = max(3, args.steps)
-        gr.replay()
+        s.graph_launch(gr)
         torch.cuda.synchronize()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         for _ in range(reps):
-            gr.replay()
+            s.graph_launch(gr)
         g1.record(stream)
         torch.cuda.synchronize()
+        s.graph_destroy(gr)
         gus = g0.elapsed_time(g1) * 1e3 / (reps * ng)
         graph = {"us_per_iteration": gus, "value": p.U / (gus * 1e-6), "unit": UNIT, "iterations_per_graph": ng,
-                 "replays": reps, "what": "pint_iterate x16 captured in one CUDA graph on the library stream "
-                 "(fixed alpha: every replay is the same iterations), device-timed replays"}
+                 "replays": reps, "what": "16 iterations captured in one CUDA graph by pint_graph_create on the library stream "
+                 "(fixed alpha: every replay is 16 more iterations), device-timed replays"}
 
     # ---- end to end through the public API with host buffers -----------------------------------
     e2e = None

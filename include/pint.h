@@ -209,6 +209,17 @@ pint_status pint_sequential(pint_ctx *c);
 pint_status pint_solve(pint_ctx *c, double m0, double eps, double tau, double tol, int32_t max_iter,
                        int32_t *iters, double *diffs, double *m_out, int32_t *stop_reason);
 
+/* CUDA-graph form of pint_iterate for launch-bound problems (configs 1-2: a few microseconds of
+ * kernels per iteration).  pint_graph_create captures n_iter iterations k, k+1, ... (alpha_k from
+ * the schedule; advances k by n_iter like pint_iterate) into one executable graph on the context
+ * stream; every pint_graph_launch replays exactly those iterations on the current buffers (with
+ * the alphas captured: a fixed-alpha schedule makes each replay n_iter further iterations).
+ * No last-step difference is produced.  One rank only.  The caller owns the graph
+ * (pint_graph_destroy).  Errors: PINT_ERR_INVALID, PINT_ERR_SCHEDULE, PINT_ERR_CUDA. */
+pint_status pint_graph_create(pint_ctx *c, int32_t n_iter, void **graph_exec);
+pint_status pint_graph_launch(pint_ctx *c, void *graph_exec);
+pint_status pint_graph_destroy(void *graph_exec);
+
 /* Enqueues n_iter iterations k, k+1, ... with alpha_k from the schedule.  last_step_diff_inf:
  * nullable; if given, n_iter doubles receive ||u_{L-1}^{k+1} - u_{L-1}^{k}||_inf (Alg. 2 line 7,
  * P:421) and the call synchronises the stream; a non-finite difference (diverged or NaN iterate:

@@ -947,6 +947,49 @@ pint_status pint_destroy(pint_ctx *c) {
   return PINT_OK;
 }
 
+pint_status pint_graph_create(pint_ctx *c, int32_t n_iter, void **graph_exec) {
+  if (!c || !graph_exec || n_iter < 1) return fail(PINT_ERR_INVALID, "NULL argument or n_iter < 1");
+  BIND_DEVICE(c);
+  *graph_exec = nullptr;
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  if (c->P > 1) return fail(PINT_ERR_INVALID, "graph capture: one rank (the NCCL calls are not captured here)");
+  if (c->k + n_iter > (int)c->alphas.size())
+    return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
+  cudaGraph_t graph = nullptr;
+  CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  pint_status st = PINT_OK;
+  for (int i = 0; i < n_iter && st == PINT_OK; ++i) {
+    st = run_iteration(c, c->k, nullptr);
+    if (st == PINT_OK) c->k++;
+  }
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (st != PINT_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) { c->poisoned = true; return fail(PINT_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e)); }
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiate(&ex, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(PINT_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  *graph_exec = (void *)ex;
+  return PINT_OK;
+}
+
+pint_status pint_graph_launch(pint_ctx *c, void *graph_exec) {
+  if (!c || !graph_exec) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
+  if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
+  CUDA_TRY(c, cudaGraphLaunch((cudaGraphExec_t)graph_exec, c->stream));
+  return PINT_OK;
+}
+
+pint_status pint_graph_destroy(void *graph_exec) {
+  if (graph_exec && cudaGraphExecDestroy((cudaGraphExec_t)graph_exec) != cudaSuccess)
+    return fail(PINT_ERR_CUDA, "cudaGraphExecDestroy failed");
+  return PINT_OK;
+}
+
 pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms) {
   if (!c || !kernel_ms) return fail(PINT_ERR_INVALID, "NULL argument");
   BIND_DEVICE(c);

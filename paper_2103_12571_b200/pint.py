@@ -31,7 +31,8 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_debug_stage", "pint_debug_get_work", "pint_iterate_profiled", "pint_kernel_name",
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
            "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential", "pint_set_forcing",
-           "pint_next_window", "pint_experiments_enabled"]
+           "pint_next_window", "pint_experiments_enabled", "pint_graph_create", "pint_graph_launch",
+           "pint_graph_destroy"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -100,6 +101,9 @@ def load_library(path: str = LIB_PATH):
         "pint_sequential": (i32, [vp]),
         "pint_set_forcing": (i32, [vp, vp]),
         "pint_next_window": (i32, [vp]),
+        "pint_graph_create": (i32, [vp, i32, ctypes.POINTER(vp)]),
+        "pint_graph_launch": (i32, [vp, vp]),
+        "pint_graph_destroy": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -254,6 +258,18 @@ class Solver:
             return d
         _check(self.lib.pint_iterate(self.ctx, n, None))
         return None
+
+    def graph_create(self, n: int):
+        """Capture n iterations into a CUDA graph (launch-bound problems); returns a handle."""
+        h = ctypes.c_void_p()
+        _check(self.lib.pint_graph_create(self.ctx, n, ctypes.byref(h)))
+        return h
+
+    def graph_launch(self, h):
+        _check(self.lib.pint_graph_launch(self.ctx, h))
+
+    def graph_destroy(self, h):
+        _check(self.lib.pint_graph_destroy(h))
 
     def residual_norm(self):
         a, b = ctypes.c_double(), ctypes.c_double()
