@@ -3,7 +3,7 @@
 Periodic grid x_j = j/n on [0,1) (2-D: n = y*nx + x); 2-D sums the two axes.
 reading for the configs, plus the paper's other discretisations (P:751-799, SURVEY §8(f) row 3;
 DESIGN.md reading R14): centred differences of order kappa = 2, 4, 6 for the second derivative
-and upwind differences of order 1, 3, 5 for the first derivative.
+and upwind differences of order 1, 2, 3, 4, 5 for the first derivative.
   heat  (kappa):   (A u)_j = nu n^2 sum_s d2[s] u_{j+s}
   advection:       (A u)_j = -c n/2 (u_{j+1} - u_{j-1})                      (centred, kappa 2)
   upwind (kappa):  (A u)_j = -c n sum_s d1[s] u_{j+s},  d1 biased against the flow (c > 0: left)
@@ -11,6 +11,10 @@ Stencil weights (exact rationals):
   d2, kappa 2: (1, -2, 1);  4: (-1/12, 4/3, -5/2, 4/3, -1/12);  6: (1/90, -3/20, 3/2, -49/18, ...)
   d1 (c > 0), kappa 1: {-1: -1, 0: 1};  3: (u_{j-2} - 6u_{j-1} + 3u_j + 2u_{j+1})/6;
               5: (-2u_{j-3} + 15u_{j-2} - 60u_{j-1} + 20u_j + 30u_{j+1} - 3u_{j+2})/60;  c < 0: mirrored.
+  Table 1 also lists upwind kappa = 2 and 4 without printing them (DESIGN.md reading
+  R16): the unique (kappa+1)-point stencils of order kappa on the offsets -(kappa/2 + 1) ..
+  kappa/2 - 1 (one point more upwind than downwind, as for the odd orders):
+              2: (u_{j-2} - 4u_{j-1} + 3u_j)/2;  4: (-u_{j-3} + 6u_{j-2} - 18u_{j-1} + 10u_j + 3u_{j+1})/12.
 Fourier symbols (A e^{2 pi i k j/n} = lambda(k) e^{2 pi i k j/n}) in cancellation-free forms
 (SURVEY §8(c) C6): with theta = 2 pi k/n (index reduced mod n),
   symmetric d2:  lambda = -4 nu n^2 sum_{s>=1} d2[s] sin^2(s theta/2)
@@ -26,10 +30,12 @@ D2 = {2: {-1: 1.0, 0: -2.0, 1: 1.0},
       4: {-2: -1 / 12, -1: 4 / 3, 0: -5 / 2, 1: 4 / 3, 2: -1 / 12},
       6: {-3: 1 / 90, -2: -3 / 20, -1: 3 / 2, 0: -49 / 18, 1: 3 / 2, 2: -3 / 20, 3: 1 / 90}}
 D1_LEFT = {1: {-1: -1.0, 0: 1.0},
+           2: {-2: 1 / 2, -1: -2.0, 0: 3 / 2},
            3: {-2: 1 / 6, -1: -1.0, 0: 1 / 2, 1: 1 / 3},
+           4: {-3: -1 / 12, -2: 1 / 2, -1: -3 / 2, 0: 5 / 6, 1: 1 / 4},
            5: {-3: -2 / 60, -2: 15 / 60, -1: -60 / 60, 0: 20 / 60, 1: 30 / 60, 2: -3 / 60}}
 HEAT_OPS = {"heat": 2, "heat4": 4, "heat6": 6}
-UPWIND_OPS = {"upwind1": 1, "upwind3": 3, "upwind5": 5}
+UPWIND_OPS = {"upwind1": 1, "upwind2": 2, "upwind3": 3, "upwind4": 4, "upwind5": 5}
 
 
 def axis_stencil(op: str, n: int, coef: float) -> dict:

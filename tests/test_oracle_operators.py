@@ -14,7 +14,7 @@ SMALL = [
 # the paper's other discretisations: centred kappa 4, 6 and upwind 1, 3, 5 (both flow signs)
 SMALL += [W.Problem(op + ("_2d" if d == 2 else ""), d, 16, 8 if d == 2 else 1, op, 0.4,
                     1.1 if op != "heat4" else 0, -0.6 if d == 2 else 0, 1, 2, 1, "random", "fixed", 0.1, 1)
-          for op in ("heat4", "heat6", "upwind1", "upwind3", "upwind5") for d in (1, 2)]
+          for op in ("heat4", "heat6", "upwind1", "upwind2", "upwind3", "upwind4", "upwind5") for d in (1, 2)]
 SMALL += [W.Problem("up3_neg", 1, 16, 1, "upwind3", 0, -0.8, 0, 1, 2, 1, "random", "fixed", 0.1, 1)]
 
 
@@ -63,7 +63,8 @@ def test_heat_symbol_is_nonpositive_and_advection_imaginary():
 
 
 @pytest.mark.parametrize("op,order", [("heat", 2), ("heat4", 4), ("heat6", 6), ("advection", 2),
-                                      ("upwind1", 1), ("upwind3", 3), ("upwind5", 5)])
+                                      ("upwind1", 1), ("upwind2", 2), ("upwind3", 3), ("upwind4", 4),
+                                      ("upwind5", 5)])
 @pytest.mark.parametrize("sign", [1.0, -1.0])
 def test_consistency_order(op, order, sign):
     """A applied to sin(2 pi x) (+ 0.5 cos(4 pi x)) approaches nu u'' (heat) or -c u' (advection,
@@ -85,7 +86,7 @@ def test_consistency_order(op, order, sign):
 def test_upwind_damps_and_centred_heat_is_real():
     """Upwind symbols have Re lambda <= 0 (dissipative, flow-sign independent); centred heat symbols
     of every order are real and non-positive."""
-    for op in ("upwind1", "upwind3", "upwind5"):
+    for op in ("upwind1", "upwind2", "upwind3", "upwind4", "upwind5"):
         for c in (1.0, -1.0):
             p = W.Problem("u", 2, 16, 8, op, 0, c, 0.5 * c, 1, 2, 1, "random", "fixed", 0.1, 1)
             assert np.all(symbol_grid(p).real <= 1e-12)
