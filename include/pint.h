@@ -27,6 +27,8 @@
  *   PINT_OP_HEAT4/6:    nu * centred second differences of order 4 / 6 (5- / 7-point)
  *   PINT_OP_UPWIND1/3/5: -(cx d/dx + cy d/dy) by upwind-biased first differences of order 1/3/5
  *                        (offsets -(k+1)/2 .. (k-1)/2 for c > 0, mirrored per axis for c < 0)
+ *   PINT_OP_UPWIND2/4:   the same with order 2 / 4 (Table 1), offsets -(k/2+1) .. k/2-1
+ *                        (reading R16: one point more upwind than downwind)
  * 1-D solves (I - s A) by PCR on the tridiagonal factors of I - s A (the 3-point operators are
  * one factor; wider stencils are factored on the host per (alpha, k, m); pint_set_alpha_schedule
  * fails with PINT_ERR_NUMERIC if a factor cannot be formed).  2-D solves are diagonal in Fourier.
@@ -80,7 +82,9 @@ typedef enum {
   PINT_OP_HEAT6 = 3,
   PINT_OP_UPWIND1 = 4,
   PINT_OP_UPWIND3 = 5,
-  PINT_OP_UPWIND5 = 6
+  PINT_OP_UPWIND5 = 6,
+  PINT_OP_UPWIND2 = 7,
+  PINT_OP_UPWIND4 = 8
 } pint_op;
 
 typedef struct {

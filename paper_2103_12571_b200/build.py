@@ -15,8 +15,8 @@ LIB = os.path.join(HERE, "libpint.so")
 # A/B experiment library (-DPINT_EXPERIMENTS: reads the PINT_* switches of internal.h); never the
 # product: bench.py refuses it unless --allow-experiments, and records it
 LIB_EXP = os.path.join(HERE, "libpint_exp.so")
-SOURCES = ["kernels.cu", "spatial2d.cu", "pint_abi.cpp", "host_numerics.cpp"]
-HEADERS = ["internal.h", "host_numerics.h", "fft_reg.cuh", "device_common.cuh"]
+SOURCES = ["kernels.cu", "spatial2d.cu", "generic.cu", "pint_abi.cpp", "host_numerics.cpp"]
+HEADERS = ["internal.h", "host_numerics.h", "fft_reg.cuh", "device_common.cuh", "residual.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 LIBS = ["-lnccl"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

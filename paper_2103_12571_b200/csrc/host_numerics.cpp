@@ -337,20 +337,29 @@ size_t pass_twiddle_count(int logn, int maxb) {
 
 // ---------------------------------------------------------------------------------------------
 // Spatial operators.  Centred second differences of order 2, 4, 6 and upwind-biased first
-// differences of order 1, 3, 5 (c > 0; mirrored for c < 0); exact rational weights.
+// differences of order 1 .. 5 (c > 0; mirrored for c < 0); exact rational weights.
 
 static const ld kD2[3][4] = {{-2.0L, 1.0L, 0, 0},                                   // kappa 2: d_0, d_1
                              {-5.0L / 2, 4.0L / 3, -1.0L / 12, 0},                  // kappa 4
                              {-49.0L / 18, 3.0L / 2, -3.0L / 20, 1.0L / 90}};       // kappa 6
-// upwind (c > 0): offsets -3 .. 2 at index o + 3
-static const ld kD1[3][6] = {{0, 0, -1.0L, 1.0L, 0, 0},
+// upwind (c > 0): offsets -3 .. 2 at index o + 3; orders 1, 3, 5 on -(k+1)/2 .. (k-1)/2 and the
+// even orders 2, 4 of Table 1 on -(k/2+1) .. k/2-1 (reading R16)
+static const ld kD1[5][6] = {{0, 0, -1.0L, 1.0L, 0, 0},
+                             {0, 1.0L / 2, -2.0L, 3.0L / 2, 0, 0},
                              {0, 1.0L / 6, -1.0L, 1.0L / 2, 1.0L / 3, 0},
+                             {-1.0L / 12, 1.0L / 2, -3.0L / 2, 5.0L / 6, 1.0L / 4, 0},
                              {-2.0L / 60, 15.0L / 60, -1.0L, 20.0L / 60, 30.0L / 60, -3.0L / 60}};
 
 bool op_is_heat(int op) { return op == PINT_OP_HEAT || op == PINT_OP_HEAT4 || op == PINT_OP_HEAT6; }
 
 static int heat_row(int op) { return op == PINT_OP_HEAT ? 0 : op == PINT_OP_HEAT4 ? 1 : 2; }
-static int upwind_row(int op) { return op == PINT_OP_UPWIND1 ? 0 : op == PINT_OP_UPWIND3 ? 1 : 2; }
+static bool op_is_upwind(int op) {
+  return op == PINT_OP_UPWIND1 || op == PINT_OP_UPWIND2 || op == PINT_OP_UPWIND3 || op == PINT_OP_UPWIND4 ||
+         op == PINT_OP_UPWIND5;
+}
+static int upwind_row(int op) {
+  return op == PINT_OP_UPWIND1 ? 0 : op == PINT_OP_UPWIND2 ? 1 : op == PINT_OP_UPWIND3 ? 2 : op == PINT_OP_UPWIND4 ? 3 : 4;
+}
 
 bool axis_stencil(int op, long long n, ld coef, AxisStencil &st) {
   st = AxisStencil{};
@@ -367,7 +376,7 @@ bool axis_stencil(int op, long long n, ld coef, AxisStencil &st) {
     st.w[4] = -coef * nn / 2;
     return true;
   }
-  if (op == PINT_OP_UPWIND1 || op == PINT_OP_UPWIND3 || op == PINT_OP_UPWIND5) {
+  if (op_is_upwind(op)) {
     const ld *d = kD1[upwind_row(op)];
     const bool mirror = coef < 0;
     st.h0 = st.h1 = 3;

@@ -43,6 +43,7 @@ struct Geometry {
   int hx0, hx1, hy0, hy1, hw;
   double wx[7], wy[7];
   int nfac;                   // 1-D: tridiagonal factors of I - s A solved by PCR (1..3)
+  int pow2;                   // 1: power-of-two grid; 0: 7-smooth grid on the generic path (log2 fields 0)
   double dTQ[8 * 8];          // dT * Q, row-major
 };
 
@@ -132,6 +133,15 @@ bool tfft_pipe_supported(const Geometry &g, const StaticTables &st);
 cudaError_t launch_tfft_pipe(const Geometry &g, const StaticTables &st, const AlphaTables *at, double2 *X,
                              const double2 *x2, double2 *u, bool inverse, unsigned long long *diff_slot, int overwrite,
                              cudaStream_t s);
+// Generic-grid path (generic.cu): 7-smooth, non-power-of-two nx / ny (Tables 1-2), one rank,
+// correction form; the residual and the spatial solves (node transforms included)
+bool grid_is_smooth(long long n);
+int generic_launches(const Geometry &g);
+const char *generic_kernel_name(const Geometry &g, int i);
+cudaError_t launch_generic_residual(const Geometry &g, const StaticTables &st, const AlphaTables &at,
+                                    const double2 *u, double2 *X, cudaStream_t s);
+cudaError_t launch_generic_solve(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                                 cudaStream_t s);
 bool spatial_pipe_geometry(const Geometry &g);                          // grid/M served (needs a 2nd vector)
 bool spatial_pipe_supported(const Geometry &g, const StaticTables &st);  // ... and the current mode
 // X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector

@@ -20,76 +20,13 @@
 
 #include "device_common.cuh"
 #include "internal.h"
+#include "residual.cuh"   // residual_point (shared with generic.cu)
 
 namespace pint {
 
 // ---------------------------------------------------------------------------------------------
 // residual of one (l, n) for all nodes: r_m = w_m - u_m + dT sum_j Q_mj (A u_j) + u_{l-1, M-1}
 // (C = I_L (x) C_coll + E (x) H; w_0 = u0 replicated, w_{l>0} = 0 since b == 0)
-
-// H-term source (last node of the previous global step) of local step l at point n
-__device__ __forceinline__ double2 prev_value(const StaticTables &st, int l, int n) {
-  const int jj = l - st.prev_shift;
-  return jj < 0 ? __ldg(st.u0 + n) : __ldg(st.prev_base + (long long)jj * st.prev_stride + n);
-}
-
-// Hermitian (packed) mode stores the iterate as real fp64 u[l][m][n] in the first L M N doubles
-// of u_dev (its imaginary parts are zero in exact arithmetic)
-__device__ __forceinline__ double2 u_at(const double2 *__restrict__ u, size_t i, bool real) {
-  return real ? make_double2(__ldg((const double *)u + i), 0.0) : __ldg(u + i);
-}
-
-template <int M, bool REAL = false, int HW = 3>
-__device__ __forceinline__ void residual_point(const Geometry &g, const StaticTables &st,
-                                               const double2 *__restrict__ u, int l, int n, double2 r[M]) {
-  constexpr bool real = REAL;   // Hermitian mode: real storage (st.packed)
-  const size_t plane = (size_t)M * g.N;
-  const size_t ul = (size_t)l * plane;
-  const int x = n & (g.nx - 1);
-  const int y = n >> g.lognx;
-  const int row = y << g.lognx;
-  double2 uc[M], Au[M];
-#pragma unroll
-  for (int j = 0; j < M; ++j) {
-    const size_t uj = ul + (size_t)j * g.N;
-    const double2 c = u_at(u, uj + n, real);
-    uc[j] = c;
-    double2 s = make_double2(g.wx[3] * c.x, g.wx[3] * c.y);
-    // unrolled over the halo HW (1: the 3-point operators, whose missing offsets carry weight 0;
-    // 3: any stencil, offsets outside [-h0, h1] skipped by uniform predicates)
-#pragma unroll
-    for (int o = -HW; o <= HW; ++o) {
-      if (o == 0 || (HW > 1 && (o < -g.hx0 || o > g.hx1))) continue;
-      const double2 v = u_at(u, uj + row + ((x + o) & (g.nx - 1)), real);
-      s.x = fma(g.wx[3 + o], v.x, s.x);
-      s.y = fma(g.wx[3 + o], v.y, s.y);
-    }
-    if (g.dim == 2) {
-#pragma unroll
-      for (int o = -HW; o <= HW; ++o) {
-        if (o == 0 || (HW > 1 && (o < -g.hy0 || o > g.hy1))) continue;
-        const double2 v = u_at(u, uj + ((((y + o) & (g.ny - 1)) << g.lognx) + x), real);
-        s.x = fma(g.wy[3 + o], v.x, s.x);
-        s.y = fma(g.wy[3 + o], v.y, s.y);
-      }
-    }
-    Au[j] = s;
-  }
-  // w (global l = 0) or the H-term u_{l-1, M-1} (real storage: one rank, previous local step)
-  const double2 base = real ? (l == 0 ? __ldg(st.u0 + n) : u_at(u, ul - g.N + n, true)) : prev_value(st, l, n);
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    double2 acc = csub(base, uc[m]);
-    if (st.v) acc = cadd(acc, __ldg(st.v + ((size_t)l * M + m) * g.N + n));   // forcing part of w
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      const double q = g.dTQ[m * M + j];
-      acc.x = fma(q, Au[j].x, acc.x);
-      acc.y = fma(q, Au[j].y, acc.y);
-    }
-    r[m] = acc;
-  }
-}
 
 // ---------------------------------------------------------------------------------------------
 // Time-transform tile kernels.  Tile: all l x all m x T consecutive n, element (l, m, t) at
@@ -1150,7 +1087,7 @@ __global__ void __launch_bounds__(256) xdft_kernel(Geometry g, StaticTables st, 
 // ---------------------------------------------------------------------------------------------
 // residual norms and initialisation
 
-template <int M>
+template <int M, bool P2 = true>
 __global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables st,
                                                       const double2 *__restrict__ u, double *partial) {
   __shared__ double s2[32], sm_[32];
@@ -1160,7 +1097,8 @@ __global__ void __launch_bounds__(256) resnorm_kernel(Geometry g, StaticTables s
        i += (long long)gridDim.x * blockDim.x) {
     const int l = (int)(i / g.N), n = (int)(i - (long long)l * g.N);
     double2 r[M];
-    if (st.packed) residual_point<M, true>(g, st, u, l, n, r);
+    if (!P2) residual_point<M, false, 3, false>(g, st, u, l, n, r);
+    else if (st.packed) residual_point<M, true>(g, st, u, l, n, r);
     else residual_point<M, false>(g, st, u, l, n, r);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
@@ -1314,6 +1252,7 @@ LaunchCfg choose_launch(const Geometry &g) {
   int T2 = 32;
   while (T2 > 1 && (size_t)g.L * T2 * sizeof(double2) > 64 * 1024) T2 >>= 1;
   while (T2 > g.N) T2 >>= 1;
+  while (T2 > 1 && g.N % T2) T2 >>= 1;   // generic grids: T must divide N
   lc.tfft_T = T2;
   if (g.dim == 1) {
     if (g.N <= 4096) {
@@ -1349,6 +1288,7 @@ static bool pipe2d(const Geometry &g, const StaticTables &st) {
 bool pipe2d_geometry(const Geometry &g) { return reg2d(g) && spatial_pipe_geometry(g); }
 
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc, const StaticTables &st) {
+  if (!g.pow2) return generic_launches(g);
   if (g.dim == 2) return pipe2d(g, st) ? 6 : (reg2d(g) ? 4 : 6);
   return lc.pcr_mode == 0 ? 3 : 4;
 }
@@ -1365,6 +1305,7 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
                               "rows_pipe_kernel<inv>", "tfft_pipe_kernel<inv>"};
   const int n = launches_per_iteration(g, lc, st);
   if (i < 0 || i >= n) return "";
+  if (!g.pow2) return generic_kernel_name(g, i);
   if (g.dim == 2) {
     if (pipe2d(g, st)) return tfft_pipe_supported(g, st) && !legacy_tfft() ? k2t[i] : k2q[i];
     const char *nm = reg2d(g) ? k2p[i] : k2[i];
@@ -1430,6 +1371,16 @@ static void residual_block(const Geometry &g, int &BX, int &BY) {
 
 cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                            const AlphaTables &at, const Buffers &b, cudaStream_t s) {
+  if (!g.pow2) {   // generic grids (generic.cu): residual, then the time DFT on T | N columns
+    cudaError_t e = launch_generic_residual(g, st, at, b.u, b.X, s);
+    if (e != cudaSuccess) return e;
+    const int T2 = lc.tfft_T;
+    const size_t sm2 = (size_t)g.L * (T2 + 1) * sizeof(double2);
+    if ((e = set_smem((const void *)tfft_fwd_kernel, sm2)) != cudaSuccess) return e;
+    tfft_fwd_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, b.X, T2);
+    rec(s);
+    return cudaGetLastError();
+  }
   int T = lc.fwd_T;
   if (st.packed) while (T > g.N / 2) T >>= 1;
   const size_t smem = fwd_smem_bytes(g, T) + (size_t)g.L * sizeof(double2);   // + staged twiddles
@@ -1502,6 +1453,10 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
 cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                          const AlphaTables &at, const Buffers &b, cudaStream_t s, double2 **out) {
   cudaError_t e = cudaSuccess;
+  if (!g.pow2) {   // generic grids: node transforms + mixed-radix FFT-diagonal solves (generic.cu)
+    *out = b.X;
+    return launch_generic_solve(g, st, at, b.X, s);
+  }
   const int lines = st.nsolve * g.M;   // solved units x nodes (Hermitian mode: k <= L/2)
   if (g.dim == 1) {
     if (lc.pcr_mode == 0) {
@@ -1592,7 +1547,14 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   const size_t smem = fwd_smem_bytes(g, T);
   const int grid = (st.packed && g.dim == 1 ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
-  if (g.dim == 1) {
+  if (!g.pow2) {   // generic grids: G^{-1} S was applied by the solve; inverse DFT on T | N columns
+    const int T2 = lc.tfft_T;
+    const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
+    e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
+    if (e == cudaSuccess)
+      tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
+                                                                           (unsigned long long *)diff_slot, overwrite);
+  } else if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
       if (st.packed) {
         e = set_smem((const void *)bwd_kernel<MM, true, true>, smem);
@@ -1769,7 +1731,10 @@ cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, cons
   int blocks = (int)((total + 255) / 256);
   const int cap = 148 * 8;  // partials scratch is sized for 148*8 blocks (pint_abi.cpp layout)
   if (blocks > cap) blocks = cap;
-  PINT_DISPATCH_M(g.M, { resnorm_kernel<MM><<<blocks, 256, 0, s>>>(g, st, b.u, b.red); });
+  PINT_DISPATCH_M(g.M, {
+    if (g.pow2) resnorm_kernel<MM><<<blocks, 256, 0, s>>>(g, st, b.u, b.red);
+    else resnorm_kernel<MM, false><<<blocks, 256, 0, s>>>(g, st, b.u, b.red);
+  });
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   reduce_partials_kernel<<<1, 32, 0, s>>>(b.red, blocks, out2);

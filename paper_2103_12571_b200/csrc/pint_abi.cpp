@@ -73,12 +73,18 @@ struct pint_ctx {
 static pint_status validate(const pint_problem *p, const pint_dist *d) {
   if (!p) return fail(PINT_ERR_INVALID, "problem is NULL");
   if (p->dim != 1 && p->dim != 2) return fail(PINT_ERR_INVALID, "dim must be 1 or 2");
-  if (!is_pow2(p->nx) || p->nx < 4) return fail(PINT_ERR_INVALID, "nx must be a power of two >= 4");
+  // power-of-two grids (every BASELINE config), or 7-smooth sizes 2^a 3^b 5^c 7^d (Tables 1-2,
+  // P:751-799) on the generic path: <= 4096 per axis, one rank
+  if (!grid_is_smooth(p->nx) || p->nx < 4) return fail(PINT_ERR_INVALID, "nx must be a power of two or 7-smooth, >= 4");
   if (p->dim == 1 && p->ny != 1) return fail(PINT_ERR_INVALID, "ny must be 1 in 1-D");
-  if (p->dim == 2 && (!is_pow2(p->ny) || p->ny < 4)) return fail(PINT_ERR_INVALID, "ny must be a power of two >= 4");
+  if (p->dim == 2 && (!grid_is_smooth(p->ny) || p->ny < 4))
+    return fail(PINT_ERR_INVALID, "ny must be a power of two or 7-smooth, >= 4");
   if (p->nx > (1 << 20) || p->ny > 4096) return fail(PINT_ERR_INVALID, "grid too large");
   if (p->dim == 2 && (p->nx > 4096)) return fail(PINT_ERR_INVALID, "2-D nx must be <= 4096");
-  if (p->op < PINT_OP_HEAT || p->op > PINT_OP_UPWIND5) return fail(PINT_ERR_INVALID, "unknown op");
+  const bool pow2 = is_pow2(p->nx) && (p->dim == 1 || is_pow2(p->ny));
+  if (!pow2 && p->nx > 4096) return fail(PINT_ERR_INVALID, "non-power-of-two grids: nx <= 4096");
+  if (!pow2 && d && d->nranks > 1) return fail(PINT_ERR_INVALID, "non-power-of-two grids run on one rank");
+  if (p->op < PINT_OP_HEAT || p->op > PINT_OP_UPWIND4) return fail(PINT_ERR_INVALID, "unknown op");
   if (!is_pow2(p->L) || p->L > 1024) return fail(PINT_ERR_INVALID, "L must be a power of two <= 1024 (P:592)");
   if (p->M < 1 || p->M > PINT_MAX_M) return fail(PINT_ERR_INVALID, "M must be in [1, 8]");
   if (!(p->T > 0) || !std::isfinite(p->T)) return fail(PINT_ERR_INVALID, "T must be > 0");
@@ -106,10 +112,11 @@ static Geometry make_geometry(const pint_problem *p, int P) {
   g.L = p->L / P;          // local step count (cyclic distribution l = rank + P j)
   g.M = p->M;
   g.op = p->op;
+  g.pow2 = is_pow2(g.nx) && is_pow2(g.ny) ? 1 : 0;
   g.logL = ilog2(g.L);
-  g.logN = ilog2(g.N);
-  g.lognx = ilog2(g.nx);
-  g.logny = ilog2(g.ny);
+  g.logN = g.pow2 ? ilog2(g.N) : 0;        // generic grids: no log2 plans (generic.cu)
+  g.lognx = g.pow2 ? ilog2(g.nx) : 0;
+  g.logny = g.pow2 ? ilog2(g.ny) : 0;
   g.dT = p->T / p->L;      // global step size
   // stencil weights (long double rationals rounded once; readings R8, R14)
   AxisStencil sx, sy;
@@ -121,7 +128,7 @@ static Geometry make_geometry(const pint_problem *p, int P) {
     g.wx[o] = (double)(o == 3 ? sx.w[3] + sy.w[3] : sx.w[o]);
     g.wy[o] = o == 3 ? 0.0 : (double)sy.w[o];
   }
-  g.nfac = g.dim == 1 ? stencil_factor_count(p->op, sx) : 1;
+  g.nfac = g.dim == 1 && g.pow2 ? stencil_factor_count(p->op, sx) : 1;
   return g;
 }
 
@@ -517,7 +524,7 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
       for (int m = 0; m < M; ++m) {
         const cld s = lam[m] * dT;                          // (I - d_km dT A)
         shift[(size_t)p * M + m] = make_double2((double)s.real(), (double)s.imag());
-        if (g.dim == 1) {
+        if (g.dim == 1 && g.pow2) {
           // I - s A = lead prod_f T_f; row-sum-carrying PCR coefficients per factor (DESIGN.md
           // reading R6), levels interleaved: lev[(j F + f) 2 + {0, 1}] = (p_j, q_j) of factor f
           std::vector<TriFactor> fac;
@@ -1040,6 +1047,8 @@ pint_status pint_set_form(pint_ctx *c, int32_t form) {
   if (form != PINT_FORM_CORRECTION && form != PINT_FORM_DIRECT) return fail(PINT_ERR_INVALID, "unknown form");
   if (form == PINT_FORM_DIRECT && c->P > 1) return fail(PINT_ERR_INVALID, "the direct form is single-rank only");
   if (form == PINT_FORM_DIRECT && c->st.v) return fail(PINT_ERR_INVALID, "the direct form assumes b == 0");
+  if (form == PINT_FORM_DIRECT && !c->g.pow2)
+    return fail(PINT_ERR_INVALID, "non-power-of-two grids: correction form only (generic path)");
   c->form = form;
   return PINT_OK;
 }
@@ -1050,6 +1059,7 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
   if (on) {
+    if (!g.pow2) return fail(PINT_ERR_INVALID, "Hermitian mode: power-of-two grids only");
     if (g.dim == 2 && (!reg2d_path(g) || g.ny < 2))
       return fail(PINT_ERR_INVALID, "Hermitian mode: 2-D grids of the register FFT engine, 4 <= L <= 1024, only");
     if (g.dim == 1 && (g.N < 8 || g.L < 2)) return fail(PINT_ERR_INVALID, "Hermitian mode needs N >= 8 and L >= 2");

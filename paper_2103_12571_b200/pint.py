@@ -20,7 +20,8 @@ LIB_PATH = os.environ.get("PINT_LIBRARY") or os.path.join(HERE, "libpint.so")
 PINT_OK = 0
 STATUS = {0: "PINT_OK", 1: "PINT_ERR_INVALID", 2: "PINT_ERR_SCHEDULE", 3: "PINT_ERR_NOT_DIAGONALIZABLE",
           4: "PINT_ERR_NUMERIC", 5: "PINT_ERR_CUDA", 6: "PINT_ERR_NCCL", 7: "PINT_ERR_STATE"}
-OPS = {"heat": 0, "advection": 1, "heat4": 2, "heat6": 3, "upwind1": 4, "upwind3": 5, "upwind5": 6}
+OPS = {"heat": 0, "advection": 1, "heat4": 2, "heat6": 3, "upwind1": 4, "upwind3": 5, "upwind5": 6,
+       "upwind2": 7, "upwind4": 8}
 MAX_SCHEDULE = 64
 
 # every symbol include/pint.h declares (checked by tests/test_abi.py)

@@ -16,7 +16,7 @@ using namespace pint;
 int main() {
   int fails = 0;
   const int ops[] = {PINT_OP_HEAT, PINT_OP_ADVECTION, PINT_OP_HEAT4, PINT_OP_HEAT6,
-                     PINT_OP_UPWIND1, PINT_OP_UPWIND3, PINT_OP_UPWIND5};
+                     PINT_OP_UPWIND1, PINT_OP_UPWIND2, PINT_OP_UPWIND3, PINT_OP_UPWIND4, PINT_OP_UPWIND5};
   const long long n = 128;
   const ld coefs[] = {1.0L, -0.7L, 1e-2L};
   const cld shifts[] = {cld(1e-4L, 0), cld(3e-3L, 1e-3L), cld(2e-2L, -4e-2L), cld(0.5L, 0.3L), cld(5.0L, -2.0L)};

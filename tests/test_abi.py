@@ -89,8 +89,10 @@ def test_workspace_and_validation():
     v5 = 512 * 4 * 1024 * 1024 * 16
     assert 2 * v5 <= n5 < 2.05 * v5
     n4s, _ = _ws(dim=2, nx=64, ny=64, L=16, M=3, nu=1e-2, T=1.0)   # small grids: one work vector
+    nt, err = _ws(dim=2, nx=350, ny=490, L=8, M=2, nu=1.0, T=0.1)   # Table 1/2 sizes (generic path)
+    assert nt >= 8 * 2 * 350 * 490 * 16, err
     assert 16 * 3 * 64 * 64 * 16 <= n4s < 2 * 16 * 3 * 64 * 64 * 16
-    for bad, msg in [(dict(L=3), "power of two"), (dict(nx=48), "power of two"), (dict(M=9), "M must"),
+    for bad, msg in [(dict(L=3), "power of two"), (dict(nx=44), "7-smooth"), (dict(nx=22), "7-smooth"), (dict(M=9), "M must"),
                      (dict(dim=3), "dim"), (dict(T=-1.0), "T must"), (dict(dim=2, ny=1), "ny")]:
         n, err = _ws(**bad)
         assert n == 0 and msg in err, (bad, err)

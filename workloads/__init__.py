@@ -208,3 +208,31 @@ def discretisation_cases():
     out.append(heat.replace(name="disc_heat4_2d_64x8", op="heat4", M=2, nx=64, ny=8))
     out.append(heat.replace(name="disc_heat6_2d_M8", op="heat6", M=8, nx=16, ny=16, L=4, T=0.01))
     return out
+
+
+def table_cases():
+    """The paper's own test problems at their Table 1/2 sizes:
+    heat u_t = Laplace(u) (nu = 1, centred kappa 2/4/6) and advection u_t + u_x + u_y = 0 (upwind
+    kappa 1..5) on the periodic unit square, with the printed N (7-smooth, mostly not
+    powers of two: 300, 350, 400, 450, 490, 700, 800), kappa, M, L and T (Table 1) or dT = T_64/64
+    (Table 2).  2-D grids are N x N, the 1-D variants N points.  Seeded random complex u0 (every
+    spatial mode excited; the forcing of P:706-712 is not needed for parity), fixed alpha."""
+    heat = Problem("tab", 2, 8, 8, "heat", 1.0, 0.0, 0.0, 0.1, 32, 1, "random", "fixed", 1e-3, 2)
+    adv = heat.replace(op="upwind2", nu=0.0, cx=1.0, cy=1.0)
+    out = []
+    # Table 1: heat T = 0.1, advection T = 1e-2
+    for N, kap, M, L in ((450, 2, 1, 32), (400, 4, 2, 32), (300, 6, 3, 16)):
+        op = {2: "heat", 4: "heat4", 6: "heat6"}[kap]
+        out.append(heat.replace(name=f"t1_heat_k{kap}_N{N}", op=op, nx=N, ny=N, M=M, L=L, T=0.1))
+    for N, kap, M, L in ((350, 2, 2, 8), (350, 4, 2, 16), (490, 5, 3, 32)):
+        out.append(adv.replace(name=f"t1_adv_k{kap}_N{N}", op=f"upwind{kap}", nx=N, ny=N, M=M, L=L, T=1e-2))
+    # Table 2: dT = T_64 / 64, here L = 8 steps of it
+    for N, kap, M, T64 in ((350, 2, 1, 0.32), (400, 4, 2, 0.16), (350, 6, 3, 0.16)):
+        op = {2: "heat", 4: "heat4", 6: "heat6"}[kap]
+        out.append(heat.replace(name=f"t2_heat_k{kap}_N{N}", op=op, nx=N, ny=N, M=M, L=8, T=8 * T64 / 64))
+    for N, kap, M, T64 in ((800, 1, 1, 0.00016), (800, 3, 2, 0.00064), (700, 5, 3, 0.0128)):
+        out.append(adv.replace(name=f"t2_adv_k{kap}_N{N}", op=f"upwind{kap}", nx=N, ny=N, M=M, L=8, T=8 * T64 / 64))
+    # 1-D variants of every entry (N points)
+    out += [p.replace(name=p.name + "_1d", dim=1, ny=1, cy=0.0) for p in list(out)]
+    return out
+
