@@ -119,7 +119,8 @@ def test_create_rejects_null_and_bad_sharding():
     assert "M * nranks" in lib.pint_last_error().decode()
 
 
-@pytest.mark.parametrize("op", ["heat", "advection", "heat4", "heat6", "upwind1", "upwind3", "upwind5"])
+@pytest.mark.parametrize("op", ["heat", "advection", "heat4", "heat6", "upwind1", "upwind2", "upwind3", "upwind4",
+                                "upwind5"])
 def test_every_operator_is_accepted(op):
     """All pint_op codes of include/pint.h validate in 1-D and 2-D (reading R14); the
     1-D workspace grows with the number of tridiagonal factors of I - s A (PCR tables per factor)."""
@@ -130,7 +131,7 @@ def test_every_operator_is_accepted(op):
     n2, err = _ws(dim=2, nx=32, ny=32, cy=0.0 if heat else -0.3, **kw)
     assert n2 > 0, err
     base1, _ = _ws(op="heat", nu=0.5)
-    if op in ("heat4", "heat6", "upwind3", "upwind5"):
+    if op in ("heat4", "heat6", "upwind2", "upwind3", "upwind4", "upwind5"):
         assert n1 > base1          # F = 2 or 3 factor tables
     else:
         assert n1 == base1
@@ -138,7 +139,7 @@ def test_every_operator_is_accepted(op):
 
 def test_unknown_operator_code_is_rejected():
     lib = P.load_library()
-    cp = P.pint.Problem(1, 64, 1, 7, 1.0, 0.0, 0.0, 0.1, 4, 2)   # 7: no such pint_op
+    cp = P.pint.Problem(1, 64, 1, 9, 1.0, 0.0, 0.0, 0.1, 4, 2)   # 9: no such pint_op
     d = P.pint.Dist(0, 1, None, 0, None)
     assert lib.pint_workspace_bytes(ctypes.byref(cp), ctypes.byref(d)) == 0
     assert "unknown op" in lib.pint_last_error().decode()
