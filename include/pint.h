@@ -89,7 +89,10 @@ typedef enum {
 
 typedef struct {
   int32_t dim;     /* 1 or 2                                                                  */
-  int32_t nx, ny;  /* grid; powers of two, nx >= 4 (ny == 1 if dim == 1, ny >= 4 if dim == 2) */
+  int32_t nx, ny;  /* grid, >= 4 per axis (ny == 1 if dim == 1): powers of two (every BASELINE
+                      config; 1-D nx <= 2^20, 2-D <= 4096), or 7-smooth sizes 2^a 3^b 5^c 7^d <= 4096
+                      (the paper's Table 1/2 grids) on the generic-grid path: one rank,
+                      correction form, no Hermitian mode (generic.cu: mixed-radix FFT solves) */
   int32_t op;      /* pint_op                                                                 */
   double nu;       /* heat diffusivity                                                        */
   double cx, cy;   /* advection velocity (cy ignored in 1-D)                                  */
