@@ -79,6 +79,7 @@ struct StaticTables {
   const int *slots, *unitof;
   int nsolve;
   int packed;
+  int sm_reserve;             // NCCL ranks: SMs the persistent kernels leave free (comm/compute overlap)
   const double2 *v;           // forcing part of w, [L][M][N] local steps (nullptr: b == 0)
 };
 
@@ -192,8 +193,10 @@ cudaError_t launch_halo_pack(const Geometry &g, const Buffers &b, double2 *hsend
 // P > 1: cross-rank P-point DFT (+ S^{-1}) from the all-to-all receive buffer Yin[src][pl][m][n]
 // into slot order Xout[q*(L/P^2... see kernels.cu)], and its inverse (G^{-1} S, inverse DFT) into
 // send chunks by destination.
+// pl0 / npl: the band of chunk slots pl0 .. pl0 + npl (npl < 0: to the end) of the overlapped
+// schedule
 cudaError_t launch_xdft(const Geometry &g, const StaticTables &st, const AlphaTables &at,
-                        const double2 *in, double2 *out, bool inverse, cudaStream_t s);
+                        const double2 *in, double2 *out, bool inverse, cudaStream_t s, int pl0 = 0, int npl = -1);
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc, const StaticTables &st);
 const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i);
 

@@ -1019,14 +1019,15 @@ __global__ void halo_pack_kernel(Geometry g, const double2 *__restrict__ u, doub
 //          [dst g][pl][m][n]
 template <int M, int P, bool INV>
 __global__ void __launch_bounds__(256) xdft_kernel(Geometry g, StaticTables st, AlphaTables at,
-                                                   const double2 *__restrict__ in, double2 *__restrict__ out) {
+                                                   const double2 *__restrict__ in, double2 *__restrict__ out,
+                                                   int pl0, int npl) {
   const int Lc = g.L / P;
-  const long long total = (long long)Lc * g.N;
+  const long long total = (long long)npl * g.N;           // band pl0 .. pl0 + npl of the chunk slots
   const long long chunk = (long long)Lc * M * g.N;       // elements per peer chunk
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int pl = (int)(i / g.N);
-    const long long n = i - (long long)pl * g.N;
+    const int pl = pl0 + (int)(i / g.N);
+    const long long n = i - (long long)(pl - pl0) * g.N;
     double2 x[P][M];
     if (!INV) {
 #pragma unroll
@@ -1751,8 +1752,9 @@ cudaError_t launch_halo_pack(const Geometry &g, const Buffers &b, double2 *hsend
 }
 
 cudaError_t launch_xdft(const Geometry &g, const StaticTables &st, const AlphaTables &at,
-                        const double2 *in, double2 *out, bool inverse, cudaStream_t s) {
-  const long long total = (long long)(g.L / st.P) * g.N;
+                        const double2 *in, double2 *out, bool inverse, cudaStream_t s, int pl0, int npl) {
+  if (npl < 0) npl = g.L / st.P - pl0;
+  const long long total = (long long)npl * g.N;
   long long blocks = (total + 255) / 256;
   if (blocks > num_sms() * 16) blocks = num_sms() * 16;
   cudaError_t e = cudaErrorInvalidValue;
@@ -1760,8 +1762,8 @@ cudaError_t launch_xdft(const Geometry &g, const StaticTables &st, const AlphaTa
   if (st.P == PP) {                                                                            \
     PINT_DISPATCH_M(g.M, {                                                                     \
       if constexpr (MM * PP <= 32) {                                                           \
-        if (inverse) xdft_kernel<MM, PP, true><<<(int)blocks, 256, 0, s>>>(g, st, at, in, out);  \
-        else xdft_kernel<MM, PP, false><<<(int)blocks, 256, 0, s>>>(g, st, at, in, out);         \
+        if (inverse) xdft_kernel<MM, PP, true><<<(int)blocks, 256, 0, s>>>(g, st, at, in, out, pl0, npl); \
+        else xdft_kernel<MM, PP, false><<<(int)blocks, 256, 0, s>>>(g, st, at, in, out, pl0, npl);       \
         e = cudaGetLastError();                                                                \
       }                                                                                        \
     });                                                                                        \

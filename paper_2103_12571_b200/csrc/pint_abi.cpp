@@ -37,6 +37,7 @@ struct Layout {
   size_t off_red, red_bytes;
   size_t off_sync, sync_bytes;                // 2-D spatial pipeline completion counters
   size_t off_sym;                             // unit slot list and slot -> unit map [2][L] int
+  size_t off_band;                            // P > 1: band slot lists of the overlapped schedule
   size_t off_seq;                             // sequential baseline: Q eigen tables (sig, shift, V)
   size_t total;
   bool two_vectors;
@@ -63,6 +64,12 @@ struct pint_ctx {
   int form = PINT_FORM_CORRECTION;
   bool hermitian = false;
   bool poisoned = false;
+  // P > 1, overlapped schedule: the chunk slots pl < L/P^2 split into `bands`
+  // bands; the all-to-alls of band b run on `comm` while the compute stream solves band b - 1
+  int bands = 1;
+  cudaStream_t commstream = nullptr;
+  bool commstream_owned = false;
+  std::vector<cudaEvent_t> ev;     // [0] forward done, then per band: a2a#1, mid, a2a#2
   std::vector<ld> t, Q;
   std::vector<double> u0;          // host copy (2N)
   // host copies of the factor tables (natural frequency order) for introspection
@@ -173,6 +180,8 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   off = align_up(off + L.sync_bytes, 256);
   L.off_sym = off;
   off = align_up(off + 2 * (size_t)g.L * sizeof(int), 256);
+  L.off_band = off;                                        // P > 1: slot lists of the bands (L ints)
+  off = align_up(off + (size_t)g.L * sizeof(int), 256);
   L.off_seq = off;
   off = align_up(off + (size_t)(2 * g.M + g.M * g.M) * sizeof(double2), 256);
   L.total = off;
@@ -392,6 +401,30 @@ pint_status pint_create(const pint_problem *p, const pint_dist *d, void *u_dev, 
     c->st.nsolve = g.L;
     c->st.packed = 0;
     c->st.v = nullptr;
+    c->st.sm_reserve = (P > 1 && !c->loopback) ? 16 : 0;   // SMs left to NCCL's kernels (overlap)
+  }
+  if (P > 1) {
+    // overlapped schedule: bands of the chunk slots pl (the 2-D plane passes of spatial2d.cu address
+    // planes by slot, so a band's slot list {q Lc + pl : q < P, pl in band} is enough; the 1-D PCR
+    // and the generic row / column kernels work on whole slot ranges: one band)
+    const int Lc = g.L / P;
+    int B = g.dim == 2 && reg2d_path(g) ? 4 : 1;
+    while (B > 1 && Lc % B) B >>= 1;
+    c->bands = B;
+    std::vector<int> band((size_t)g.L);
+    const int nb = Lc / B;
+    size_t o2 = 0;
+    for (int bb = 0; bb < B; ++bb)
+      for (int q = 0; q < P; ++q)
+        for (int pl = bb * nb; pl < (bb + 1) * nb; ++pl) band[o2++] = q * Lc + pl;
+    CREATE_TRY(c, cudaMemcpyAsync(c->work + lay.off_band, band.data(), band.size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, c->stream));
+    if (!c->loopback) {
+      CREATE_TRY(c, cudaStreamCreateWithFlags(&c->commstream, cudaStreamNonBlocking));
+      c->commstream_owned = true;
+    }
+    c->ev.resize(1 + 3 * B);
+    for (auto &e : c->ev) CREATE_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   Buffers b{c->u, (double2 *)(c->work + lay.off_X), (double2 *)(c->work + lay.off_Y),
             (double *)(c->work + lay.off_red), (unsigned *)(c->work + lay.off_sync)};
@@ -654,18 +687,40 @@ static pint_status nccl_halo(pint_ctx *c) {
   return PINT_OK;
 }
 
-static pint_status nccl_alltoall(pint_ctx *c, const double2 *send, double2 *recv) {
-  const size_t ce = chunk_elems(c);
+// band bb of every peer chunk: chunk slots pl in [bb nb, (bb + 1) nb), contiguous in both buffers
+static size_t band_elems(pint_ctx *c) { return chunk_elems(c) / c->bands; }
+
+static pint_status nccl_alltoall(pint_ctx *c, const double2 *send, double2 *recv, int bb) {
+  const size_t ce = chunk_elems(c), be = band_elems(c), off = (size_t)bb * be;
   ncclResult_t r = ncclGroupStart();
   for (int d = 0; d < c->P && r == ncclSuccess; ++d) {
-    r = ncclSend(send + d * ce, ce * 2, ncclDouble, d, c->comm, c->stream);
-    if (r == ncclSuccess) r = ncclRecv(recv + d * ce, ce * 2, ncclDouble, d, c->comm, c->stream);
+    r = ncclSend(send + d * ce + off, be * 2, ncclDouble, d, c->comm, c->commstream);
+    if (r == ncclSuccess) r = ncclRecv(recv + d * ce + off, be * 2, ncclDouble, d, c->comm, c->commstream);
   }
   ncclResult_t r2 = ncclGroupEnd();
   if (r != ncclSuccess || r2 != ncclSuccess) {
     c->poisoned = true;
     return fail(PINT_ERR_NCCL, std::string("all-to-all: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
   }
+  return PINT_OK;
+}
+
+// P > 1: the middle of one band (chunk slots pl in band bb): cross-rank DFT + S^{-1} (Y -> X),
+// the spatial solves of the band's slots, G^{-1} S + inverse cross-rank DFT (X -> Y send chunks)
+static pint_status run_mid_band(pint_ctx *c, int a, int bb, IterState &is) {
+  Buffers b = buffers(c);
+  const AlphaTables &at = c->at[a];
+  const int Lc = c->g.L / c->P, nb = Lc / c->bands;
+  CUDA_TRY(c, launch_xdft(c->g, c->st, at, b.Y, b.X, false, c->stream, bb * nb, nb));
+  StaticTables sb = c->st;
+  sb.slots = (const int *)(c->work + c->lay.off_band) + (size_t)bb * c->P * nb;
+  sb.nsolve = c->P * nb;
+  double2 *x2 = nullptr;
+  CUDA_TRY(c, launch_solve(c->g, c->lc, sb, at, b, c->stream, &x2));
+  double2 *other = (x2 == b.X) ? b.Y : b.X;
+  CUDA_TRY(c, launch_xdft(c->g, c->st, at, x2, other, true, c->stream, bb * nb, nb));
+  is.send_back = other;
+  is.solved = x2;
   return PINT_OK;
 }
 
@@ -692,9 +747,25 @@ static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
   if ((st = run_phase(c, PH_PRE, a, nullptr, is)) != PINT_OK) return st;
   if ((st = nccl_halo(c)) != PINT_OK) return st;
   if ((st = run_phase(c, PH_FWD, a, nullptr, is)) != PINT_OK) return st;
-  if ((st = nccl_alltoall(c, b.X, b.Y)) != PINT_OK) return st;
-  if ((st = run_phase(c, PH_MID, a, nullptr, is)) != PINT_OK) return st;
-  if ((st = nccl_alltoall(c, is.send_back, is.solved)) != PINT_OK) return st;
+  // overlapped middle: all-to-all #1 of every band on the comm stream; band b's
+  // cross-rank DFT + solves + inverse DFT on the compute stream as soon as its data arrived, its
+  // all-to-all #2 right after it, overlapping band b + 1's compute
+  const int B = c->bands;
+  CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->commstream, c->ev[0], 0));
+  for (int bb = 0; bb < B; ++bb) {
+    if ((st = nccl_alltoall(c, b.X, b.Y, bb)) != PINT_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[1 + 3 * bb], c->commstream));
+  }
+  for (int bb = 0; bb < B; ++bb) {
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev[1 + 3 * bb], 0));
+    if ((st = run_mid_band(c, a, bb, is)) != PINT_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[2 + 3 * bb], c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->commstream, c->ev[2 + 3 * bb], 0));
+    if ((st = nccl_alltoall(c, is.send_back, is.solved, bb)) != PINT_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[3 + 3 * bb], c->commstream));
+  }
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev[3 * B], 0));   // the comm stream is in order
   // last-step diff: only the rank holding global step L-1 (rank P-1) reports it
   return run_phase(c, PH_BWD, a, c->rank == c->P - 1 ? diff_slot : nullptr, is);
 }
@@ -774,6 +845,19 @@ pint_status pint_group_iterate(pint_ctx *const *ctxs, int32_t P, int32_t n_iter,
     slots = (double *)(last->work + last->lay.off_red) + 148 * 8 * 2 + 64;
     CUDA_TRY(last, cudaMemsetAsync(slots, 0, n_iter * sizeof(double), s));
   }
+  // second (copy) stream of the group and its events (the virtual ranks' own ones are unused)
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> gev(1 + 3 * ctxs[0]->bands, nullptr);
+  struct Cleanup {
+    cudaStream_t &cs;
+    std::vector<cudaEvent_t> &ev;
+    ~Cleanup() {
+      if (cs) { cudaStreamSynchronize(cs); cudaStreamDestroy(cs); }
+      for (cudaEvent_t e : ev) if (e) cudaEventDestroy(e);
+    }
+  } cleanup{cs, gev};
+  CUDA_TRY(last, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  for (auto &e : gev) CUDA_TRY(last, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int it = 0; it < n_iter; ++it) {
     std::vector<IterState> is(P);
     const int a = ctxs[0]->k;
@@ -784,18 +868,34 @@ pint_status pint_group_iterate(pint_ctx *const *ctxs, int32_t P, int32_t n_iter,
       CUDA_TRY(ctxs[r], cudaMemcpyAsync(hrecv(ctxs[(r + 1) % P]), hsend(ctxs[r]), hb, cudaMemcpyDeviceToDevice, s));
     for (int r = 0; r < P; ++r)
       if ((st = run_phase(ctxs[r], PH_FWD, a, nullptr, is[r])) != PINT_OK) return st;
-    for (int src = 0; src < P; ++src)
-      for (int dst = 0; dst < P; ++dst)
-        CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)buffers(ctxs[dst]).Y + src * ce,
-                                            (const char *)buffers(ctxs[src]).X + dst * ce, ce,
-                                            cudaMemcpyDeviceToDevice, s));
-    for (int r = 0; r < P; ++r)
-      if ((st = run_phase(ctxs[r], PH_MID, a, nullptr, is[r])) != PINT_OK) return st;
-    for (int src = 0; src < P; ++src)
-      for (int dst = 0; dst < P; ++dst)
-        CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)is[dst].solved + src * ce,
-                                            (const char *)is[src].send_back + dst * ce, ce,
-                                            cudaMemcpyDeviceToDevice, s));
+    // the overlapped middle of run_iteration with device copies on a second stream: every band's
+    // all-to-all #1, then per band the middle of every rank and its all-to-all #2
+    const int B = ctxs[0]->bands;
+    const size_t be = ce / B;
+    CUDA_TRY(last, cudaEventRecord(gev[0], s));
+    CUDA_TRY(last, cudaStreamWaitEvent(cs, gev[0], 0));
+    for (int bb = 0; bb < B; ++bb) {
+      for (int src = 0; src < P; ++src)
+        for (int dst = 0; dst < P; ++dst)
+          CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)buffers(ctxs[dst]).Y + src * ce + bb * be,
+                                              (const char *)buffers(ctxs[src]).X + dst * ce + bb * be, be,
+                                              cudaMemcpyDeviceToDevice, cs));
+      CUDA_TRY(last, cudaEventRecord(gev[1 + 3 * bb], cs));
+    }
+    for (int bb = 0; bb < B; ++bb) {
+      CUDA_TRY(last, cudaStreamWaitEvent(s, gev[1 + 3 * bb], 0));
+      for (int r = 0; r < P; ++r)
+        if ((st = run_mid_band(ctxs[r], a, bb, is[r])) != PINT_OK) return st;
+      CUDA_TRY(last, cudaEventRecord(gev[2 + 3 * bb], s));
+      CUDA_TRY(last, cudaStreamWaitEvent(cs, gev[2 + 3 * bb], 0));
+      for (int src = 0; src < P; ++src)
+        for (int dst = 0; dst < P; ++dst)
+          CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)is[dst].solved + src * ce + bb * be,
+                                              (const char *)is[src].send_back + dst * ce + bb * be, be,
+                                              cudaMemcpyDeviceToDevice, cs));
+      CUDA_TRY(last, cudaEventRecord(gev[3 + 3 * bb], cs));
+    }
+    CUDA_TRY(last, cudaStreamWaitEvent(s, gev[3 * B], 0));
     for (int r = 0; r < P; ++r)
       if ((st = run_phase(ctxs[r], PH_BWD, a, (r == P - 1 && slots) ? slots + it : nullptr, is[r])) != PINT_OK)
         return st;
@@ -950,6 +1050,10 @@ pint_status pint_next_window(pint_ctx *c) {
 
 pint_status pint_destroy(pint_ctx *c) {
   if (c && c->comm) ncclCommDestroy(c->comm);
+  if (c) {
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    if (c->commstream_owned) cudaStreamDestroy(c->commstream);
+  }
   delete c;
   return PINT_OK;
 }

@@ -530,6 +530,7 @@ cudaError_t launch_sp(const Geometry &g, const StaticTables &st, const AlphaTabl
   const double2 *ss = spec;
   unsigned *sy = sync;
   void *args[] = {&gg, &sst, &aat, &ssp, &xx, &ss, &sy};
+  if (st.sm_reserve > 0 && sms > 2 * st.sm_reserve) sms -= st.sm_reserve;   // leave SMs to NCCL
   return cudaLaunchCooperativeKernel(fn, dim3(sms * per), dim3(kSpThreads), args, smem, s);
 }
 
@@ -946,6 +947,7 @@ cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTa
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (st.sm_reserve > 0 && sms > 2 * st.sm_reserve) sms -= st.sm_reserve;   // leave SMs to NCCL
   cudaError_t e;
   const int TC = 1 << pp.lT;
   const unsigned nblk = g.nx / kBW;
