@@ -323,6 +323,7 @@ def main():
 
     # ---- per-kernel device times (same kernels, events after every launch; 1 rank only) -------
     peak, peak_src = measured_peaks()
+    phases = None
     if world == 1:
         nprof = max(3, min(args.steps, 10))
         s.set_alpha_schedule(schedule_for(p, w_inf, nprof + 1))
@@ -330,6 +331,14 @@ def main():
         kms = s.iterate_profiled(nprof)
     else:
         kms = None
+        # communication / computation split of the overlapped schedule (events around the phases
+        # of one iteration on every rank, max over ranks)
+        s.set_phase_timing(True)
+        s.set_alpha_schedule(schedule_for(p, w_inf, 2))
+        s.iterate(1)
+        ph = s.phase_times()
+        s.set_phase_timing(False)
+        phases = {k: max_over_ranks(v) for k, v in ph.items()}
     algo_tab = dict(ALGO_BYTES_DIRECT if args.form == "direct" else ALGO_BYTES)
     if args.hermitian:
         # packed real data: time series of N/2 complex columns (8 B per unknown), L/2 + 1 of L
@@ -466,6 +475,7 @@ def main():
                            "parallelism": "single GPU" if world == 1 else
                            f"time-sharded over {world} GPUs (cyclic steps, four-step FFT, NCCL all-to-all + ring halo)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sequential_baseline": seq,
+                "phases_ms": phases,
                 "gpu_launches": (nlaunch if world == 1 else nlaunch + 3) * args.steps,
                 "clocks": {**clk.summary(), "window": ("timed region +- 0.5 s of the same iterations"
                                                        if p.U < 1e9 else "timed region")},

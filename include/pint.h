@@ -295,6 +295,17 @@ int32_t pint_launches_per_iteration(pint_ctx *c);
  * iteration. */
 pint_status pint_iterate_profiled(pint_ctx *c, int32_t n_iter, double *kernel_ms);
 
+/* Per-phase device times of the last iteration of an NCCL rank (nranks > 1), for the
+ * communication / computation split of the overlapped schedule.  With timing on,
+ * pint_iterate records CUDA events around the phases; ms[7] receives: 0 halo (pack + ring),
+ * 1 forward (residual + local time FFT), 2 all-to-all #1 on the comm stream (first band issued ->
+ * last band received), 3 middle on the compute stream (bands' cross-rank DFTs + spatial solves),
+ * 4 from the end of the middle to the end of the iteration (exposed all-to-all #2 + backward),
+ * 5 forward start -> all-to-all #2 complete, 6 the whole iteration.  Synchronises on the
+ * iteration's last event.  Errors: PINT_ERR_INVALID (one rank / loopback), PINT_ERR_STATE. */
+pint_status pint_set_phase_timing(pint_ctx *c, int32_t on);
+pint_status pint_phase_times(pint_ctx *c, double *ms);
+
 /* Name of launch i of an iteration ("" if out of range). */
 const char *pint_kernel_name(pint_ctx *c, int32_t i);
 

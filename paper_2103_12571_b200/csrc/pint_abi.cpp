@@ -70,6 +70,8 @@ struct pint_ctx {
   cudaStream_t commstream = nullptr;
   bool commstream_owned = false;
   std::vector<cudaEvent_t> ev;     // [0] forward done, then per band: a2a#1, mid, a2a#2
+  bool phase_timing = false;       // pint_set_phase_timing: timed events around the phases
+  cudaEvent_t tev[8] = {};         // start, halo, fwd, a2a#1 first, a2a#1 last, mid end, a2a#2 last, end
   std::vector<ld> t, Q;
   std::vector<double> u0;          // host copy (2N)
   // host copies of the factor tables (natural frequency order) for introspection
@@ -744,19 +746,25 @@ static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
   }
   if (!c->comm) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: use pint_group_iterate");
   Buffers b = buffers(c);
+  const bool pt = c->phase_timing;
+  if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[0], c->stream));
   if ((st = run_phase(c, PH_PRE, a, nullptr, is)) != PINT_OK) return st;
   if ((st = nccl_halo(c)) != PINT_OK) return st;
+  if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[1], c->stream));
   if ((st = run_phase(c, PH_FWD, a, nullptr, is)) != PINT_OK) return st;
+  if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[2], c->stream));
   // overlapped middle: all-to-all #1 of every band on the comm stream; band b's
   // cross-rank DFT + solves + inverse DFT on the compute stream as soon as its data arrived, its
   // all-to-all #2 right after it, overlapping band b + 1's compute
   const int B = c->bands;
   CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
   CUDA_TRY(c, cudaStreamWaitEvent(c->commstream, c->ev[0], 0));
+  if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[3], c->commstream));
   for (int bb = 0; bb < B; ++bb) {
     if ((st = nccl_alltoall(c, b.X, b.Y, bb)) != PINT_OK) return st;
     CUDA_TRY(c, cudaEventRecord(c->ev[1 + 3 * bb], c->commstream));
   }
+  if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[4], c->commstream));
   for (int bb = 0; bb < B; ++bb) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev[1 + 3 * bb], 0));
     if ((st = run_mid_band(c, a, bb, is)) != PINT_OK) return st;
@@ -765,9 +773,15 @@ static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
     if ((st = nccl_alltoall(c, is.send_back, is.solved, bb)) != PINT_OK) return st;
     CUDA_TRY(c, cudaEventRecord(c->ev[3 + 3 * bb], c->commstream));
   }
+  if (pt) {
+    CUDA_TRY(c, cudaEventRecord(c->tev[5], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->tev[6], c->commstream));
+  }
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev[3 * B], 0));   // the comm stream is in order
   // last-step diff: only the rank holding global step L-1 (rank P-1) reports it
-  return run_phase(c, PH_BWD, a, c->rank == c->P - 1 ? diff_slot : nullptr, is);
+  if ((st = run_phase(c, PH_BWD, a, c->rank == c->P - 1 ? diff_slot : nullptr, is)) != PINT_OK) return st;
+  if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[7], c->stream));
+  return PINT_OK;
 }
 
 pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf) {
@@ -1052,6 +1066,7 @@ pint_status pint_destroy(pint_ctx *c) {
   if (c && c->comm) ncclCommDestroy(c->comm);
   if (c) {
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->tev) if (e) cudaEventDestroy(e);
     if (c->commstream_owned) cudaStreamDestroy(c->commstream);
   }
   delete c;
@@ -1098,6 +1113,28 @@ pint_status pint_graph_launch(pint_ctx *c, void *graph_exec) {
 pint_status pint_graph_destroy(void *graph_exec) {
   if (graph_exec && cudaGraphExecDestroy((cudaGraphExec_t)graph_exec) != cudaSuccess)
     return fail(PINT_ERR_CUDA, "cudaGraphExecDestroy failed");
+  return PINT_OK;
+}
+
+pint_status pint_set_phase_timing(pint_ctx *c, int32_t on) {
+  if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
+  BIND_DEVICE(c);
+  if (c->P == 1 || !c->comm) return fail(PINT_ERR_INVALID, "phase timing: NCCL ranks (nranks > 1) only");
+  if (on && !c->tev[0])
+    for (auto &e : c->tev) CUDA_TRY(c, cudaEventCreate(&e));
+  c->phase_timing = on != 0;
+  return PINT_OK;
+}
+
+pint_status pint_phase_times(pint_ctx *c, double *ms) {
+  if (!c || !ms) return fail(PINT_ERR_INVALID, "NULL argument");
+  BIND_DEVICE(c);
+  if (!c->phase_timing) return fail(PINT_ERR_STATE, "phase timing is off (pint_set_phase_timing)");
+  CUDA_TRY(c, cudaEventSynchronize(c->tev[7]));
+  float t[7];
+  const int from[7] = {0, 1, 3, 2, 5, 2, 0}, to[7] = {1, 2, 4, 5, 7, 6, 7};
+  for (int i = 0; i < 7; ++i) CUDA_TRY(c, cudaEventElapsedTime(&t[i], c->tev[from[i]], c->tev[to[i]]));
+  for (int i = 0; i < 7; ++i) ms[i] = t[i];
   return PINT_OK;
 }
 

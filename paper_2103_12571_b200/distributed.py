@@ -42,6 +42,23 @@ def slot_frequency(rank: int, nranks: int, L: int, slot: int) -> int:
     return kappa + Ll * q
 
 
+def bands(nranks: int, L: int, dim: int = 2) -> int:
+    """Number of bands of the overlapped schedule (pint_create: 4 in 2-D if L/P^2 allows it)."""
+    Lc = L // nranks // nranks
+    B = 4 if dim == 2 else 1
+    while B > 1 and Lc % B:
+        B //= 2
+    return B
+
+
+def band_slots(nranks: int, L: int, B: int, b: int) -> np.ndarray:
+    """Local frequency slots solved in band b: {q Lc + pl : q < P, pl in [b nb, (b+1) nb)}, the
+    order of the device list at work + off_band (pint_abi.cpp)."""
+    Lc = L // nranks // nranks
+    nb = Lc // B
+    return np.array([q * Lc + pl for q in range(nranks) for pl in range(b * nb, (b + 1) * nb)])
+
+
 def broadcast_bytes(payload: bytes | None, src: int = 0, nbytes: int = 128) -> bytes:
     """Broadcast `nbytes` bytes from rank `src` over the default torch.distributed group."""
     import torch

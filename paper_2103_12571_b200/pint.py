@@ -33,7 +33,7 @@ EXPORTS = ["pint_workspace_bytes", "pint_create", "pint_adaptive_schedule", "pin
            "pint_nccl_unique_id", "pint_local_steps", "pint_group_iterate", "pint_group_residual_norm",
            "pint_set_form", "pint_set_hermitian", "pint_solve", "pint_sequential", "pint_set_forcing",
            "pint_next_window", "pint_experiments_enabled", "pint_graph_create", "pint_graph_launch",
-           "pint_graph_destroy"]
+           "pint_graph_destroy", "pint_set_phase_timing", "pint_phase_times"]
 FORMS = {"correction": 0, "direct": 1}
 
 
@@ -105,6 +105,8 @@ def load_library(path: str = LIB_PATH):
         "pint_graph_create": (i32, [vp, i32, ctypes.POINTER(vp)]),
         "pint_graph_launch": (i32, [vp, vp]),
         "pint_graph_destroy": (i32, [vp]),
+        "pint_set_phase_timing": (i32, [vp, i32]),
+        "pint_phase_times": (i32, [vp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -259,6 +261,17 @@ class Solver:
             return d
         _check(self.lib.pint_iterate(self.ctx, n, None))
         return None
+
+    PHASES = ("halo", "forward", "alltoall1_span", "middle", "midend_to_end", "fwd_end_to_alltoall2_done", "total")
+
+    def set_phase_timing(self, on: bool = True):
+        _check(self.lib.pint_set_phase_timing(self.ctx, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """Per-phase ms of the last iteration (NCCL ranks, see include/pint.h)."""
+        out = np.zeros(7)
+        _check(self.lib.pint_phase_times(self.ctx, _dp(out)))
+        return dict(zip(self.PHASES, out.tolist()))
 
     def graph_create(self, n: int):
         """Capture n iterations into a CUDA graph (launch-bound problems); returns a handle."""
