@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: named ranges for nsys / ncu timelines
+
 #include "../../include/pint.h"
 #include "host_numerics.h"
 #include "internal.h"
@@ -643,7 +645,17 @@ struct IterState {
   double2 *send_back = nullptr;  // P > 1: inverse cross-rank DFT output (send chunks)
 };
 
+// NVTX range of one step group of the iteration (host-side markers, no device work)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 static pint_status run_phase(pint_ctx *c, Phase ph, int a, double *diff_slot, IterState &is) {
+  static const char *kPhaseName[] = {"pint halo (ring exchange pack)", "pint (i)-(ii) residual + time DFT",
+                                     "pint (iii)-(iv) node transforms + spatial solves",
+                                     "pint (v) inverse transforms + update"};
+  NvtxRange range(kPhaseName[ph]);
   Buffers b = buffers(c);
   const AlphaTables &at = c->at[a];
   switch (ph) {
@@ -727,6 +739,7 @@ static pint_status run_mid_band(pint_ctx *c, int a, int bb, IterState &is) {
 }
 
 static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
+  NvtxRange range("pint iteration");
   IterState is;
   pint_status st;
   if (c->form == PINT_FORM_DIRECT) {  // Alg. 1 as printed: u = C_a^{-1}((C_a - C) u + w), 1 rank
