@@ -37,7 +37,9 @@ ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32
               # pipelined plane passes (same 3 x 32 B, one launch each)
               "rows_pipe_kernel<fwd>": 32, "cols_pipe_kernel": 32, "rows_pipe_kernel<inv>": 32,
               # pipelined time transforms (forward in place, inverse x2 + u -> u)
-              "tfft_pipe_kernel<fwd>": 32, "tfft_pipe_kernel<inv>": 48}
+              "tfft_pipe_kernel<fwd>": 32, "tfft_pipe_kernel<inv>": 48,
+              # fused R / C / I plane passes (one launch; compulsory 3 x 32 B, L2 reuse can only lower it)
+              "spatial_fused_kernel": 96}
 # direct form (u = C_a^{-1}((C_a - C)u + w)): no read of u, input synthesized from one N-vector
 ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
                      "cols_direct_kernel": 16, "fft2d_rows_kernel<inv>": 32, "tfft_bwd_kernel": 32,

@@ -143,6 +143,10 @@ cudaError_t launch_generic_residual(const Geometry &g, const StaticTables &st, c
                                     const double2 *u, double2 *X, cudaStream_t s);
 cudaError_t launch_generic_solve(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
                                  cudaStream_t s);
+// Fused R/C/I persistent launch (1024^2 grids, one rank, complex storage): the default there
+bool spatial_fused_supported(const Geometry &g, const StaticTables &st);
+cudaError_t launch_spatial_fused(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                                 double2 *Yb, unsigned *sync, cudaStream_t s);
 bool spatial_pipe_geometry(const Geometry &g);                          // grid/M served (needs a 2nd vector)
 bool spatial_pipe_supported(const Geometry &g, const StaticTables &st);  // ... and the current mode
 // X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector

@@ -1290,7 +1290,7 @@ bool pipe2d_geometry(const Geometry &g) { return reg2d(g) && spatial_pipe_geomet
 
 int launches_per_iteration(const Geometry &g, const LaunchCfg &lc, const StaticTables &st) {
   if (!g.pow2) return generic_launches(g);
-  if (g.dim == 2) return pipe2d(g, st) ? 6 : (reg2d(g) ? 4 : 6);
+  if (g.dim == 2) return pipe2d(g, st) ? (spatial_fused_supported(g, st) ? 4 : 6) : (reg2d(g) ? 4 : 6);
   return lc.pcr_mode == 0 ? 3 : 4;
 }
 
@@ -1307,7 +1307,9 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
   const int n = launches_per_iteration(g, lc, st);
   if (i < 0 || i >= n) return "";
   if (!g.pow2) return generic_kernel_name(g, i);
+  static const char *k2f[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial_fused_kernel", "tfft_bwd_kernel"};
   if (g.dim == 2) {
+    if (pipe2d(g, st) && spatial_fused_supported(g, st)) return k2f[i];
     if (pipe2d(g, st)) return tfft_pipe_supported(g, st) && !legacy_tfft() ? k2t[i] : k2q[i];
     const char *nm = reg2d(g) ? k2p[i] : k2[i];
     if (tfft_pipe_supported(g, st) && !legacy_tfft()) {   // time transforms pipelined, spatial legacy
@@ -1489,6 +1491,11 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       rec(s);
       *out = b.Y;
     }
+  } else if (pipe2d(g, st) && spatial_fused_supported(g, st)) {
+    e = launch_spatial_fused(g, st, at, b.X, b.Y, b.sync, s);   // R, C, I items in one launch
+    *out = b.X;
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
   } else if (pipe2d(g, st)) {
     e = launch_spatial_pipe(g, st, at, b.X, b.Y, s);   // R, C, I: three launches, each recorded
     *out = b.X;

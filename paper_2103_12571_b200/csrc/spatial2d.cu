@@ -866,6 +866,284 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fused plane passes (1024^2 grids, radix-32 plans on both axes, one rank): R, C and I items of
+// consecutive frequency slots interleaved in ONE persistent launch, so the SM runs fp64-heavy C
+// items beside memory-heavy R / I items and the blocked spectra of a slot are re-read while still
+// largely in L2.  Global item sequence, round j: R(j), C(j - 1), I(j - 2) (batch = one slot, all M
+// nodes); CTA c takes items c, c + grid, ...; two groups of 128 threads alternate over a ring of
+// three slots (sized for the largest item).  Dependencies: C(b) reads what all R(b) items wrote,
+// I(b) what all C(b) items wrote: completion counters done[stage][b] (bar.sync + red.release.gpu
+// after the item's stores; ld.acquire.gpu + proxy fence before the TMA load that reads them).  A
+// refill whose dependency is not met yet is deferred to the group that will consume the item
+// (it waits once it holds no other unfinished item), so every wait points to items of an earlier
+// round that are never blocked behind a wait of a later round: deadlock free with all CTAs
+// resident (one per SM, launched as a cooperative grid).
+namespace fused {
+
+struct Seq {
+  int nb, nR, nC, nI;
+};
+
+__device__ __forceinline__ long long round_size(const Seq &q, int j) {
+  return (j < q.nb ? q.nR : 0) + (j >= 1 && j <= q.nb ? q.nC : 0) + (j >= 2 && j <= q.nb + 1 ? q.nI : 0);
+}
+
+// global item index -> (stage 0 R / 1 C / 2 I, batch, index within the stage segment)
+__device__ __forceinline__ void decode(const Seq &q, long long g, int &stage, int &b, int &idx) {
+  long long rs = 0;
+  int j = 0;
+  const long long s0 = round_size(q, 0), s1 = round_size(q, 1);
+  if (q.nb >= 3 && g >= s0 + s1) {   // skip whole middle rounds (all three segments present)
+    const long long S = (long long)q.nR + q.nC + q.nI;
+    long long jj = (g - s0 - s1) / S;
+    if (jj > q.nb - 2) jj = q.nb - 2;
+    j = 2 + (int)jj;
+    rs = s0 + s1 + jj * S;
+  }
+  for (;;) {
+    const long long rn = round_size(q, j);
+    if (g < rs + rn) break;
+    rs += rn;
+    ++j;
+  }
+  long long off = g - rs;
+  if (j < q.nb) {
+    if (off < q.nR) { stage = 0; b = j; idx = (int)off; return; }
+    off -= q.nR;
+  }
+  if (j >= 1 && j <= q.nb) {
+    if (off < q.nC) { stage = 1; b = j - 1; idx = (int)off; return; }
+    off -= q.nC;
+  }
+  stage = 2;
+  b = j - 2;
+  idx = (int)off;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void release_add(unsigned *p) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+
+}  // namespace fused
+
+template <int MM>
+__global__ void __launch_bounds__(256, 1)
+    spatial_fused_kernel(const __grid_constant__ CUtensorMap tmi, const __grid_constant__ CUtensorMap tmc,
+                         const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X,
+                         double2 *__restrict__ Yb, int YR, int nb, unsigned *__restrict__ done) {
+  using PL = rfft::Plan<10, 5>;   // both axes: 1024 points, 32 values x 32 threads per line
+  constexpr int N1 = PL::N, TPL = PL::TPL, E = PL::E, R = 1 << PL::BL, TW = PL::twsize();
+  constexpr int LG = PL::LOGN, NBLK = N1 / kBW, TC = 4, LT = 2, LS = N1 + 2, NS = 3, GT = 128;
+  constexpr int SH = PL::BL > 3 ? PL::BL : 3;
+  constexpr int SLOT = ((TC * LS * 16 + 1023) & ~1023) / 16;   // >= R / I items (4 lines x 1024)
+  extern __shared__ __align__(1024) unsigned char smraw_[];
+  unsigned char *smraw = align_smem_1024(smraw_);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  volatile int *slot_item = reinterpret_cast<volatile int *>(smraw + 64);
+  double2 *tw = reinterpret_cast<double2 *>(smraw + 128);
+  double2 *lamy = tw + TW;
+  double2 *ring = reinterpret_cast<double2 *>(smraw + 1024 + (((size_t)(TW + N1) * 16 + 1023) & ~(size_t)1023));
+  const int LINES = YR * MM;
+  const int gid = threadIdx.x / GT, t = threadIdx.x - gid * GT, l = t / TPL, tau = t - l * TPL;
+  const int gbar = 1 + gid;   // lines are warps (TPL = 32): __syncwarp exchanges, no line barriers
+  const fused::Seq q{nb, g.ny / YR, MM * (g.nx / TC), g.ny / YR};
+  const long long total = (long long)nb * (q.nR + q.nC + q.nI);
+  const double inv_n = 1.0 / ((double)g.nx * (double)g.ny);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      slot_item[s] = -1;
+    }
+    mbar_init_fence();
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmi) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmc) : "memory");
+  }
+  copy_table(tw, st.ptwx5, TW);
+  for (int P = threadIdx.x; P < N1; P += blockDim.x) lamy[P ^ ((P >> SH) & 7)] = __ldg(st.lamy + brev(P, LG));
+  __syncthreads();
+  auto item = [&](int k) { return (long long)blockIdx.x + (long long)k * gridDim.x; };
+  auto dep_ready = [&](int stage, int b) {
+    if (stage == 0) return true;
+    const unsigned need = stage == 1 ? (unsigned)q.nR : (unsigned)q.nC;
+    return fused::ld_acquire(done + (stage - 1) * nb + b) >= need;
+  };
+  auto issue_now = [&](int k) {   // dependency met (or none): arm the slot and start the copies
+    int stage, b, idx;
+    fused::decode(q, item(k), stage, b, idx);
+    const int p = __ldg(st.slots + b);
+    uint64_t *bar = full + k % NS;
+    double2 *dst = ring + (size_t)(k % NS) * SLOT;
+    if (stage == 1) {   // C: 4 S-slot columns (a half block) of plane (p, m)
+      const int bi = idx >> 1, half = idx & 1;
+      const int mm = bi / NBLK, blk = bi - mm * NBLK;
+      mbar_arrive_expect_tx(bar, (unsigned)(N1 * TC * 16));
+      for (int y = 0; y < N1; y += 256) tma_load_3d(dst + (size_t)y * TC, &tmc, 2 * TC * half, y, (p * MM + mm) * NBLK + blk, bar);
+    } else {            // R: natural rows of X; I: blocked rows of Yb
+      const int y0 = idx * YR;
+      mbar_arrive_expect_tx(bar, (unsigned)(LINES * N1 * 16));
+      for (int yy = 0; yy < YR; ++yy)
+        for (int m = 0; m < MM; ++m) {
+          double2 *d = dst + (size_t)(yy * MM + m) * N1;
+          if (stage == 0)
+            bulk_g2s(d, X + ((size_t)p * MM + m) * g.N + ((size_t)(y0 + yy) << LG), N1 * 16, bar);
+          else
+            tma_load_3d(d, &tmi, 0, y0 + yy, (p * MM + m) * NBLK, bar);
+        }
+    }
+    slot_item[k % NS] = k;
+  };
+  auto issue = [&](int k) {       // refill: start the copies now, or defer to the consumer of k
+    if (item(k) >= total) return;
+    int stage, b, idx;
+    fused::decode(q, item(k), stage, b, idx);
+    if (dep_ready(stage, b)) {
+      fused::fence_proxy_async_global();
+      issue_now(k);
+    } else {
+      slot_item[k % NS] = -(k + 2);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NS; ++k) issue(k);
+  for (int k = gid;; k += 2) {
+    const long long gi = item(k);
+    if (gi >= total) break;
+    int stage, b, idx;
+    fused::decode(q, gi, stage, b, idx);
+    const int s = k % NS;
+    double2 *tile = ring + (size_t)s * SLOT;
+    const int p = __ldg(st.slots + b);
+    // wait for the slot to hold item k (doing a deferred refill ourselves) and for its bytes
+    for (;;) {
+      const int v = slot_item[s];
+      if (v == k) break;
+      if (v == -(k + 2)) {
+        if (t == 0) {
+          const unsigned need = stage == 1 ? (unsigned)q.nR : (unsigned)q.nC;
+          while (fused::ld_acquire(done + (stage - 1) * nb + b) < need) __nanosleep(128);
+          fused::fence_proxy_async_global();
+          issue_now(k);
+        }
+        while (slot_item[s] != k) __nanosleep(32);
+        break;
+      }
+      __nanosleep(32);
+    }
+    mbar_wait(full + s, (unsigned)((k / NS) & 1));
+    double2 v[E];
+    if (stage == 0) {   // ---- R: S_p^{-1} over the natural rows, x-DIF, blocked store into Yb
+      const int y0 = idx * YR;
+      node_natural<MM>(tile, at.Sinv + (size_t)p * MM * MM, YR, N1, t, GT);
+      named_sync(gbar, GT);
+      const bool act = l < LINES;
+      double2 *line = tile + (size_t)(act ? l : 0) * N1;
+      if (act) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = line[rfft::natural_pos<PL>(tau, i)];
+        __syncwarp();
+        rfft::forward_regs<PL>(v, line, 0, tau, tw);
+      }
+      fence_proxy_async_smem();
+      named_sync(gbar, GT);
+      if (t == 0) issue(k + NS);
+      if (act) {
+        const int yy = l / MM, m = l - yy * MM;
+        double2 *dst = Yb + ((size_t)p * MM + m) * g.N;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[blocked(rfft::s_slot<PL>(tau, 0, r), y0 + yy, LG)] = v[r];
+      }
+      fused::fence_proxy_async_global();
+      named_sync(gbar, GT);
+      if (t == 0) fused::release_add(done + 0 * nb + b);
+    } else if (stage == 1) {   // ---- C: y-DIF, divide, y-DIT on 4 columns, in place in Yb
+      const int bi = idx >> 1, half = idx & 1;
+      const int mm = bi / NBLK, blk = bi - mm * NBLK;
+      const int qq = p * MM + mm;
+      const int c = l;   // 4 columns = the group's 4 warps
+      const int q0 = blk * kBW + half * TC;
+      double2 *xb = Yb + (size_t)qq * g.N + ((size_t)blk << (LG + 3)) + half * TC;
+      const double2 sh = __ldg(at.shift + qq);
+      const double2 lx = __ldg(st.lamx + brev(rfft::slot_to_pos<PL>(q0 + c), LG));
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int y = rfft::natural_pos<PL>(tau, i);
+        v[i] = tile[(y << LT) + (c ^ (((y << LT) >> 3) & (TC - 1)))];
+      }
+      named_sync(gbar, GT);
+      double2 *line = tile + (size_t)c * LS;
+      rfft::forward_regs<PL>(v, line, 0, tau, tw);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int P = rfft::last_pos<PL>(tau, 0, r);
+        const double2 lam = cadd(lx, lamy[P ^ ((P >> SH) & 7)]);
+        const double2 sl = cmul(sh, lam);
+        const double dr = 1.0 - sl.x, di = -sl.y;
+        const double q2 = dr * dr + di * di;
+        double rq = __drcp_rn(q2);
+        rq = fma(rq, fma(-q2, rq, 1.0), rq);
+        const double den = inv_n * rq;
+        v[r] = cmul(v[r], make_double2(dr * den, -di * den));
+      }
+      rfft::inverse_in_regs<PL>(v, line, 0, tau, tw);
+      rfft::to_smem<PL, 0>(v, line, tau);
+      named_sync(gbar, GT);
+      for (int i = t; i < (N1 << LT); i += GT) {
+        const int cc = i & (TC - 1), y = i >> LT;
+        xb[((size_t)y << 3) + cc] = tile[(size_t)cc * LS + rfft::F<PL>(y)];
+      }
+      fence_proxy_async_smem();
+      fused::fence_proxy_async_global();
+      named_sync(gbar, GT);
+      if (t == 0) {
+        fused::release_add(done + 1 * nb + b);
+        issue(k + NS);
+      }
+    } else {   // ---- I: x-DIT of the blocked rows, G_p^{-1} S_p on the way out to X
+      const int y0 = idx * YR;
+      const bool act = l < LINES;
+      double2 *line = tile + (size_t)(act ? l : 0) * N1;
+      if (act) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = line[rfft::s_slot<PL>(tau, 0, r)];
+        __syncwarp();
+        rfft::inverse_in_regs<PL>(v, line, 0, tau, tw);
+        rfft::to_smem<PL, 0>(v, line, tau);
+      }
+      named_sync(gbar, GT);
+      const double2 *A = at.SG + (size_t)p * MM * MM;
+      double2 ar[MM * MM];
+#pragma unroll
+      for (int i = 0; i < MM * MM; ++i) ar[i] = __ldg(A + i);
+      double2 *xp = X + (size_t)p * MM * g.N;
+      for (int i = t; i < YR * N1; i += GT) {
+        const int x = i & (N1 - 1), r2 = i >> LG;
+        const double2 *base = tile + (size_t)r2 * MM * N1 + rfft::F<PL>(x);
+        double2 w[MM];
+#pragma unroll
+        for (int j = 0; j < MM; ++j) w[j] = base[j * N1];
+        double2 *o = xp + ((size_t)(y0 + r2) << LG) + x;
+#pragma unroll
+        for (int m2 = 0; m2 < MM; ++m2) {
+          double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int j = 0; j < MM; ++j) acc = cfma(ar[m2 * MM + j], w[j], acc);
+          o[(size_t)m2 * g.N] = acc;
+        }
+      }
+      fence_proxy_async_smem();
+      named_sync(gbar, GT);
+      if (t == 0) issue(k + NS);
+    }
+  }
+}
+
 struct PipePlan {
   int YR, G, NS;           // R / I: rows per item, groups, slots
   int lT, GC, NSC, ls, BR; // C: log2 columns per item, groups (1: 255 registers, 2: 128), slots, line stride, box rows
@@ -1215,7 +1493,63 @@ cudaError_t launch_tfft_l(const Geometry &g, const StaticTables &st, const Alpha
   return cudaGetLastError();
 }
 
+template <int MM>
+cudaError_t launch_fused(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X, double2 *Yb,
+                         unsigned *done, cudaStream_t s) {
+  using PL = rfft::Plan<10, 5>;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int YR = MM == 3 ? 1 : 4 / MM;
+  int nb = st.nsolve;
+  CUtensorMap tmi, tmc;
+  if (!blocked_map(g, Yb, 2 * kBW, 1, g.nx / kBW, CU_TENSOR_MAP_SWIZZLE_NONE, tmi) ||
+      !blocked_map(g, Yb, 8, 256, 1, CU_TENSOR_MAP_SWIZZLE_64B, tmc))
+    return cudaErrorNotSupported;
+  const size_t slot = ((size_t)4 * (1024 + 2) * 16 + 1023) & ~(size_t)1023;
+  const size_t smem = 1024 + 1024 + (((size_t)(PL::twsize() + 1024) * 16 + 1023) & ~(size_t)1023) + 3 * slot;
+  const void *fn = (const void *)spatial_fused_kernel<MM>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem)) != cudaSuccess) return e;
+  if (per < 1) return cudaErrorInvalidConfiguration;
+  if ((e = cudaMemsetAsync(done, 0, 2 * (size_t)nb * sizeof(unsigned), s)) != cudaSuccess) return e;
+  Geometry gg = g;
+  StaticTables sst = st;
+  AlphaTables aat = at;
+  double2 *xx = X, *yy = Yb;
+  int yr = YR;
+  unsigned *dd = done;
+  void *args[] = {(void *)&tmi, (void *)&tmc, &gg, &sst, &aat, &xx, &yy, &yr, &nb, &dd};
+  // cooperative: all CTAs resident (the cross-CTA dependency waits need it)
+  e = cudaLaunchCooperativeKernel(fn, dim3(sms), dim3(256), args, smem, s);
+  record_launch(s);
+  return e;
+}
+
 }  // namespace
+
+// Measured on config 5: 63 ms against 46-50 ms for the three launches — ncu shows the same
+// 206 GB of DRAM traffic (three 64 MB slots in flight do not stay in the 126 MB L2), 38 % fp64,
+// instruction-cache stalls from the three unrolled item bodies.  Kept as an A/B option only
+// (PINT_FUSED=1, experiments build).
+bool spatial_fused_supported(const Geometry &g, const StaticTables &st) {
+  const char *e = experiment_env("PINT_FUSED");
+  if (!e || !atoi(e)) return false;
+  return g.dim == 2 && g.pow2 && g.lognx == 10 && g.logny == 10 && g.M <= 4 && st.P == 1 && !st.packed &&
+         st.nsolve >= 1;
+}
+
+cudaError_t launch_spatial_fused(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
+                                 double2 *Yb, unsigned *sync, cudaStream_t s) {
+  if (!spatial_fused_supported(g, st) || Yb == X) return cudaErrorInvalidValue;
+  switch (g.M) {
+    case 1: return launch_fused<1>(g, st, at, X, Yb, sync, s);
+    case 2: return launch_fused<2>(g, st, at, X, Yb, sync, s);
+    case 3: return launch_fused<3>(g, st, at, X, Yb, sync, s);
+    default: return launch_fused<4>(g, st, at, X, Yb, sync, s);
+  }
+}
 
 bool spatial_pipe_geometry(const Geometry &g) {
   PipePlan pp;
