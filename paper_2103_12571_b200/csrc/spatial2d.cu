@@ -848,9 +848,7 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
         const double2 sl = cmul(sh, lam);
         const double dr = 1.0 - sl.x, di = -sl.y;
         const double qq = dr * dr + di * di;
-        double rq = __drcp_rn(qq);
-        rq = fma(rq, fma(-qq, rq, 1.0), rq);
-        const double den = inv_n * rq;
+        const double den = inv_n * __drcp_rn(qq);   // correctly rounded reciprocal
         v[u * R + r] = cmul(v[u * R + r], make_double2(dr * den, -di * den));
       }
     rfft::inverse_in_regs<PY>(v, line, lid, tau, twy);
@@ -1086,9 +1084,7 @@ __global__ void __launch_bounds__(256, 1)
         const double2 sl = cmul(sh, lam);
         const double dr = 1.0 - sl.x, di = -sl.y;
         const double q2 = dr * dr + di * di;
-        double rq = __drcp_rn(q2);
-        rq = fma(rq, fma(-q2, rq, 1.0), rq);
-        const double den = inv_n * rq;
+        const double den = inv_n * __drcp_rn(q2);
         v[r] = cmul(v[r], make_double2(dr * den, -di * den));
       }
       rfft::inverse_in_regs<PL>(v, line, 0, tau, tw);

@@ -64,3 +64,26 @@ def test_forcing_rejects_incompatible_modes():
     s.set_forcing(None)
     s.set_form("direct")
     s.close()
+
+
+def test_w_inf_and_algorithm2_gamma_with_forcing():
+    """||w||_inf with a forcing attached is the max over the assembled w = (u0 + v_0, v_1, ...)
+    (P:105), and Algorithm 2 takes gamma = L (3 eps + tau) ||w||_inf from it: the
+    driver's alphas equal the a-priori schedule of that ||w||_inf."""
+    import paper_2103_12571_b200 as PB
+    from oracle.paralpha import w_vector
+    p = W.reduced(5)
+    u0 = p.u0()
+    rng = np.random.default_rng(3)
+    field = 40.0 * (rng.standard_normal(p.N) + 1j * rng.standard_normal(p.N))   # dominates ||u0||
+    v = forcing_vector(p, Tableau(p.M), lambda t: np.cos(t) * field)
+    s = PB.Solver(p, u0)
+    assert s.w_inf() == pytest.approx(float(np.abs(u0).max()), rel=1e-15)
+    s.set_forcing(v)
+    want = float(np.abs(w_vector(p, u0, v)).max())
+    assert s.w_inf() == pytest.approx(want, rel=1e-14)
+    tol = 1e-9 * want
+    res = s.solve(p.m0, tol, 6, p.eps, p.tau)
+    a_or, m_or = oracle_schedule(p.L, want, p.m0, res["iters"], p.eps, p.tau)
+    np.testing.assert_allclose(res["m"], m_or[:res["iters"] + 1], rtol=1e-13)
+    s.close()

@@ -235,3 +235,30 @@ def test_parity_pipe_plans_sharded(P):
         g.iterate(1)
         assert relative_l2(g.get_iterate(), u) <= TOL, k
     g.close()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_cuda_graph_replay_matches_iterate(cfg):
+    """pint_graph_create / pint_graph_launch (launch-bound configs): n captured iterations replayed
+    on the current buffers equal n pint_iterate calls with the same (fixed) alpha."""
+    import paper_2103_12571_b200 as PB
+    import torch
+    p = W.CONFIGS[cfg]
+    u0 = p.u0()
+    a = [p.alpha_fixed] * 8
+    s1 = PB.Solver(p, u0, stream=torch.cuda.Stream())
+    s2 = PB.Solver(p, u0)
+    s1.set_alpha_schedule(a)
+    s2.set_alpha_schedule(a)
+    h = s1.graph_create(2)              # captures iterations 0, 1 (not executed by the capture)
+    np.testing.assert_array_equal(s1.get_iterate(), s2.get_iterate())
+    for _ in range(3):
+        s1.graph_launch(h)
+    s1.stream.synchronize()
+    s2.iterate(6)
+    np.testing.assert_array_equal(s1.get_iterate(), s2.get_iterate())   # same kernels, same order
+    s1.graph_destroy(h)
+    with pytest.raises(PB.PintError):
+        s1.set_phase_timing(True)       # one rank: no phases
+    s1.close()
+    s2.close()
