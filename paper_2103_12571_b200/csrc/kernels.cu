@@ -515,12 +515,23 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
     double2 *dst = sm + r * W;
     for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
   }
+  // the H-term block (last node of step l - 1, or u0 for global step 0) is staged with the tile, so
+  // the point loop below has no global load whose latency it would expose
+  double2 *hb = sm + M * H * W;   // [BY][BX]
+  {
+    const int jj = l - st.prev_shift;
+    const double2 *hsrc = jj < 0 ? st.u0 : st.prev_base + (long long)jj * st.prev_stride;
+    for (int r = warp; r < BY; r += blockDim.x >> 5) {
+      const double2 *src = hsrc + ((size_t)(y0 + r) << g.lognx) + x0;
+      for (int xx = lane; xx < BX; xx += 32) cp_async16(hb + r * BX + xx, src + xx);
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
   for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
     const int ty = pt / BX, tx = pt - ty * BX;
     const int n = ((y0 + ty) << g.lognx) + x0 + tx;
-    const double2 base = prev_value(st, l, n);
+    const double2 base = hb[pt];
     double2 uc[M], Au[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
@@ -1415,8 +1426,9 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     residual_block(g, BX, BY);
     if (pk && BY > g.ny / 2) BY = g.ny / 2;
     const int hw = g.hw < 1 ? 1 : g.hw;
-    auto rbytes = [&](int bx, int by) {
-      return (size_t)g.M * (bx + 2 * hw) * (by + 2 * hw) * (pk ? 2 * sizeof(double) : sizeof(double2));
+    auto rbytes = [&](int bx, int by) {   // tile + (complex storage) the staged H-term block
+      return (size_t)g.M * (bx + 2 * hw) * (by + 2 * hw) * (pk ? 2 * sizeof(double) : sizeof(double2)) +
+             (pk ? 0 : (size_t)bx * by * sizeof(double2));
     };
     while (rbytes(BX, BY) > 200 * 1024) {   // wide halos at large M: smaller blocks
       if (BY > 1) BY >>= 1;
