@@ -180,7 +180,7 @@ pint_status pint_set_form(pint_ctx *c, int32_t form);
  * roundoff imaginary parts), switching off converts back to complex128.  pint_get_iterate and
  * pint_get_final_value still return (re, 0) pairs.  Requirements: nranks == 1, u0 real (imaginary
  * parts exactly 0; pint_set_initial_value then rejects non-real data), 2-D: grids of the register
- * FFT engine, 4 <= L <= 1024; 1-D: N >= 8; not with pint_sequential.  Errors:
+ * FFT engine, 4 <= L <= 1024; 1-D: N >= 8 and L >= 2; not with pint_sequential.  Errors:
  * PINT_ERR_INVALID, PINT_ERR_CUDA (storage conversion). */
 pint_status pint_set_hermitian(pint_ctx *c, int32_t on);
 

@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libpint.so")
 # A/B experiment library (-DPINT_EXPERIMENTS: reads the PINT_* switches of internal.h); never the
 # product: bench.py refuses it unless --allow-experiments, and records it
 LIB_EXP = os.path.join(HERE, "libpint_exp.so")
-SOURCES = ["kernels.cu", "spatial2d.cu", "generic.cu", "pint_abi.cpp", "host_numerics.cpp"]
+SOURCES = ["kernels.cu", "spatial2d.cu", "pcr1d.cu", "generic.cu", "pint_abi.cpp", "host_numerics.cpp"]
 HEADERS = ["internal.h", "host_numerics.h", "fft_reg.cuh", "device_common.cuh", "residual.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 LIBS = ["-lnccl"]
@@ -39,8 +39,23 @@ def build(verbose: bool = False, force: bool = False, experiments: bool = False)
         return lib
     os.makedirs(objdir, exist_ok=True)
     log = os.path.join(HERE, "build_exp.log" if experiments else "build.log")
+    hdr_time = max(os.path.getmtime(d) for d in deps if d not in srcs)
+
+    def obj_of(src: str) -> str:
+        return os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")
+
+    def fresh(src: str) -> bool:   # incremental: an object newer than its source and every header
+        o = obj_of(src)
+        return (not force and os.path.exists(o) and os.path.getmtime(o) >= os.path.getmtime(src)
+                and os.path.getmtime(o) >= hdr_time)
+
+    def unit(src: str):
+        if fresh(src):
+            return obj_of(src), subprocess.CompletedProcess([src, "(up to date)"], 0, "", "")
+        return _compile(src, objdir, extra)
+
     with cf.ThreadPoolExecutor(len(srcs)) as ex:
-        results = list(ex.map(lambda src: _compile(src, objdir, extra), srcs))
+        results = list(ex.map(unit, srcs))
     text = "".join(" ".join(r.args) + "\n" + r.stdout + r.stderr for _, r in results)
     failed = [r for _, r in results if r.returncode != 0]
     if not failed:

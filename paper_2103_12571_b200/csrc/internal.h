@@ -108,6 +108,12 @@ struct LaunchCfg {
 
 LaunchCfg choose_launch(const Geometry &g);
 
+// 1-D pipelined PCR passes (pcr1d.cu): classes of 256 points, one tridiagonal factor
+bool pcr1d_pipe_supported(const Geometry &g, int R);
+bool pcr1d_path(const Geometry &g, const LaunchCfg &lc);
+cudaError_t launch_pcr1d_pipe(const Geometry &g, const AlphaTables &at, double2 *X, double2 *Y, const int *slots,
+                              int lines, int R, cudaStream_t s);
+
 // 2-D spatial solves as one persistent L2-resident pipeline (spatial2d.cu)
 struct SpatialPlan {
   int lines;                  // planes (p, m) to solve

@@ -1250,6 +1250,11 @@ static bool reg2d(const Geometry &g) {
 }
 bool reg2d_path(const Geometry &g) { return reg2d(g); }
 
+// the 1-D two-pass solve runs on the pipelined passes of pcr1d.cu (correction form)
+bool pcr1d_path(const Geometry &g, const LaunchCfg &lc) {
+  return g.dim == 1 && lc.pcr_mode == 1 && pcr1d_pipe_supported(g, lc.pcr_R) && !experiment_env("PINT_PCR_LEGACY");
+}
+
 LaunchCfg choose_launch(const Geometry &g) {
   LaunchCfg lc{};
   // forward/backward tile: as many spatial points as fit ~100 KB (2 CTAs per SM), <= 16
@@ -1278,6 +1283,8 @@ LaunchCfg choose_launch(const Geometry &g) {
     } else {
       lc.pcr_mode = 1;
       int jA = g.logN / 2;            // R = 2^jA classes of length N/R
+      // pipelined passes (pcr1d.cu): classes of 256 points (strides >= N/256 in the class pass)
+      if (pcr1d_pipe_supported(g, 1 << (g.logN - 8)) && !experiment_env("PINT_PCR_LEGACY")) jA = g.logN - 8;
       lc.pcr_chunk = g.nfac > 1 ? 2048 : 4096;
       // The chunk kernel updates at most kChunkThreads * kChunkIPT values per level, so the tile
       // C + 2 F R (chunk + halos) must fit it (every nfac: N = 2^20 with F = 1 gives R = 1024 and
@@ -1312,6 +1319,7 @@ int launches_per_iteration(const Geometry &g, const LaunchCfg &lc, const StaticT
 const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i) {
   static const char *k1a[] = {"fwd_kernel", "pcr_classes_kernel", "bwd_kernel"};
   static const char *k1b[] = {"fwd_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
+  static const char *k1p[] = {"fwd_kernel", "pcr_cls_pipe_kernel", "pcr_chunk_pipe_kernel", "bwd_kernel"};
   static const char *k2[] = {"residual2d_kernel", "tfft_fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
                              "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
   static const char *k2p[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial2d_kernel", "tfft_bwd_kernel"};
@@ -1333,7 +1341,7 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
     }
     return nm;
   }
-  return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
+  return lc.pcr_mode == 0 ? k1a[i] : (pcr1d_path(g, lc) ? k1p[i] : k1b[i]);
 }
 
 static cudaError_t set_smem(const void *fn, size_t bytes, bool max_carveout = false) {
@@ -1490,6 +1498,10 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
     } else {
       const int R = lc.pcr_R, T = lc.pcr_T;
       const int jOff = __builtin_ctz((unsigned)R);
+      if (pcr1d_path(g, lc)) {   // pipelined class + chunk passes (pcr1d.cu), each launch recorded
+        *out = b.Y;
+        return launch_pcr1d_pipe(g, at, b.X, b.Y, st.slots, lines, R, s);
+      }
       const int nq = g.N / R;
       size_t smem = (size_t)nq * T * sizeof(double2);
       constexpr int E = 8;

@@ -62,12 +62,16 @@ def test_fuzz_parity(case):
             s.set_hermitian(True)
         except PB.PintError as e:
             s.close()
-            # documented requirement (pint.h): 2-D real-data mode only on the register-engine grids
-            # (|log2 nx - log2 ny| <= 1); the rejection must be that one, then the case is done
+            # documented requirements (pint.h): 1-D needs N >= 8 and L >= 2; 2-D runs only on the
+            # register-engine grids (|log2 nx - log2 ny| <= 1, 4 <= L <= 1024); the rejection must
+            # be one of those, then the case is done
             lx, ly, lL = int(np.log2(p.nx)), int(np.log2(p.ny)), int(np.log2(p.L))
-            supported = (2 <= lx <= 12 and 2 <= ly <= 12 and abs(lx - ly) <= 1 and 2 <= lL <= 10
-                         and max(p.nx // 16, 1) * p.M <= 256)
-            assert e.status == 1 and p.dim == 2 and not supported, str(e)
+            if p.dim == 1:
+                supported = p.nx >= 8 and p.L >= 2
+            else:
+                supported = (2 <= lx <= 12 and 2 <= ly <= 12 and abs(lx - ly) <= 1 and 2 <= lL <= 10
+                             and max(p.nx // 16, 1) * p.M <= 256)
+            assert e.status == 1 and not supported, str(e)
             return
     if form == "direct":
         s.set_form("direct")

@@ -70,6 +70,20 @@ def test_parity_two_pass_pcr_small():
     run_parity(p)
 
 
+# the pipelined 1-D PCR passes (pcr1d.cu) serve 8192 <= N <= 65536 with classes of 256 points:
+# R = N/256 = 32 .. 256 (chunk levels 5 .. 8), heat (symmetric levels) and centred advection
+# (antisymmetric level 0), chunk tiles wrapping at both line ends
+PIPE1D = [W.CONFIGS[3].replace(name="pcr1d_heat_N8192_L8", nx=8192, L=8, iters=3),
+          W.CONFIGS[3].replace(name="pcr1d_heat_N32768_M2_L4", nx=32768, M=2, L=4, iters=3),
+          W.CONFIGS[2].replace(name="pcr1d_adv_N16384_L8", nx=16384, L=8, iters=3),
+          W.CONFIGS[2].replace(name="pcr1d_adv_N65536_M2_L4", nx=65536, M=2, L=4, iters=2)]
+
+
+@pytest.mark.parametrize("p", PIPE1D, ids=lambda p: p.name)
+def test_parity_pcr1d_pipe(p):
+    run_parity(p)
+
+
 def test_last_step_diff_and_residual_norm():
     p = W.CONFIGS[2].replace(L=16, iters=4)
     u0 = p.u0()
