@@ -108,6 +108,9 @@ struct LaunchCfg {
 
 LaunchCfg choose_launch(const Geometry &g);
 
+// cuTensorMapEncodeTiled from the driver (a PFN_cuTensorMapEncodeTiled_v12000), or nullptr
+void *tma_encode_fn();
+bool fwd1d_tma_ok(const Geometry &g, const StaticTables &st, int T);
 // 1-D pipelined PCR passes (pcr1d.cu): classes of 256 points, one tridiagonal factor
 bool pcr1d_pipe_supported(const Geometry &g, int R);
 bool pcr1d_path(const Geometry &g, const LaunchCfg &lc);

@@ -14,6 +14,8 @@
 // kernels are organised around full-tile shared-memory staging with 16-byte coalesced global
 // accesses and are measured against the HBM roof; the FFT-heavy ones end up latency bound on
 // shared memory and fp64 dependencies (§5b).  No tensor cores: no dense contraction on this path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -137,6 +139,142 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       if (st.twr) v = cmul(v, __ldg(st.twr + row / M));
       X[(size_t)row * g.N + n0 + t] = v;
     }
+  }
+}
+
+// 1-D forward tile with the u tile staged by the TMA unit (one rank, complex storage, 3-point
+// stencils, T = 4): same arithmetic as fwd_kernel<M, true, true> without its per-thread stencil
+// loads (which kept the L1 data pipe at 90 %, half of it global-load wavefronts for 64-byte rows).
+// Persistent (one CTA per SM) with two consumer groups of 256 threads over a ring of NS slots:
+// slot = the tile [l][m][t] (box {T, M, L} of the tensor map over u, 64-byte swizzle: element a
+// at swz64(a)), then the halo columns n0 - 1 and n0 + T as [l][m] arrays (16-byte box columns;
+// wrapped column indices make the line periodic).  The group that finishes tile k refills its
+// slot with tile k + NS (ring order = tile order).  Thread l of a group evaluates the residual of
+// step l for all t and m with a sliding window along t (it first reads the H-term row l - 1 into
+// registers; a group barrier separates those reads from the in-place writes of r), then the
+// group runs the L-point DIF FFT on the swizzled tile (twiddles staged once per CTA) and
+// S_p^{-1} writes X.
+constexpr int kFwdTmaGT = 256, kFwdTmaG = 2;
+
+template <int M>
+__global__ void __launch_bounds__(kFwdTmaGT * kFwdTmaG, 1)
+    fwd1d_tma_kernel(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmh, Geometry g,
+                     StaticTables st, AlphaTables at, double2 *__restrict__ X, int NS, int ntiles) {
+  constexpr int T = 4;
+  extern __shared__ __align__(16) unsigned char smraw_[];
+  unsigned char *smb;   // 1024-byte aligned (the 64-byte swizzle pattern follows smem address bits 7-8)
+  {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smraw_);
+    smb = smraw_ + (((a + 1023u) & ~1023u) - a);
+  }
+  const int L = g.L, N = g.N;
+  const int rows = L * M, all = rows * T;
+  const size_t slot_elems = (size_t)rows * (T + 2);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smb);
+  volatile int *slot_item = reinterpret_cast<volatile int *>(smb + 64);
+  double2 *tw = reinterpret_cast<double2 *>(smb + 1024);
+  double2 *ring = reinterpret_cast<double2 *>(smb + 1024 + (((size_t)L * sizeof(double2) + 1023) & ~(size_t)1023));
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < NS; ++s2) {
+      mbar_init(full + s2, 1);
+      slot_item[s2] = -1;
+    }
+    mbar_init_fence();
+  }
+  for (int i = threadIdx.x; i < L; i += blockDim.x) tw[i] = __ldg(st.twL + i);
+  __syncthreads();
+  auto issue = [&](int k) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= ntiles) return;
+    const int n0 = it * T;
+    uint64_t *bar = full + k % NS;
+    double2 *sl = ring + (size_t)(k % NS) * slot_elems;
+    mbar_arrive_expect_tx(bar, (unsigned)((all + 2 * rows) * sizeof(double2)));
+    tma_load_3d(sl, &tmu, 2 * n0, 0, 0, bar);
+    tma_load_3d(sl + all, &tmh, 2 * ((n0 - 1 + N) & (N - 1)), 0, 0, bar);
+    tma_load_3d(sl + all + rows, &tmh, 2 * ((n0 + T) & (N - 1)), 0, 0, bar);
+    slot_item[k % NS] = k;
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NS; ++k) issue(k);
+  const int gid = threadIdx.x / kFwdTmaGT;
+  const Grp gp{(int)threadIdx.x - gid * kFwdTmaGT, kFwdTmaGT, 1 + gid};
+  const int l = gp.tid;
+  const double wl = g.wx[2], wc = g.wx[3], wr = g.wx[4];
+  const size_t plane = (size_t)M * N;
+  for (int k = gid;; k += kFwdTmaG) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= ntiles) break;
+    const int n0 = it * T;
+    double2 *sm = ring + (size_t)(k % NS) * slot_elems;
+    const double2 *hl = sm + all, *hr = hl + rows;
+    auto U = [&](int ll, int m, int t) -> double2 & { return sm[swz64((ll * M + m) * T + t)]; };
+    while (slot_item[k % NS] != k) __nanosleep(32);
+    mbar_wait(full + k % NS, (unsigned)((k / NS) & 1));
+    // (i) residual + alpha^{l/L}, one step l per thread
+    double2 h[T];
+    if (l < L) {
+#pragma unroll
+      for (int t = 0; t < T; ++t) h[t] = l == 0 ? __ldg(st.u0 + n0 + t) : U(l - 1, M - 1, t);
+    }
+    gp.sync();   // every H-term read of row l - 1 precedes the writes of row l - 1
+    if (l < L) {
+      const double sc = __ldg(at.scale_fwd + l);
+      double2 lv[M], cv[M], rv[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        lv[j] = hl[l * M + j];
+        cv[j] = U(l, j, 0);
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) rv[j] = t + 1 < T ? U(l, j, t + 1) : hr[l * M + j];
+        double2 Au[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          Au[j].x = fma(wl, lv[j].x, fma(wc, cv[j].x, wr * rv[j].x));
+          Au[j].y = fma(wl, lv[j].y, fma(wc, cv[j].y, wr * rv[j].y));
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          double2 acc = csub(h[t], cv[m]);
+          if (st.v) acc = cadd(acc, __ldg(st.v + ((size_t)l * M + m) * N + n0 + t));   // forcing part of w
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            const double q = g.dTQ[m * M + j];
+            acc.x = fma(q, Au[j].x, acc.x);
+            acc.y = fma(q, Au[j].y, acc.y);
+          }
+          U(l, m, t) = cscale(acc, sc);   // this row's u values at t are no longer needed
+        }
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          lv[j] = cv[j];
+          cv[j] = rv[j];
+        }
+      }
+    }
+    gp.sync();
+    // (ii) L-point DIF FFT along l for the M*T columns, (iii) S_p^{-1} -> X
+    fft_dif_g<3>(sm, M * T, 1, M * T, g.logL, tw, gp);
+    for (int i = gp.tid; i < rows; i += gp.nt) {
+      const int m = i % M, p = i / M;
+      double2 srow[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
+      double2 *dst = X + (size_t)p * plane + (size_t)m * N + n0;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) acc = cfma(srow[j], U(p, j, t), acc);
+        dst[t] = acc;
+      }
+    }
+    fence_proxy_async_smem();   // this thread's generic accesses of the slot before the refill
+    gp.sync();
+    if (gp.tid == 0) issue(k + NS);
   }
 }
 
@@ -1214,6 +1352,14 @@ static int num_sms() {
 
 size_t fwd_smem_bytes(const Geometry &g, int T) { return (size_t)g.L * g.M * T * sizeof(double2); }
 
+// the TMA-staged 1-D forward tile (fwd1d_tma_kernel): one rank, complex storage, 3-point stencil,
+// T = 4, L <= 256 (one step per thread), 128-byte aligned halo arrays, >= 3 CTAs per SM
+bool fwd1d_tma_ok(const Geometry &g, const StaticTables &st, int T) {
+  return g.dim == 1 && g.pow2 && st.P == 1 && !st.packed && g.hw <= 1 && T == 4 && g.N >= 8 && g.L >= 8 &&
+         g.L <= 256 && (g.L * g.M) % 32 == 0 && g.M <= 4 && 2048 + (size_t)g.L * 16 + 2 * (size_t)g.L * g.M * 6 * sizeof(double2) <= 227 * 1024 &&
+         tma_encode_fn() != nullptr && !experiment_env("PINT_FWD_LEGACY");
+}
+
 // 2-D path selection: default = all-node time tiles + the persistent spatial pipeline
 // (spatial2d.cu); PINT_LEGACY2D=1 selects the six-pass path (A/B measurements only).
 static bool legacy_pipe() {   // A/B: the fused persistent spatial2d kernel instead of the pipelined passes
@@ -1320,6 +1466,7 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
   static const char *k1a[] = {"fwd_kernel", "pcr_classes_kernel", "bwd_kernel"};
   static const char *k1b[] = {"fwd_kernel", "pcr_classes_kernel", "pcr_chunk_kernel", "bwd_kernel"};
   static const char *k1p[] = {"fwd_kernel", "pcr_cls_pipe_kernel", "pcr_chunk_pipe_kernel", "bwd_kernel"};
+  if (g.dim == 1 && i == 0 && fwd1d_tma_ok(g, st, lc.fwd_T)) return "fwd1d_tma_kernel";
   static const char *k2[] = {"residual2d_kernel", "tfft_fwd_kernel", "fft2d_rows_kernel<fwd>", "fft2d_cols_kernel",
                              "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
   static const char *k2p[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial2d_kernel", "tfft_bwd_kernel"};
@@ -1412,7 +1559,40 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
   const size_t smem = fwd_smem_bytes(g, T) + (size_t)g.L * sizeof(double2);   // + staged twiddles
   const int grid = (st.packed ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
-  if (g.dim == 1) {
+  if (g.dim == 1 && fwd1d_tma_ok(g, st, T)) {   // TMA-staged tile (the product 1-D path)
+    CUtensorMap tmu, tmh;
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * g.N, (cuuint64_t)g.M, (cuuint64_t)g.L};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.N * 16, (cuuint64_t)g.M * g.N * 16};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const cuuint32_t BL = (cuuint32_t)g.L;
+    const cuuint32_t boxu[3] = {2 * 4, (cuuint32_t)g.M, BL}, boxh[3] = {2, (cuuint32_t)g.M, BL};
+    if (!enc ||
+        enc(&tmu, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.u, dims, strides, boxu, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&tmh, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.u, dims, strides, boxh, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorNotSupported;
+    const size_t slot = (size_t)g.L * g.M * (4 + 2) * sizeof(double2);
+    const size_t head = 1024 + (((size_t)g.L * sizeof(double2) + 1023) & ~(size_t)1023);
+    int NS = 3;
+    while (NS > 2 && 1024 + head + NS * slot > 227 * 1024) --NS;
+    const size_t sm1 = 1024 + head + NS * slot;
+    const int ntiles = g.N / 4;
+    int grid = num_sms();
+    if (grid > ntiles) grid = ntiles;
+    switch (g.M) {
+#define PINT_FWDT(MM_)                                                                                        \
+  case MM_:                                                                                                   \
+    e = set_smem((const void *)fwd1d_tma_kernel<MM_>, sm1);                                                   \
+    if (e == cudaSuccess)                                                                                     \
+      fwd1d_tma_kernel<MM_><<<grid, kFwdTmaGT * kFwdTmaG, sm1, s>>>(tmu, tmh, g, st, at, b.X, NS, ntiles);          \
+    break;
+      PINT_FWDT(1) PINT_FWDT(2) PINT_FWDT(3) default: PINT_FWDT(4)
+#undef PINT_FWDT
+    }
+    rec(s);
+  } else if (g.dim == 1) {
 #define PINT_FWD1(NODE_, PACK_, HW_)                                                              \
   e = set_smem((const void *)fwd_kernel<MM, true, NODE_, PACK_, HW_>, smem);                       \
   if (e == cudaSuccess) fwd_kernel<MM, true, NODE_, PACK_, HW_><<<grid, kTileThreads, smem, s>>>(g, st, at, b.u, b.X, T);

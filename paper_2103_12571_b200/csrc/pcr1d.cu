@@ -386,22 +386,22 @@ __global__ void __launch_bounds__(G * (CC + 2 * kCH) / kE, 1)
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+constexpr int kClsG = 2, kClsNS = 4;              // class pass: 2 groups of 128 threads, 4 x 32 KB slots
+constexpr int kChkCC = 2048, kChkG = 2, kChkNS = 4;  // chunk pass: 2 groups of 160 threads, 4 x 40 KB slots
+
+}  // namespace
+
+void *tma_encode_fn() {
+  static void *fn = nullptr;
   if (!fn) {
     void *ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+      fn = ptr;
   }
   return fn;
 }
-
-constexpr int kClsG = 2, kClsNS = 4;              // class pass: 2 groups of 128 threads, 4 x 32 KB slots
-constexpr int kChkCC = 2048, kChkG = 2, kChkNS = 4;  // chunk pass: 2 groups of 160 threads, 4 x 40 KB slots
-
-}  // namespace
 
 bool pcr1d_pipe_supported(const Geometry &g, int R) {
   return g.dim == 1 && g.pow2 && g.nfac == 1 && g.N >= 8192 && g.N <= 65536 && g.N == kNQ * R && R >= 32 &&
@@ -416,7 +416,7 @@ cudaError_t launch_pcr1d_pipe(const Geometry &g, const AlphaTables &at, double2 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int jA = __builtin_ctz((unsigned)R);
   const bool sym = g.op == 0 || g.op == 1;   // centred 3-point heat / advection (see upd)
-  auto enc = encoder();
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tm;
   {

@@ -84,6 +84,18 @@ def test_parity_pcr1d_pipe(p):
     run_parity(p)
 
 
+# the TMA-staged 1-D forward tile (fwd1d_tma_kernel) runs where the tile is 4 points wide
+# (512 < L M <= 1024, L <= 256): config 3's shape at small N, both operators, M = 3 and 4
+FWD1D = [W.CONFIGS[3].replace(name="fwd1d_heat_N256_L256", nx=256, L=256, iters=3),
+         W.CONFIGS[2].replace(name="fwd1d_adv_N512_M4_L256", nx=512, M=4, L=256, iters=3),
+         W.CONFIGS[3].replace(name="fwd1d_heat_N8192_L256_twopass", nx=8192, L=256, iters=2)]
+
+
+@pytest.mark.parametrize("p", FWD1D, ids=lambda p: p.name)
+def test_parity_fwd1d_tma(p):
+    run_parity(p)
+
+
 def test_last_step_diff_and_residual_norm():
     p = W.CONFIGS[2].replace(L=16, iters=4)
     u0 = p.u0()
