@@ -158,8 +158,9 @@ constexpr int kFwdTmaGT = 256, kFwdTmaG = 2;
 
 template <int M>
 __global__ void __launch_bounds__(kFwdTmaGT * kFwdTmaG, 1)
-    fwd1d_tma_kernel(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmh, Geometry g,
-                     StaticTables st, AlphaTables at, double2 *__restrict__ X, int NS, int ntiles) {
+    fwd1d_tma_kernel(const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmh,
+                     const __grid_constant__ CUtensorMap tmx, Geometry g, StaticTables st, AlphaTables at, int NS,
+                     int ntiles) {
   constexpr int T = 4;
   extern __shared__ __align__(16) unsigned char smraw_[];
   unsigned char *smb;   // 1024-byte aligned (the 64-byte swizzle pattern follows smem address bits 7-8)
@@ -201,7 +202,6 @@ __global__ void __launch_bounds__(kFwdTmaGT * kFwdTmaG, 1)
   const Grp gp{(int)threadIdx.x - gid * kFwdTmaGT, kFwdTmaGT, 1 + gid};
   const int l = gp.tid;
   const double wl = g.wx[2], wc = g.wx[3], wr = g.wx[4];
-  const size_t plane = (size_t)M * N;
   for (int k = gid;; k += kFwdTmaG) {
     const int it = blockIdx.x + k * gridDim.x;
     if (it >= ntiles) break;
@@ -258,24 +258,40 @@ __global__ void __launch_bounds__(kFwdTmaGT * kFwdTmaG, 1)
     gp.sync();
     // (ii) L-point DIF FFT along l for the M*T columns, (iii) S_p^{-1} -> X
     fft_dif_g<3>(sm, M * T, 1, M * T, g.logL, tw, gp);
-    for (int i = gp.tid; i < rows; i += gp.nt) {
-      const int m = i % M, p = i / M;
-      double2 srow[M];
+    // (iii) S_p^{-1} in place, one (p, m) row per item: all reads, a group barrier, the writes
+    const int pstep = kFwdTmaGT / M;   // whole slots per pass: a slot's rows are read before any is written
+    const int mi = gp.tid % M, pi = gp.tid / M;
+    for (int p0 = 0; p0 < L; p0 += pstep) {
+      const int m = mi, p = p0 + pi;
+      const bool act = pi < pstep && p < L;
+      double2 acc[T];
+      if (act) {
+        double2 srow[M];
 #pragma unroll
-      for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
-      double2 *dst = X + (size_t)p * plane + (size_t)m * N + n0;
+        for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        double2 acc = make_double2(0.0, 0.0);
+        for (int t = 0; t < T; ++t) {
+          acc[t] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < M; ++j) acc = cfma(srow[j], U(p, j, t), acc);
-        dst[t] = acc;
+          for (int j = 0; j < M; ++j) acc[t] = cfma(srow[j], U(p, j, t), acc[t]);
+        }
+      }
+      gp.sync();
+      if (act) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) U(p, m, t) = acc[t];
       }
     }
-    fence_proxy_async_smem();   // this thread's generic accesses of the slot before the refill
+    fence_proxy_async_smem();   // the generic writes of the slot before the TMA store reads it
     gp.sync();
-    if (gp.tid == 0) issue(k + NS);
+    if (gp.tid == 0) {          // X[p][m][n0 .. n0 + T) <- the tile; refill once the store has read it
+      tma_store_3d(&tmx, 2 * n0, 0, 0, sm);
+      bulk_commit();
+      bulk_wait_read();
+      issue(k + NS);
+    }
   }
+  if (threadIdx.x % kFwdTmaGT == 0) bulk_wait_all();   // the last stores complete before exit
 }
 
 __device__ __forceinline__ unsigned long long dbl_bits(double v) { return (unsigned long long)__double_as_longlong(v); }
@@ -1560,7 +1576,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
   const int grid = (st.packed ? g.N / 2 : g.N) / T;
   cudaError_t e = cudaSuccess;
   if (g.dim == 1 && fwd1d_tma_ok(g, st, T)) {   // TMA-staged tile (the product 1-D path)
-    CUtensorMap tmu, tmh;
+    CUtensorMap tmu, tmh, tmx;
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
     const cuuint64_t dims[3] = {(cuuint64_t)2 * g.N, (cuuint64_t)g.M, (cuuint64_t)g.L};
     const cuuint64_t strides[2] = {(cuuint64_t)g.N * 16, (cuuint64_t)g.M * g.N * 16};
@@ -1571,7 +1587,9 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
         enc(&tmu, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.u, dims, strides, boxu, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
         enc(&tmh, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.u, dims, strides, boxh, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.X, dims, strides, boxu, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorNotSupported;
     const size_t slot = (size_t)g.L * g.M * (4 + 2) * sizeof(double2);
     const size_t head = 1024 + (((size_t)g.L * sizeof(double2) + 1023) & ~(size_t)1023);
@@ -1586,7 +1604,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
   case MM_:                                                                                                   \
     e = set_smem((const void *)fwd1d_tma_kernel<MM_>, sm1);                                                   \
     if (e == cudaSuccess)                                                                                     \
-      fwd1d_tma_kernel<MM_><<<grid, kFwdTmaGT * kFwdTmaG, sm1, s>>>(tmu, tmh, g, st, at, b.X, NS, ntiles);          \
+      fwd1d_tma_kernel<MM_><<<grid, kFwdTmaGT * kFwdTmaG, sm1, s>>>(tmu, tmh, tmx, g, st, at, NS, ntiles);          \
     break;
       PINT_FWDT(1) PINT_FWDT(2) PINT_FWDT(3) default: PINT_FWDT(4)
 #undef PINT_FWDT
