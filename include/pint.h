@@ -209,7 +209,9 @@ pint_status pint_set_forcing(pint_ctx *c, const void *v_dev);
  * u_{l-1,M-1} (u_{-1} = u0), solved per step through Q = V diag(lambda) V^{-1} and the FFT
  * diagonal spatial solves on the same kernels as the iteration (one spatial pipeline launch per
  * step).  The fixed point of the iteration; used as the honest single-GPU time-stepping baseline.
- * Synchronous.  Requirements: dim == 2 (grids of the spatial pipeline), nranks == 1.  Errors:
+ * 1-D: the M shifted tridiagonal solves of each step by the PCR kernels of the iteration (the
+ * direct-form solve path with the shifts dT lambda_m), then U_l = (V (x) I) z.  Synchronous.
+ * Requirements: power-of-two grids (2-D: grids of the spatial pipeline), nranks == 1.  Errors:
  * PINT_ERR_INVALID, PINT_ERR_NOT_DIAGONALIZABLE, PINT_ERR_CUDA. */
 pint_status pint_sequential(pint_ctx *c);
 

@@ -191,6 +191,11 @@ const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const Sta
 // stage planes of the step at `out`.
 cudaError_t launch_sequential_step(const Geometry &g, const StaticTables &st, const AlphaTables &at,
                                    const Buffers &b, double2 *r0, double2 *out, cudaStream_t s);
+// 1-D step of the sequential baseline: the M shifted PCR solves of sig_m r0 (launch_direct_solve
+// on one slot with the tables `at`), then U_m = sum_j V_mj y_j into `out` ([M][N])
+cudaError_t launch_sequential_step_1d(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                      const AlphaTables &at, const Buffers &b, double2 *r0, double2 *out,
+                                      cudaStream_t s);
 cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
                                  double *out2, cudaStream_t s);
 cudaError_t launch_init_iterate(const Geometry &g, const StaticTables &st, const Buffers &b,

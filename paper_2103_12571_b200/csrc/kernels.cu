@@ -1963,6 +1963,35 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
   return cudaGetLastError();
 }
 
+// U_m = sum_j V_mj y_j (the node basis back-transform of a sequential step)
+template <int M>
+__global__ void seq_node_mix_kernel(const double2 *__restrict__ V, const double2 *__restrict__ y,
+                                    double2 *__restrict__ out, int N) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    double2 v[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) v[j] = __ldg(y + (size_t)j * N + n);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = cfma(__ldg(V + m * M + j), v[j], acc);
+      out[(size_t)m * N + n] = acc;
+    }
+  }
+}
+
+cudaError_t launch_sequential_step_1d(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                      const AlphaTables &at, const Buffers &b, double2 *r0, double2 *out,
+                                      cudaStream_t s) {
+  double2 *y = nullptr;
+  cudaError_t e = launch_direct_solve(g, lc, st, at, b, r0, s, &y);
+  if (e != cudaSuccess) return e;
+  const int blocks = (g.N + 255) / 256 < num_sms() * 4 ? (g.N + 255) / 256 : num_sms() * 4;
+  PINT_DISPATCH_M(g.M, { seq_node_mix_kernel<MM><<<blocks, 256, 0, s>>>(at.SG, y, out, g.N); });
+  return cudaGetLastError();
+}
+
 cudaError_t launch_residual_norm(const Geometry &g, const StaticTables &st, const Buffers &b,
                                  double *out2, cudaStream_t s) {
   const long long total = (long long)g.L * g.N;

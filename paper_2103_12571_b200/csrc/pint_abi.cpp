@@ -186,8 +186,9 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
   off = align_up(off + 2 * (size_t)g.L * sizeof(int), 256);
   L.off_band = off;                                        // P > 1: slot lists of the bands (L ints)
   off = align_up(off + (size_t)g.L * sizeof(int), 256);
-  L.off_seq = off;
+  L.off_seq = off;   // 1-D: + the PCR level tables and 1/e of the M shifts
   off = align_up(off + (size_t)(2 * g.M + g.M * g.M) * sizeof(double2), 256);
+  if (g.dim == 1) off = align_up(off + ((size_t)g.M * g.logN * g.nfac * 2 + g.M) * sizeof(double2), 256);
   L.total = off;
   return L;
 }
@@ -469,6 +470,41 @@ pint_status pint_w_inf(pint_ctx *c, double *w_inf) {
   return PINT_OK;
 }
 
+// 1-D: I - s A = lead prod_f T_f (host_numerics: factor_shifted); row-sum-carrying PCR
+// coefficients per factor (reading R6), levels interleaved: lev[(j F + f) 2 + {0, 1}] =
+// (p_j, q_j) of factor f; *inv_e = 1 / (lead prod_f e_f,final)
+static bool pcr_tables(const pint_ctx *c, const AxisStencil &sx, cld s, double2 *lev, double2 *inv_e,
+                       std::string &err) {
+  const Geometry &g = c->g;
+  const int F = g.nfac;
+  std::vector<TriFactor> fac;
+  cld lead;
+  if (!factor_shifted(c->prob.op, sx, s, fac, lead, err) || (int)fac.size() != F) {
+    if (err.empty()) err = "unexpected factor count";
+    return false;
+  }
+  cld ie = 1.0L / lead;
+  for (int f = 0; f < F; ++f) {
+    cld ca = fac[f].a, cc = fac[f].c, e = fac[f].e;
+    cld cb = e - ca - cc;
+    for (int j = 0; j < g.logN - 1; ++j) {
+      cld pj = ca / cb, qj = cc / cb;
+      lev[(j * F + f) * 2] = make_double2((double)pj.real(), (double)pj.imag());
+      lev[(j * F + f) * 2 + 1] = make_double2((double)qj.real(), (double)qj.imag());
+      cld e2 = e * (e - 2.0L * (ca + cc)) / cb;
+      cld a2 = -ca * ca / cb, c2 = -cc * cc / cb;
+      ca = a2; cc = c2; e = e2; cb = e - ca - cc;
+    }
+    cld pl = (ca + cc) / cb;                        // pair level: i-h == i+h
+    lev[((g.logN - 1) * F + f) * 2] = make_double2((double)pl.real(), (double)pl.imag());
+    lev[((g.logN - 1) * F + f) * 2 + 1] = make_double2(0.0, 0.0);
+    e = e * (e - 2.0L * (ca + cc)) / cb;
+    ie /= e;
+  }
+  *inv_e = make_double2((double)ie.real(), (double)ie.imag());
+  return true;
+}
+
 pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
   BIND_DEVICE(c);
@@ -562,37 +598,13 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
         const cld s = lam[m] * dT;                          // (I - d_km dT A)
         shift[(size_t)p * M + m] = make_double2((double)s.real(), (double)s.imag());
         if (g.dim == 1 && g.pow2) {
-          // I - s A = lead prod_f T_f; row-sum-carrying PCR coefficients per factor (DESIGN.md
-          // reading R6), levels interleaved: lev[(j F + f) 2 + {0, 1}] = (p_j, q_j) of factor f
-          std::vector<TriFactor> fac;
-          cld lead;
           std::string ferr;
-          if (!factor_shifted(c->prob.op, sx, s, fac, lead, ferr) || (int)fac.size() != F) {
+          if (!pcr_tables(c, sx, s, pcr + ((size_t)p * M + m) * g.logN * F * 2, inv_e + (size_t)p * M + m, ferr)) {
             char buf[256];
             snprintf(buf, sizeof buf, "1-D spatial factorisation failed for alpha=%.6g, k=%d, m=%d: %s",
                      (double)al, k, m, ferr.c_str());
             return fail(PINT_ERR_NUMERIC, buf);
           }
-          double2 *lev = pcr + ((size_t)p * M + m) * g.logN * F * 2;
-          cld ie = 1.0L / lead;
-          for (int f = 0; f < F; ++f) {
-            cld ca = fac[f].a, cc = fac[f].c, e = fac[f].e;
-            cld cb = e - ca - cc;
-            for (int j = 0; j < g.logN - 1; ++j) {
-              cld pj = ca / cb, qj = cc / cb;
-              lev[(j * F + f) * 2] = make_double2((double)pj.real(), (double)pj.imag());
-              lev[(j * F + f) * 2 + 1] = make_double2((double)qj.real(), (double)qj.imag());
-              cld e2 = e * (e - 2.0L * (ca + cc)) / cb;
-              cld a2 = -ca * ca / cb, c2 = -cc * cc / cb;
-              ca = a2; cc = c2; e = e2; cb = e - ca - cc;
-            }
-            cld pl = (ca + cc) / cb;                        // pair level: i-h == i+h
-            lev[((g.logN - 1) * F + f) * 2] = make_double2((double)pl.real(), (double)pl.imag());
-            lev[((g.logN - 1) * F + f) * 2 + 1] = make_double2(0.0, 0.0);
-            e = e * (e - 2.0L * (ca + cc)) / cb;
-            ie /= e;
-          }
-          inv_e[(size_t)p * M + m] = make_double2((double)ie.real(), (double)ie.imag());
         }
       }
     }
@@ -1310,8 +1322,8 @@ pint_status pint_sequential(pint_ctx *c) {
   if (c->st.v) return fail(PINT_ERR_INVALID, "the sequential baseline assumes b == 0");
   if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
   const Geometry &g = c->g;
-  if (g.dim != 2 || !reg2d_path(g) || c->P != 1)
-    return fail(PINT_ERR_INVALID, "sequential baseline: 2-D grids of the spatial pipeline, one rank");
+  if (c->P != 1 || !g.pow2 || (g.dim == 2 && !reg2d_path(g)))
+    return fail(PINT_ERR_INVALID, "sequential baseline: power-of-two grids (2-D: of the spatial pipeline), one rank");
   if (c->hermitian) return fail(PINT_ERR_INVALID, "sequential baseline: complex storage only (pint_set_hermitian(0))");
   const int M = g.M;
   // Q = V diag(lambda) V^{-1} (Radau IIA): step l solves (I - dT Q (x) A) U_l = 1 (x) u_{l-1,M-1}
@@ -1321,7 +1333,10 @@ pint_status pint_sequential(pint_ctx *c) {
   ld cond, gap;
   if (!eig_diagonalize(M, B, lam, S, Si, cond, gap)) return fail(PINT_ERR_NOT_DIAGONALIZABLE, "Q not diagonalisable");
   const ld dT = (ld)c->prob.T / c->prob.L;
-  std::vector<double2> tab(2 * M + M * M);
+  const size_t npcr = g.dim == 1 ? (size_t)M * g.logN * g.nfac * 2 : 0;
+  std::vector<double2> tab(2 * M + M * M + npcr + (g.dim == 1 ? M : 0));
+  AxisStencil sx;
+  if (g.dim == 1) axis_stencil(c->prob.op, g.nx, op_is_heat(c->prob.op) ? c->prob.nu : c->prob.cx, sx);
   for (int m = 0; m < M; ++m) {
     cld rs = 0;
     for (int j = 0; j < M; ++j) rs += Si[(size_t)m * M + j];
@@ -1332,6 +1347,12 @@ pint_status pint_sequential(pint_ctx *c) {
       const cld v = S[(size_t)m * M + j];
       tab[2 * M + m * M + j] = make_double2((double)v.real(), (double)v.imag());       // V
     }
+    if (g.dim == 1) {   // PCR tables of the shifted system I - dT lambda_m A (line m)
+      std::string ferr;
+      if (!pcr_tables(c, sx, sh, tab.data() + 2 * M + M * M + (size_t)m * g.logN * g.nfac * 2,
+                      tab.data() + 2 * M + M * M + npcr + m, ferr))
+        return fail(PINT_ERR_NUMERIC, "sequential baseline: 1-D spatial factorisation failed: " + ferr);
+    }
   }
   double2 *dtab = (double2 *)(c->work + c->lay.off_seq);
   CUDA_TRY(c, cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
@@ -1339,6 +1360,10 @@ pint_status pint_sequential(pint_ctx *c) {
   at.sig = dtab;
   at.shift = dtab + M;
   at.SG = dtab + 2 * M;
+  if (g.dim == 1) {
+    at.pcr = dtab + 2 * M + M * M;
+    at.inv_e = dtab + 2 * M + M * M + npcr;
+  }
   StaticTables st = c->st;       // one "slot" (slot 0) per step, never packed
   st.nsolve = 1;
   st.packed = 0;
@@ -1347,7 +1372,10 @@ pint_status pint_sequential(pint_ctx *c) {
   for (int l = 0; l < g.L; ++l) {
     const double2 *prev = l == 0 ? c->st.u0 : c->u + ((size_t)(l - 1) * M + (M - 1)) * g.N;
     CUDA_TRY(c, cudaMemcpyAsync(r0, prev, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_TRY(c, launch_sequential_step(g, st, at, b, r0, c->u + (size_t)l * M * g.N, c->stream));
+    if (g.dim == 1)
+      CUDA_TRY(c, launch_sequential_step_1d(g, c->lc, st, at, b, r0, c->u + (size_t)l * M * g.N, c->stream));
+    else
+      CUDA_TRY(c, launch_sequential_step(g, st, at, b, r0, c->u + (size_t)l * M * g.N, c->stream));
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PINT_OK;

@@ -236,7 +236,7 @@ class Solver:
         _check(self.lib.pint_next_window(self.ctx))
 
     def sequential(self):
-        """Overwrite the iterate with the sequential Radau IIA solution (2-D baseline)."""
+        """Overwrite the iterate with the sequential Radau IIA solution (baseline)."""
         _check(self.lib.pint_sequential(self.ctx))
 
     def set_hermitian(self, on: bool = True):

@@ -12,6 +12,13 @@ pytestmark = pytest.mark.gpu
 
 CASES = [W.reduced(4), W.reduced(5), W.reduced(5).replace(name="red5_adv2d_32x64_M2_L8", nx=32, ny=64, M=2, L=8)] + [
     p for p in W.edge_cases() if p.dim == 2]
+# 1-D: the shifted tridiagonal solves by the PCR kernels (one-pass N <= 4096, two-pass beyond),
+# heat and centred advection, and a wider stencil (tridiagonal factors)
+CASES_1D = [W.CONFIGS[1], W.CONFIGS[2].replace(L=16), W.reduced(3),
+            W.CONFIGS[3].replace(name="seq_heat_N16384_L8", nx=16384, L=8),
+            W.CONFIGS[2].replace(name="seq_adv_N8192_M2_L8", nx=8192, M=2, L=8),
+            W.CONFIGS[1].replace(name="seq_heat4_N64", op="heat4")] + [
+    p for p in W.edge_cases() if p.dim == 1 and p.nx >= 8]
 
 
 @pytest.mark.parametrize("p", CASES, ids=lambda p: p.name)
@@ -23,6 +30,11 @@ def test_sequential_matches_oracle(p):
     ref = sequential_solution(p, Tableau(p.M), u0)
     assert relative_l2(s.get_iterate(), ref) <= 1e-11
     s.close()
+
+
+@pytest.mark.parametrize("p", CASES_1D, ids=lambda p: p.name)
+def test_sequential_1d_matches_oracle(p):
+    test_sequential_matches_oracle(p)
 
 
 def test_iteration_converges_to_sequential():
