@@ -161,7 +161,11 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
  * u <- u + C_a^{-1}(w - C u).  PINT_FORM_DIRECT (Alg. 1 as printed, eq. Riteration
  * P:159): u <- C_a^{-1}((C_a - C) u + w); (C_a - C) u + w = w - alpha e_1 (x) H u_L has a
  * single non-zero block r0 = u0 - alpha u_{L-1,M-1}, so the residual pass and the forward time
- * transform collapse to one N-vector.  Direct form: nranks == 1 only. */
+ * transform collapse to one N-vector.  nranks > 1: the rank holding global
+ * step L - 1 forms r0 and broadcasts it (N complex values); every rank synthesizes its local
+ * frequencies S^{-1} x_k = sig_k r0, solves, and the inverse cross-rank DFT + all-to-all return
+ * the result (no halo, no forward all-to-all).  Errors: PINT_ERR_INVALID (unknown form, a forcing
+ * attached, non-power-of-two grids). */
 #define PINT_FORM_CORRECTION 0
 #define PINT_FORM_DIRECT 1
 pint_status pint_set_form(pint_ctx *c, int32_t form);

@@ -181,6 +181,13 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
 // pass; then launch_backward(..., overwrite = 1).
 cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                                 const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s);
+// the two halves of launch_direct_front: r0 = u0 - alpha u_{L-1,M-1} (local last step), and (2-D)
+// its plane spectrum (+ the synthesized column pass on the legacy path); P ranks: rank P - 1
+// computes r0, every rank the spectrum of the broadcast r0
+cudaError_t launch_direct_r0(const Geometry &g, const StaticTables &st, const AlphaTables &at, const Buffers &b,
+                             double2 *r0, cudaStream_t s);
+cudaError_t launch_direct_spectrum(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                   const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s);
 cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                                 const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
                                 double2 **out);

@@ -1852,15 +1852,27 @@ const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const Sta
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
 }
 
-cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
-                                const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s) {
-  (void)lc;
+cudaError_t launch_direct_r0(const Geometry &g, const StaticTables &st, const AlphaTables &at, const Buffers &b,
+                             double2 *r0, cudaStream_t s) {
   int blocks = (g.N + 255) / 256;
   if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   direct_r0_kernel<<<blocks, 256, 0, s>>>(g, st, at, b.u, r0);
   rec(s);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || g.dim == 1) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct_front(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s) {
+  cudaError_t e = launch_direct_r0(g, st, at, b, r0, s);
+  if (e != cudaSuccess) return e;
+  return launch_direct_spectrum(g, lc, st, at, b, r0, s);
+}
+
+cudaError_t launch_direct_spectrum(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
+                                   const AlphaTables &at, const Buffers &b, double2 *r0, cudaStream_t s) {
+  (void)lc;
+  cudaError_t e = cudaSuccess;
+  if (g.dim == 1) return e;
   int YG = 4096 / g.nx;
   if (YG < 1) YG = 1;
   if (YG > g.ny) YG = g.ny;
@@ -1924,9 +1936,14 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
     while (g.ny % YG) YG >>= 1;
     const size_t smem = (size_t)YG * g.M * g.nx * sizeof(double2);
     const unsigned rgrid = (unsigned)(g.L * (g.ny / YG));
-    PINT_DISPATCH_M(g.M, {
-      e = set_smem((const void *)fft2d_rows_kernel<MM, true, true>, smem);
-      if (e == cudaSuccess) fft2d_rows_kernel<MM, true, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+    PINT_DISPATCH_M(g.M, {   // P > 1: G^{-1} S lives in the inverse cross-rank DFT
+      if (st.P == 1) {
+        e = set_smem((const void *)fft2d_rows_kernel<MM, true, true>, smem);
+        if (e == cudaSuccess) fft2d_rows_kernel<MM, true, true><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+      } else {
+        e = set_smem((const void *)fft2d_rows_kernel<MM, true, false>, smem);
+        if (e == cudaSuccess) fft2d_rows_kernel<MM, true, false><<<rgrid, kFftThreads, smem, s>>>(g, st, at, b.X, YG);
+      }
     });
     rec(s);
     *out = b.X;

@@ -750,10 +750,47 @@ static pint_status run_mid_band(pint_ctx *c, int a, int bb, IterState &is) {
   return PINT_OK;
 }
 
+// P > 1, direct form: the middle of every rank once r0 (broadcast from rank P - 1) is in place:
+// x1_sigma = sig_sigma r0 synthesized in the local slot order (the alpha-scaled time DFT of the
+// single non-zero block r0 is r0 at every frequency), the spatial solves, G^{-1} S + inverse
+// cross-rank DFT into the send chunks
+static pint_status run_direct_mid(pint_ctx *c, int a, IterState &is) {
+  Buffers b = buffers(c);
+  const AlphaTables &at = c->at[a];
+  double2 *r0 = (double2 *)(c->work + c->lay.off_r0);
+  CUDA_TRY(c, launch_direct_spectrum(c->g, c->lc, c->st, at, b, r0, c->stream));
+  double2 *x2 = nullptr;
+  CUDA_TRY(c, launch_direct_solve(c->g, c->lc, c->st, at, b, r0, c->stream, &x2));
+  double2 *other = (x2 == b.X) ? b.Y : b.X;
+  CUDA_TRY(c, launch_xdft(c->g, c->st, at, x2, other, true, c->stream));
+  is.send_back = other;
+  is.solved = x2;
+  return PINT_OK;
+}
+
 static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
   NvtxRange range("pint iteration");
   IterState is;
   pint_status st;
+  if (c->form == PINT_FORM_DIRECT && c->P > 1) {   // time-sharded direct form
+    if (!c->comm) return fail(PINT_ERR_STATE, "loopback (virtual-rank) context: use pint_group_iterate");
+    Buffers b = buffers(c);
+    const AlphaTables &at = c->at[a];
+    double2 *r0 = (double2 *)(c->work + c->lay.off_r0);
+    if (c->rank == c->P - 1) CUDA_TRY(c, launch_direct_r0(c->g, c->st, at, b, r0, c->stream));
+    ncclResult_t r = ncclBroadcast(r0, r0, (size_t)c->g.N * 2, ncclDouble, c->P - 1, c->comm, c->stream);
+    if (r != ncclSuccess) { c->poisoned = true; return fail(PINT_ERR_NCCL, std::string("broadcast: ") + ncclGetErrorString(r)); }
+    if ((st = run_direct_mid(c, a, is)) != PINT_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->commstream, c->ev[0], 0));
+    for (int bb = 0; bb < c->bands; ++bb)
+      if ((st = nccl_alltoall(c, is.send_back, is.solved, bb)) != PINT_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev[1], c->commstream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev[1], 0));
+    CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, is.solved, c->rank == c->P - 1 ? diff_slot : nullptr,
+                                c->stream, 1));
+    return PINT_OK;
+  }
   if (c->form == PINT_FORM_DIRECT) {  // Alg. 1 as printed: u = C_a^{-1}((C_a - C) u + w), 1 rank
     Buffers b = buffers(c);
     const AlphaTables &at = c->at[a];
@@ -868,8 +905,8 @@ pint_status pint_group_iterate(pint_ctx *const *ctxs, int32_t P, int32_t n_iter,
     if (c->poisoned) return fail(PINT_ERR_STATE, "context poisoned by an earlier CUDA error");
     if (c->stream != ctxs[0]->stream || c->dist.device != ctxs[0]->dist.device)
       return fail(PINT_ERR_INVALID, "virtual ranks must share one device and one stream");
-    if (c->k != ctxs[0]->k || c->alphas.size() != ctxs[0]->alphas.size())
-      return fail(PINT_ERR_STATE, "virtual ranks out of step");
+    if (c->k != ctxs[0]->k || c->alphas.size() != ctxs[0]->alphas.size() || c->form != ctxs[0]->form)
+      return fail(PINT_ERR_STATE, "virtual ranks out of step (schedule position or form)");
     if (c->k + n_iter > (int)c->alphas.size())
       return fail(PINT_ERR_SCHEDULE, "alpha schedule exhausted (call pint_set_alpha_schedule)");
   }
@@ -901,6 +938,24 @@ pint_status pint_group_iterate(pint_ctx *const *ctxs, int32_t P, int32_t n_iter,
     std::vector<IterState> is(P);
     const int a = ctxs[0]->k;
     pint_status st;
+    if (last->form == PINT_FORM_DIRECT) {   // the time-sharded direct form of run_iteration
+      double2 *r0l = (double2 *)(last->work + last->lay.off_r0);
+      CUDA_TRY(last, launch_direct_r0(last->g, last->st, last->at[a], buffers(last), r0l, s));
+      for (int r = 0; r < P - 1; ++r)   // "broadcast" from rank P - 1
+        CUDA_TRY(ctxs[r], cudaMemcpyAsync(ctxs[r]->work + ctxs[r]->lay.off_r0, r0l,
+                                          (size_t)last->g.N * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      for (int r = 0; r < P; ++r)
+        if ((st = run_direct_mid(ctxs[r], a, is[r])) != PINT_OK) return st;
+      for (int src = 0; src < P; ++src)
+        for (int dst = 0; dst < P; ++dst)
+          CUDA_TRY(ctxs[src], cudaMemcpyAsync((char *)is[dst].solved + src * ce, (const char *)is[src].send_back + dst * ce,
+                                              ce, cudaMemcpyDeviceToDevice, s));
+      for (int r = 0; r < P; ++r)
+        CUDA_TRY(ctxs[r], launch_backward(ctxs[r]->g, ctxs[r]->lc, ctxs[r]->st, ctxs[r]->at[a], buffers(ctxs[r]),
+                                          is[r].solved, (r == P - 1 && slots) ? slots + it : nullptr, s, 1));
+      for (int r = 0; r < P; ++r) ctxs[r]->k++;
+      continue;
+    }
     for (int r = 0; r < P; ++r)
       if ((st = run_phase(ctxs[r], PH_PRE, a, nullptr, is[r])) != PINT_OK) return st;
     for (int r = 0; r < P; ++r)  // ring: rank r -> rank r+1
@@ -1211,7 +1266,6 @@ int32_t pint_launches_per_iteration(pint_ctx *c) {
 pint_status pint_set_form(pint_ctx *c, int32_t form) {
   if (!c) return fail(PINT_ERR_INVALID, "ctx is NULL");
   if (form != PINT_FORM_CORRECTION && form != PINT_FORM_DIRECT) return fail(PINT_ERR_INVALID, "unknown form");
-  if (form == PINT_FORM_DIRECT && c->P > 1) return fail(PINT_ERR_INVALID, "the direct form is single-rank only");
   if (form == PINT_FORM_DIRECT && c->st.v) return fail(PINT_ERR_INVALID, "the direct form assumes b == 0");
   if (form == PINT_FORM_DIRECT && !c->g.pow2)
     return fail(PINT_ERR_INVALID, "non-power-of-two grids: correction form only (generic path)");

@@ -369,6 +369,10 @@ class Group:
         for s in self.ranks:
             s.set_alpha_schedule(alphas)
 
+    def set_form(self, form: str):
+        for s in self.ranks:
+            s.set_form(form)
+
     def iterate(self, n: int = 1, want_diff: bool = False):
         d = np.zeros(n) if want_diff else None
         _check(self.lib.pint_group_iterate(self._ctxs, self.P, n, _dp(d)))

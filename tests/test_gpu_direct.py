@@ -65,13 +65,17 @@ def test_direct_form_full_size_config5_sampled():
     s.close()
 
 
-def test_direct_form_refused_when_sharded():
+def test_direct_form_group_needs_one_form():
+    """The direct form runs on sharded ranks (tests/test_gpu_sharded.py::test_sharded_direct_form);
+    a group whose virtual ranks disagree on the form is refused, not run half-and-half."""
     import paper_2103_12571_b200 as PB
     p = W.CONFIGS[2].replace(L=16)
     grp = PB.Group(p, p.u0(), 2)
+    grp.set_alpha_schedule([1e-5])
+    grp.ranks[0].set_form("direct")
     with pytest.raises(PB.PintError) as e:
-        grp.ranks[0].set_form("direct")
-    assert e.value.status == 1
+        grp.iterate(1)
+    assert e.value.status == 7
     grp.close()
 
 
