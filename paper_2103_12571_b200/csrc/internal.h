@@ -158,9 +158,11 @@ cudaError_t launch_spatial_fused(const Geometry &g, const StaticTables &st, cons
                                  double2 *Yb, unsigned *sync, cudaStream_t s);
 bool spatial_pipe_geometry(const Geometry &g);                          // grid/M served (needs a 2nd vector)
 bool spatial_pipe_supported(const Geometry &g, const StaticTables &st);  // ... and the current mode
-// X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector
+// X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector.
+// spec != nullptr: direct form -- no R pass; spec (the plane spectrum of r0) is re-laid out blocked
+// into the first plane of X, the C pass loads it and synthesizes sig_q r0hat into Yb, then I -> X
 cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
-                                double2 *Yb, cudaStream_t s);
+                                double2 *Yb, cudaStream_t s, const double2 *spec = nullptr);
 bool reg2d_path(const Geometry &g);
 bool pipe2d_geometry(const Geometry &g);   // the 2-D path can run the pipelined passes (2 work vectors)   // the 2-D path runs spatial2d (else the generic row/column kernels)
 size_t fwd_smem_bytes(const Geometry &g, int T);
@@ -191,7 +193,7 @@ cudaError_t launch_direct_spectrum(const Geometry &g, const LaunchCfg &lc, const
 cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const StaticTables &st,
                                 const AlphaTables &at, const Buffers &b, const double2 *r0, cudaStream_t s,
                                 double2 **out);
-int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc);
+int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc, const StaticTables &st);
 const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const StaticTables &st, int i);
 // Sequential Radau IIA baseline (2-D, one step): the spectrum of r0 (in place), then the direct-form
 // synthesized spatial pipeline with the Q-eigen tables `at` (sig, shift, SG = V) writing the M

@@ -1831,8 +1831,9 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   return cudaGetLastError();
 }
 
-int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc) {
-  if (g.dim == 2) return reg2d(g) ? 5 : 6;  // r0, plane rows, plane cols, [spatial2d | synthesized cols, rows<inv>], bwd
+int launches_per_iteration_direct(const Geometry &g, const LaunchCfg &lc, const StaticTables &st) {
+  // r0, plane rows, plane cols, [spatial2d | synthesized cols, rows<inv>], bwd
+  if (g.dim == 2) return pipe2d(g, st) ? 7 : reg2d(g) ? 5 : 6;
   return lc.pcr_mode == 0 ? 3 : 4;            // r0, pcr (1 or 2), bwd
 }
 
@@ -1843,10 +1844,13 @@ const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const Sta
                              "cols_direct_kernel", "fft2d_rows_kernel<inv>", "tfft_bwd_kernel"};
   static const char *k2p[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel",
                               "spatial2d_kernel", "tfft_bwd_kernel"};
-  const int n = launches_per_iteration_direct(g, lc);
+  static const char *k2q[] = {"direct_r0_kernel", "plane_rows_dif_kernel", "plane_cols_dif_kernel", "spec_blocked_kernel",
+                              "cols_pipe_kernel<synth>", "rows_pipe_kernel<inv>", "tfft_bwd_kernel"};
+  const int n = launches_per_iteration_direct(g, lc, st);
   if (i < 0 || i >= n) return "";
   if (g.dim == 2) {
     if (i == n - 1 && tfft_pipe_supported(g, st) && !legacy_tfft()) return "tfft_pipe_kernel<inv>";
+    if (pipe2d(g, st)) return k2q[i];
     return reg2d(g) ? k2p[i] : k2[i];
   }
   return lc.pcr_mode == 0 ? k1a[i] : k1b[i];
@@ -1923,6 +1927,11 @@ cudaError_t launch_direct_solve(const Geometry &g, const LaunchCfg &lc, const St
                                 double2 **out) {
   cudaError_t e = cudaSuccess;
   const int lines = st.nsolve * g.M;   // solved units x nodes (Hermitian mode: k <= L/2)
+  if (pipe2d(g, st) && b.Y != b.X) {   // synthesized C pass + I pass (each launch recorded)
+    *out = b.X;
+    e = launch_spatial_pipe(g, st, at, b.X, b.Y, s, r0);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   if (reg2d(g)) {
     e = launch_spatial2d(g, st, at, b.X, r0, b.sync, st.nsolve * g.M, s);
     rec(s);

@@ -1259,7 +1259,7 @@ const char *pint_kernel_name(pint_ctx *c, int32_t i) {
 
 int32_t pint_launches_per_iteration(pint_ctx *c) {
   if (!c) return -1;
-  if (c->form == PINT_FORM_DIRECT) return launches_per_iteration_direct(c->g, c->lc);
+  if (c->form == PINT_FORM_DIRECT) return launches_per_iteration_direct(c->g, c->lc, c->st);
   return launches_per_iteration(c->g, c->lc, c->st);
 }
 

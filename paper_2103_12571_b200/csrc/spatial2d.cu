@@ -761,7 +761,12 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
 // lines of stride ls for the engine's exchanges: y-DIF, x2 = x1 / ((1 - s lambda) nx ny) with the
 // y-symbol table staged in shared memory, y-DIT; the transpose back to block rows goes through
 // the slot.  Named barriers: 1 + group, then 1 + GC + line (TPL > 32).
-template <class PX, class PY, int GC>
+//
+// SYN (direct form, Alg. 1 as printed): the x1 spectrum of every plane q is sig_q r0hat, so the
+// tile loaded is the item's block of r0hat itself (the same for every plane; `tmc` then maps the
+// blocked spectrum of r0, plane 0, L2-resident) read at the DIF output positions, times sig_q; no
+// y-DIF, the divide and the y-DIT follow.
+template <class PX, class PY, int GC, bool SYN = false>
 __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 : 1), 1)
     cols_pipe_kernel(const __grid_constant__ CUtensorMap tmc, const Geometry g, StaticTables st, AlphaTables at,
                      double2 *__restrict__ Yb, int lT, int NS, int ls, int BR, int nitems) {
@@ -809,7 +814,8 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
     uint64_t *bar = full + k % NS;
     double2 *dst = ring + (size_t)(k % NS) * slot_elems;
     mbar_arrive_expect_tx(bar, (unsigned)(NY * TC * sizeof(double2)));
-    for (int b = 0; b < NY; b += BR) tma_load_3d(dst + (size_t)b * TC, &tmc, 2 * TC * half, b, plane * NBLK + blk, bar);
+    for (int b = 0; b < NY; b += BR)
+      tma_load_3d(dst + (size_t)b * TC, &tmc, 2 * TC * half, b, (SYN ? 0 : plane) * NBLK + blk, bar);
     slot_item[k % NS] = k;   // after the barrier's arm (ring_wait)
   };
   if (threadIdx.x == 0)
@@ -829,15 +835,27 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
     const double2 lx = __ldg(st.lamx + brev(rfft::slot_to_pos<PX>(q0 + c), LX));
     ring_wait(full + s, slot_item, k, NS);
     double2 v[E];
-    // column c, row y of the swizzled TMA tile: 16-byte chunk c ^ ((y TC / 8) mod TC) of row y
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int y = rfft::natural_pos<PY>(tau, i);
-      v[i] = tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))];
-    }
-    named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
     double2 *line = tile + (size_t)c * ls;
-    rfft::forward_regs<PY>(v, line, lid, tau, twy);
+    // column c, row y of the swizzled TMA tile: 16-byte chunk c ^ ((y TC / 8) mod TC) of row y
+    if constexpr (SYN) {   // the x1 spectrum sig_q r0hat at the DIF output positions (rows = P)
+      const double2 sg = __ldg(at.sig + q);
+#pragma unroll
+      for (int u = 0; u < E / R; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int y = rfft::last_pos<PY>(tau, u, r);
+          v[u * R + r] = cmul(sg, tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))]);
+        }
+      named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int y = rfft::natural_pos<PY>(tau, i);
+        v[i] = tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))];
+      }
+      named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
+      rfft::forward_regs<PY>(v, line, lid, tau, twy);
+    }
 #pragma unroll
     for (int u = 0; u < E / R; ++u)
 #pragma unroll
@@ -1215,9 +1233,20 @@ bool blocked_map(const Geometry &g, double2 *Yb, unsigned box0, unsigned box1, u
              swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// direct form: r0hat (position order, [py][px]) -> the blocked S-slot layout of the C pass
+// (S-slot q of row py at blocked(q, py)) in `out` (one plane)
+template <class PX>
+__global__ void spec_blocked_kernel(const Geometry g, const double2 *__restrict__ spec, double2 *__restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.N; i += gridDim.x * blockDim.x) {
+    const int q = i & (g.nx - 1), py = i >> g.lognx;
+    out[blocked(q, py, g.logny)] = __ldg(spec + ((size_t)py << g.lognx) + rfft::slot_to_pos<PX>(q));
+  }
+}
+
 template <class PX, class PY, int MM, int GC>
 cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, const PipePlan &pp,
-                        double2 *X, double2 *Yb, int units, bool node, cudaStream_t s) {
+                        double2 *X, double2 *Yb, int units, bool node, cudaStream_t s,
+                        const double2 *spec = nullptr) {   // spec: direct form (no R pass, C synthesized)
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1226,9 +1255,17 @@ cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTa
   const int TC = 1 << pp.lT;
   const unsigned nblk = g.nx / kBW;
   CUtensorMap tmi, tmc;
+  // direct form: the blocked spectrum of r0 goes to the first plane of X (X is written only by the
+  // I pass, after the C pass has read it)
   if (!blocked_map(g, Yb, 2 * kBW, 1, nblk < 256 ? nblk : 256, CU_TENSOR_MAP_SWIZZLE_NONE, tmi) ||
-      !blocked_map(g, Yb, 2 * TC, pp.BR, 1, TC == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, tmc))
+      !blocked_map(g, spec ? X : Yb, 2 * TC, pp.BR, 1, TC == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   tmc))
     return cudaErrorNotSupported;
+  if (spec) {
+    spec_blocked_kernel<PX><<<sms * 4, 256, 0, s>>>(g, spec, X);
+    record_launch(s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   const int rthreads = pp.G * pp.YR * MM * PX::TPL;
   const int ritems = units * (g.ny / pp.YR);
   auto rows = [&](auto fn) -> cudaError_t {
@@ -1238,16 +1275,22 @@ cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTa
     record_launch(s);
     return cudaGetLastError();
   };
-  e = node ? rows(rows_pipe_kernel<PX, MM, false, true>) : rows(rows_pipe_kernel<PX, MM, false, false>);
-  if (e != cudaSuccess) return e;
+  if (!spec) {
+    e = node ? rows(rows_pipe_kernel<PX, MM, false, true>) : rows(rows_pipe_kernel<PX, MM, false, false>);
+    if (e != cudaSuccess) return e;
+  }
   {
-    const void *fn = (const void *)cols_pipe_kernel<PX, PY, GC>;
+    const void *fn = spec ? (const void *)cols_pipe_kernel<PX, PY, GC, true> : (const void *)cols_pipe_kernel<PX, PY, GC>;
     if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.csmem)) != cudaSuccess)
       return e;
     const int cthreads = GC * TC * PY::TPL;
     const int citems = units * g.M * (g.nx / TC);
-    cols_pipe_kernel<PX, PY, GC><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls, pp.BR,
-                                                                 citems);
+    if (spec)
+      cols_pipe_kernel<PX, PY, GC, true><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls,
+                                                                         pp.BR, citems);
+    else
+      cols_pipe_kernel<PX, PY, GC><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls, pp.BR,
+                                                                   citems);
     record_launch(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -1258,17 +1301,18 @@ cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTa
 // 1024-point axes when selected, radix-16 (Plan<L, 4>) otherwise
 template <int LX, int LY, int MM>
 cudaError_t launch_pipe_dispatch(const Geometry &g, const StaticTables &st, const AlphaTables &at, const PipePlan &pp,
-                                 double2 *X, double2 *Yb, int units, bool node, cudaStream_t s) {
+                                 double2 *X, double2 *Yb, int units, bool node, cudaStream_t s,
+                                 const double2 *spec = nullptr) {
   using PX4 = rfft::Plan<LX, 4>;
   using PY4 = rfft::Plan<LY, 4>;
   if constexpr (LX == 10 && LY == 10) {
     using P5 = rfft::Plan<10, 5>;
-    if (pp.rx32 && pp.ry32) return launch_pipe<P5, P5, MM, 2>(g, st, at, pp, X, Yb, units, node, s);
-    if (pp.ry32) return launch_pipe<PX4, P5, MM, 2>(g, st, at, pp, X, Yb, units, node, s);
-    if (pp.rx32) return launch_pipe<P5, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s);
+    if (pp.rx32 && pp.ry32) return launch_pipe<P5, P5, MM, 2>(g, st, at, pp, X, Yb, units, node, s, spec);
+    if (pp.ry32) return launch_pipe<PX4, P5, MM, 2>(g, st, at, pp, X, Yb, units, node, s, spec);
+    if (pp.rx32) return launch_pipe<P5, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s, spec);
   }
-  return pp.GC == 2 ? launch_pipe<PX4, PY4, MM, 2>(g, st, at, pp, X, Yb, units, node, s)
-                    : launch_pipe<PX4, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s);
+  return pp.GC == 2 ? launch_pipe<PX4, PY4, MM, 2>(g, st, at, pp, X, Yb, units, node, s, spec)
+                    : launch_pipe<PX4, PY4, MM, 1>(g, st, at, pp, X, Yb, units, node, s, spec);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1555,13 +1599,13 @@ bool spatial_pipe_geometry(const Geometry &g) {
 bool spatial_pipe_supported(const Geometry &g, const StaticTables &st) { return !st.packed && spatial_pipe_geometry(g); }
 
 cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
-                                double2 *Yb, cudaStream_t s) {
+                                double2 *Yb, cudaStream_t s, const double2 *spec) {
   PipePlan pp;
   if (st.packed || !pipe_plan(g, pp) || Yb == X) return cudaErrorInvalidValue;
   const bool node = st.P == 1;
   const int units = st.nsolve;
 #define PINT_PIPE(LXX, LYY, MMM) \
-  if (g.lognx == LXX && g.logny == LYY && g.M == MMM) return launch_pipe_dispatch<LXX, LYY, MMM>(g, st, at, pp, X, Yb, units, node, s);
+  if (g.lognx == LXX && g.logny == LYY && g.M == MMM) return launch_pipe_dispatch<LXX, LYY, MMM>(g, st, at, pp, X, Yb, units, node, s, spec);
 #define PINT_PIPE_M(LXX, LYY) PINT_PIPE(LXX, LYY, 1) PINT_PIPE(LXX, LYY, 2) PINT_PIPE(LXX, LYY, 3) PINT_PIPE(LXX, LYY, 4)
   PINT_PIPE_M(9, 9) PINT_PIPE_M(10, 10) PINT_PIPE_M(9, 10) PINT_PIPE_M(10, 9) PINT_PIPE_M(11, 11) PINT_PIPE_M(10, 11)
   PINT_PIPE_M(11, 10)

@@ -288,3 +288,43 @@ def test_cuda_graph_replay_matches_iterate(cfg):
         s1.set_phase_timing(True)       # one rank: no phases
     s1.close()
     s2.close()
+
+
+@pytest.mark.parametrize("p", PIPE_CASES, ids=lambda p: p.name)
+def test_parity_pipe_plans_direct_form(p):
+    """Direct form (Alg. 1 as printed) on the pipelined plans: the C pass synthesizes
+    sig_q r0hat (no R pass), then the I pass; against the oracle's direct-form iteration."""
+    import paper_2103_12571_b200 as PB
+    rng = np.random.default_rng(p.nx + 3 * p.ny + p.M)
+    u0 = rng.standard_normal(p.N) + 1j * rng.standard_normal(p.N)
+    s = PB.Solver(p, u0)
+    s.set_form("direct")
+    assert "cols_pipe_kernel<synth>" in s.kernel_names(), s.kernel_names()
+    a = [1e-3, 2e-2, 0.2][:p.iters]
+    s.set_alpha_schedule(a)
+    o = Oracle(p, u0, "fourier")
+    u = o.initial()
+    for k in range(p.iters):
+        u = o.iterate_direct(u, a[k])
+        s.iterate(1)
+        assert relative_l2(s.get_iterate(), u) <= TOL, k
+    s.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_parity_pipe_plans_sharded_direct_form(P):
+    import paper_2103_12571_b200 as PB
+    p = W.CONFIGS[5].replace(name=f"pipe_sharded_direct_P{P}", L=16, M=2, iters=2)
+    rng = np.random.default_rng(10 + P)
+    u0 = rng.standard_normal(p.N) + 1j * rng.standard_normal(p.N)
+    g = PB.Group(p, u0, P)
+    g.set_form("direct")
+    a = [1e-3, 5e-2]
+    g.set_alpha_schedule(a)
+    o = Oracle(p, u0, "fourier")
+    u = o.initial()
+    for k in range(2):
+        u = o.iterate_direct(u, a[k])
+        g.iterate(1)
+        assert relative_l2(g.get_iterate(), u) <= TOL, k
+    g.close()
