@@ -79,6 +79,10 @@ struct StaticTables {
   const int *slots, *unitof;
   int nsolve;
   int packed;
+  // packed mode on the pipelined plane passes: the complex series pairs the points (y, x) and
+  // (y, x + nx/2), packed column y nx/2 + x (x < nx/2), so the R pass unpacks X_k row by row;
+  // 0: the pairs (y, x), (y + ny/2, x) (packed column = point index of the first half)
+  int xpair;
   int sm_reserve;             // NCCL ranks: SMs the persistent kernels leave free (comm/compute overlap)
   const double2 *v;           // forcing part of w, [L][M][N] local steps (nullptr: b == 0)
 };
@@ -157,6 +161,7 @@ bool spatial_fused_supported(const Geometry &g, const StaticTables &st);
 cudaError_t launch_spatial_fused(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
                                  double2 *Yb, unsigned *sync, cudaStream_t s);
 bool spatial_pipe_geometry(const Geometry &g);                          // grid/M served (needs a 2nd vector)
+bool hermitian_pipe_path(const Geometry &g);                            // packed mode runs on the plane passes
 bool spatial_pipe_supported(const Geometry &g, const StaticTables &st);  // ... and the current mode
 // X natural -> R -> Yb blocked -> C (in place) -> I -> X natural; Yb must be a distinct vector.
 // spec != nullptr: direct form -- no R pass; spec (the plane spectrum of r0) is re-laid out blocked

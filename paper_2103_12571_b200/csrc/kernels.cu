@@ -477,7 +477,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   const int m = blockIdx.x / per;
   const int n0 = (blockIdx.x - m * per) * T;
   const size_t lstride = (size_t)g.M * g.N;
-  const double2 *xb = X2 + (size_t)m * g.N + n0;
+  // packed: the tile's first column as a point index and the partner offset of its pairs
+  const bool xp = PACK && st.xpair;
+  const int np0 = xp ? ((n0 >> (g.lognx - 1)) << g.lognx) + (n0 & (g.nx / 2 - 1)) : n0;
+  const int poff = xp ? g.nx / 2 : g.N / 2;
+  const double2 *xb = X2 + (size_t)m * g.N + (PACK ? np0 : n0);
   double2 *ub = u + (size_t)m * g.N + n0;
   const int all = g.L * T;
   if (PACK) {
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
           const int t = idx & (T - 1), q = idx >> lT;
           const double2 *yp = xb + (size_t)q * g.M * g.N + t;
           a[k] = __ldg(yp);
-          b[k] = __ldg(yp + g.N / 2);
+          b[k] = __ldg(yp + poff);
         }
       }
 #pragma unroll
@@ -536,9 +540,9 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
         const int t = idx & (T - 1), l = idx >> lT;
         const bool need_old = !overwrite || (diff_slot && l == g.L - 1);
         if (PACK) {   // real storage (u_dev holds doubles; same element offsets)
-          const double *ur = (const double *)u + (size_t)m * g.N + n0 + (size_t)l * lstride + t;
+          const double *ur = (const double *)u + (size_t)m * g.N + np0 + (size_t)l * lstride + t;
           uo[k] = make_double2(need_old ? ur[0] : 0.0, 0.0);
-          uo2[k] = make_double2(need_old ? ur[g.N / 2] : 0.0, 0.0);
+          uo2[k] = make_double2(need_old ? ur[poff] : 0.0, 0.0);
         } else {
           uo[k] = need_old ? ub[(size_t)l * lstride + t] : make_double2(0.0, 0.0);
         }
@@ -555,9 +559,9 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
           // real points n' (Re c) and n' + N/2 (Im c), stored real
           const double n1 = overwrite ? c.x : uo[k].x + c.x;
           const double n2 = overwrite ? c.y : uo2[k].x + c.y;
-          double *ur = (double *)u + (size_t)m * g.N + n0 + (size_t)l * lstride + t;
+          double *ur = (double *)u + (size_t)m * g.N + np0 + (size_t)l * lstride + t;
           ur[0] = n1;
-          ur[g.N / 2] = n2;
+          ur[poff] = n2;
           if (l == g.L - 1) dmax = nanmax(dmax, nanmax(fabs(n1 - uo[k].x), fabs(n2 - uo2[k].x)));
         } else {
           ub[(size_t)l * lstride + t] = overwrite ? c : cadd(uo[k], c);
@@ -595,7 +599,8 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
                                                          const double2 *__restrict__ u,
                                                          double2 *__restrict__ X, int BX, int BY, int LG) {
   extern __shared__ double2 sm[];  // [1 + PACK][M][BY+2HW][BX+2HW]
-  const int bxs = g.nx / BX, bys = (PACK ? g.ny / 2 : g.ny) / BY;
+  const bool xp = PACK && st.xpair;   // packed partner (y, x + nx/2) instead of (y + ny/2, x)
+  const int bxs = (xp ? g.nx / 2 : g.nx) / BX, bys = (PACK && !xp ? g.ny / 2 : g.ny) / BY;
   int b = blockIdx.x;
   // LG > 1: LG consecutive steps of one spatial block on consecutive CTAs, so the H-term plane
   // u_{l-1, M-1} of a block is read while the CTA of step l-1 streams the same lines (L2 hit)
@@ -617,10 +622,11 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
     for (int r = warp; r < 2 * M * H; r += blockDim.x >> 5) {
       const int hh = r / (M * H), rr = r - hh * M * H;
       const int j = rr / H, yy = rr - j * H;
-      const int y = (y0 + hh * (g.ny / 2) + yy - HW) & (g.ny - 1);
+      const int y = (y0 + (xp ? 0 : hh * (g.ny / 2)) + yy - HW) & (g.ny - 1);
+      const int xs = x0 + (xp ? hh * (g.nx / 2) : 0) - HW;
       const double *src = ur + (size_t)j * g.N + ((size_t)y << g.lognx);
       double *dst = smr + r * W;
-      for (int xx = lane; xx < W; xx += 32) cp_async8(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
+      for (int xx = lane; xx < W; xx += 32) cp_async8(dst + xx, src + ((xs + xx) & (g.nx - 1)));
     }
     cp_async_wait_all();
     __syncthreads();
@@ -630,7 +636,7 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
       double res[2][M];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        const int nn = n + hh * (g.N / 2);
+        const int nn = n + hh * (xp ? g.nx / 2 : g.N / 2);
         // one rank: w (l = 0) or the H-term u_{l-1, M-1}
         const double base = l == 0 ? __ldg(st.u0 + nn).x : __ldg(ur - g.N + nn);
         double uc[M], Au[M];
@@ -657,7 +663,9 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
         }
       }
 #pragma unroll
-      for (int m = 0; m < M; ++m) X[((size_t)l * M + m) * (g.N / 2) + n] = make_double2(res[0][m], res[1][m]);
+      const int col = xp ? ((y0 + ty) << (g.lognx - 1)) + x0 + tx : n;   // packed column
+#pragma unroll
+      for (int m = 0; m < M; ++m) X[((size_t)l * M + m) * (g.N / 2) + col] = make_double2(res[0][m], res[1][m]);
     }
     return;
   } else {
@@ -1467,6 +1475,8 @@ LaunchCfg choose_launch(const Geometry &g) {
   return lc;
 }
 
+bool hermitian_pipe_path(const Geometry &g) { return reg2d(g) && spatial_pipe_geometry(g) && !legacy_pipe(); }
+
 static bool pipe2d(const Geometry &g, const StaticTables &st) {
   return reg2d(g) && spatial_pipe_supported(g, st) && !legacy_pipe();
 }
@@ -1630,7 +1640,9 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     const bool pk = st.packed != 0;   // Hermitian mode: two real points per complex time series
     int BX, BY;
     residual_block(g, BX, BY);
-    if (pk && BY > g.ny / 2) BY = g.ny / 2;
+    const bool xp = pk && st.xpair;
+    if (pk && !xp && BY > g.ny / 2) BY = g.ny / 2;
+    if (xp && BX > g.nx / 2) BX = g.nx / 2;
     const int hw = g.hw < 1 ? 1 : g.hw;
     auto rbytes = [&](int bx, int by) {   // tile + (complex storage) the staged H-term block
       return (size_t)g.M * (bx + 2 * hw) * (by + 2 * hw) * (pk ? 2 * sizeof(double) : sizeof(double2)) +
@@ -1641,7 +1653,7 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
       else BX >>= 1;
     }
     const size_t rs = rbytes(BX, BY);
-    const int rgrid = g.L * (g.nx / BX) * ((pk ? g.ny / 2 : g.ny) / BY);
+    const int rgrid = g.L * ((xp ? g.nx / 2 : g.nx) / BX) * ((pk && !xp ? g.ny / 2 : g.ny) / BY);
     // step-grouped block order where a plane no longer fits L2 comfortably (config 5: 16 MB planes,
     // 14.3 -> 13.6 ms measured in round 1; config 4's 4 MB planes: slower, so not there)
     int lg = (size_t)g.N * sizeof(double2) >= ((size_t)8 << 20) ? 8 : 1;

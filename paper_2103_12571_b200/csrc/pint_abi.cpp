@@ -1310,6 +1310,7 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->st.nsolve = ns;
   c->st.packed = on ? 1 : 0;
+  c->st.xpair = on && hermitian_pipe_path(g) ? 1 : 0;
   if ((on != 0) != c->hermitian) {
     // iterate storage: real fp64 in the Hermitian mode (its imaginary parts are zero in exact
     // arithmetic; roundoff-level ones are dropped), complex128 otherwise

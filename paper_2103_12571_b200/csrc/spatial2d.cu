@@ -673,6 +673,12 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
         if constexpr (INV) {
           for (int b = 0; b < NBLK; b += IBOX)
             tma_load_3d(d + b * kBW, &tmi, 0, y0 + yy, (p * MM + m) * NBLK + b, bar);
+        } else if (st.packed) {
+          // packed spectra (pairs (y, x), (y, x + nx/2)): row y of Z_k and of Z_{L-k} side by side
+          const int kf = brev(p, g.logL), pc = brev((g.L - kf) & (g.L - 1), g.logL);
+          const size_t ro = (size_t)(y0 + yy) << (PX::LOGN - 1);
+          bulk_g2s(d, X + ((size_t)p * MM + m) * (g.N / 2) + ro, NX / 2 * sizeof(double2), bar);
+          bulk_g2s(d + NX / 2, X + ((size_t)pc * MM + m) * (g.N / 2) + ro, NX / 2 * sizeof(double2), bar);
         } else {
           bulk_g2s(d, X + ((size_t)p * MM + m) * g.N + ((size_t)(y0 + yy) << PX::LOGN), NX * sizeof(double2), bar);
         }
@@ -689,11 +695,22 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
     double2 *line = tile + (size_t)l * NX;
     const int un = it / ygroups, y0 = (it - un * ygroups) * YR;
     const int p = __ldg(st.slots + un);
-    double2 *xp = X + (size_t)p * MM * g.N;
+    // I output: the natural planes of slot p, or (packed mode) the unit planes behind Z
+    double2 *xp = st.packed ? unit_planes(g, X) + (size_t)un * MM * g.N : X + (size_t)p * MM * g.N;
     const int yy = l / MM, m = l - yy * MM;
     ring_wait(full + s, slot_item, k, NS);
     double2 v[E];
     if constexpr (!INV) {
+      if (st.packed) {   // X_k = (Z_k + conj Z_{L-k}) / 2 at x, (Z_k - conj Z_{L-k}) / 2i at x + nx/2
+        for (int i = t; i < LINES * (NX / 2); i += GT) {
+          const int li = i / (NX / 2), x = i - li * (NX / 2);
+          double2 *a_ = tile + (size_t)li * NX + x;
+          const double2 a = a_[0], b = a_[NX / 2];
+          a_[0] = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+          a_[NX / 2] = make_double2(0.5 * (a.y + b.y), 0.5 * (b.x - a.x));
+        }
+        named_sync(gbar, GT);
+      }
       if constexpr (NODE) {   // x1 = S_p^{-1} x on the natural rows, in place
         node_natural<MM>(tile, at.Sinv + (size_t)p * MM * MM, YR, NX, t, GT);
         named_sync(gbar, GT);
@@ -1596,12 +1613,14 @@ bool spatial_pipe_geometry(const Geometry &g) {
   return pipe_plan(g, pp);
 }
 
-bool spatial_pipe_supported(const Geometry &g, const StaticTables &st) { return !st.packed && spatial_pipe_geometry(g); }
+bool spatial_pipe_supported(const Geometry &g, const StaticTables &st) {
+  return (!st.packed || st.xpair) && spatial_pipe_geometry(g);
+}
 
 cudaError_t launch_spatial_pipe(const Geometry &g, const StaticTables &st, const AlphaTables &at, double2 *X,
                                 double2 *Yb, cudaStream_t s, const double2 *spec) {
   PipePlan pp;
-  if (st.packed || !pipe_plan(g, pp) || Yb == X) return cudaErrorInvalidValue;
+  if ((st.packed && !st.xpair) || !pipe_plan(g, pp) || Yb == X) return cudaErrorInvalidValue;
   const bool node = st.P == 1;
   const int units = st.nsolve;
 #define PINT_PIPE(LXX, LYY, MMM) \

@@ -110,3 +110,34 @@ def test_real_storage_roundtrip():
     assert relative_l2(s.get_iterate(), ref.get_iterate()) < 1e-12
     s.close()
     ref.close()
+
+
+# the real-data mode on the pipelined plane passes (grids 512^2 .. 2048^2): packed pairs (y, x),
+# (y, x + nx/2), the R pass unpacks X_k row by row, the I pass writes the unit planes
+HERM_PIPE = [W.CONFIGS[5].replace(name="hpipe_1024sq_M4_L4", L=4, iters=3),
+             W.CONFIGS[4].replace(name="hpipe_512sq_M3_L8", L=8, iters=3),
+             W.CONFIGS[5].replace(name="hpipe_1024x512_M2_L4", ny=512, M=2, L=4, iters=3),
+             W.CONFIGS[4].replace(name="hpipe_512x1024_M1_L8", ny=1024, M=1, L=8, iters=3),
+             W.CONFIGS[5].replace(name="hpipe_2048x1024_heat_M2_L4", nx=2048, op="heat", nu=1e-2, M=2, L=4,
+                                  iters=2)]
+
+
+@pytest.mark.parametrize("form", ["correction", "direct"])
+@pytest.mark.parametrize("p", HERM_PIPE, ids=lambda p: p.name)
+def test_hermitian_pipe_plans(p, form):
+    import paper_2103_12571_b200 as PB
+    rng = np.random.default_rng(p.nx + 7 * p.ny + p.M)
+    u0 = rng.standard_normal(p.N).astype(np.complex128)   # real data, every spatial mode excited
+    s = PB.Solver(p, u0)
+    s.set_form(form)
+    s.set_hermitian(True)
+    assert "cols_pipe_kernel" in " ".join(s.kernel_names()), s.kernel_names()
+    a = [1e-3, 2e-2, 0.2][:p.iters]
+    s.set_alpha_schedule(a)
+    o = Oracle(p, u0, "fourier")
+    u = o.initial()
+    for k in range(p.iters):
+        u = o.iterate(u, a[k]) if form == "correction" else o.iterate_direct(u, a[k])
+        s.iterate(1)
+        assert relative_l2(s.get_iterate(), u) <= TOL, k
+    s.close()
