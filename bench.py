@@ -278,6 +278,8 @@ def main():
     if args.form != "correction":
         s.set_form(args.form)
     if args.hermitian:
+        if world > 1:
+            sys.exit("bench.py: --hermitian is single-rank (the real-data mode is not built for time-sharded ranks)")
         s.set_hermitian(True)
     stream = s.stream
     w_inf = s.w_inf()

@@ -777,18 +777,25 @@ static pint_status run_iteration(pint_ctx *c, int a, double *diff_slot) {
     Buffers b = buffers(c);
     const AlphaTables &at = c->at[a];
     double2 *r0 = (double2 *)(c->work + c->lay.off_r0);
+    const bool pt = c->phase_timing;   // phases: halo = the broadcast, no forward, no all-to-all #1
+    if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[0], c->stream));
     if (c->rank == c->P - 1) CUDA_TRY(c, launch_direct_r0(c->g, c->st, at, b, r0, c->stream));
     ncclResult_t r = ncclBroadcast(r0, r0, (size_t)c->g.N * 2, ncclDouble, c->P - 1, c->comm, c->stream);
     if (r != ncclSuccess) { c->poisoned = true; return fail(PINT_ERR_NCCL, std::string("broadcast: ") + ncclGetErrorString(r)); }
+    if (pt)
+      for (int i : {1, 2, 3, 4}) CUDA_TRY(c, cudaEventRecord(c->tev[i], c->stream));
     if ((st = run_direct_mid(c, a, is)) != PINT_OK) return st;
     CUDA_TRY(c, cudaEventRecord(c->ev[0], c->stream));
     CUDA_TRY(c, cudaStreamWaitEvent(c->commstream, c->ev[0], 0));
     for (int bb = 0; bb < c->bands; ++bb)
       if ((st = nccl_alltoall(c, is.send_back, is.solved, bb)) != PINT_OK) return st;
     CUDA_TRY(c, cudaEventRecord(c->ev[1], c->commstream));
+    if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[6], c->commstream));
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev[1], 0));
+    if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[5], c->stream));
     CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, is.solved, c->rank == c->P - 1 ? diff_slot : nullptr,
                                 c->stream, 1));
+    if (pt) CUDA_TRY(c, cudaEventRecord(c->tev[7], c->stream));
     return PINT_OK;
   }
   if (c->form == PINT_FORM_DIRECT) {  // Alg. 1 as printed: u = C_a^{-1}((C_a - C) u + w), 1 rank
