@@ -262,33 +262,21 @@ __device__ __forceinline__ void chunk_blk_level(double2 (&y)[kE], const double2 
   for (int e = 0; e < kE; ++e) y[e] = nv[e];
 }
 
-// one comb level with shift S (stride 16 S): PUB publishes this thread's edge teeth (the values of
-// the previous level) at their natural positions first, between two group barriers
-template <int S, bool PUB, int CT, bool SYM>
-__device__ __forceinline__ void comb_step(double2 (&y)[kE], double2 *tile, int p0, const double2 *c, int gbar) {
-  constexpr int GT = CT / kE;
-  if (PUB) {
-    bar_sync(gbar, GT);   // everyone has read the previous level's teeth
+// Exchanges ping-pong between the slot and a second buffer of the group: a level reads its
+// neighbours' values from `src` and publishes the edge values the next level needs into `dst`
+// (comb: natural positions; block: swizzled), one group barrier, then the buffers swap roles.  A
+// write to a buffer always follows the barrier after which every read of it is complete.
+template <int S, int CT>
+__device__ __forceinline__ void comb_publish(const double2 (&y)[kE], double2 *dst, int p0) {
 #pragma unroll
-    for (int e = 0; e < kE; ++e)
-      if (e < S || e >= kE - S) tile[p0 + 16 * e] = y[e];
-    bar_sync(gbar, GT);
-  }
-  const double2 p = c[0], q = c[1];
-  comb_level<S, CT, SYM>(y, tile, p0, p, q, 1.0);
+  for (int e = 0; e < kE; ++e)
+    if (e < S || e >= kE - S) dst[p0 + 16 * e] = y[e];
 }
-template <int H, bool PUB, int CT, bool SYM>
-__device__ __forceinline__ void blk_step(double2 (&y)[kE], double2 *tile, int t, const double2 *c, int gbar) {
-  constexpr int GT = CT / kE;
-  if (PUB) {
-    bar_sync(gbar, GT);
+template <int H>
+__device__ __forceinline__ void blk_publish(const double2 (&y)[kE], double2 *dst, int t) {
 #pragma unroll
-    for (int e = 0; e < kE; ++e)
-      if (e < H || e >= kE - H) tile[chk_sw(16 * t + e)] = y[e];
-    bar_sync(gbar, GT);
-  }
-  const double2 p = c[0], q = c[1];
-  chunk_blk_level<H, CT, SYM>(y, tile, t, p, q, (H == 1 && (p.x != q.x || p.y != q.y)) ? -1.0 : 1.0);
+  for (int e = 0; e < kE; ++e)
+    if (e < H || e >= kE - H) dst[chk_sw(16 * t + e)] = y[e];
 }
 
 template <int CC, int G, bool SYM>
@@ -341,6 +329,7 @@ __global__ void __launch_bounds__(G * (CC + 2 * kCH) / kE, 1)
     for (int k = 0; k < NS; ++k) issue(k);
   const int gbar = 1 + gid;
   const int p0 = 256 * B + beta;
+  double2 *edge = ring + (size_t)NS * CT + (size_t)gid * CT;   // the group's second exchange buffer
   for (int k = gid;; k += G) {
     const int it = blockIdx.x + k * gridDim.x;
     if (it >= nitems) break;
@@ -351,30 +340,55 @@ __global__ void __launch_bounds__(G * (CC + 2 * kCH) / kE, 1)
     double2 y[kE];
 #pragma unroll
     for (int e = 0; e < kE; ++e) y[e] = tile[p0 + 16 * e];
+    const double2 *src = tile;
+    double2 *dst = edge;
+    auto flip = [&]() {
+      bar_sync(gbar, GT);
+      double2 *tmp = const_cast<double2 *>(src);
+      src = dst;
+      dst = tmp;
+    };
     // comb levels j = 4 .. jA - 1 (h = 16 .. 128); the first reads the loaded tile as is
-    if (jA > 4) comb_step<1, false, CT, SYM>(y, tile, p0, cf + 8, gbar);
-    if (jA > 5) comb_step<2, true, CT, SYM>(y, tile, p0, cf + 10, gbar);
-    if (jA > 6) comb_step<4, true, CT, SYM>(y, tile, p0, cf + 12, gbar);
-    if (jA > 7) comb_step<8, true, CT, SYM>(y, tile, p0, cf + 14, gbar);
-    // transposition comb -> block (swizzled positions)
-    bar_sync(gbar, GT);
+    if (jA > 4) {
+      comb_level<1, CT, SYM>(y, src, p0, cf[8], cf[9], 1.0);
+      if (jA > 5) { comb_publish<2, CT>(y, dst, p0); flip(); }
+    }
+    if (jA > 5) {
+      comb_level<2, CT, SYM>(y, src, p0, cf[10], cf[11], 1.0);
+      if (jA > 6) { comb_publish<4, CT>(y, dst, p0); flip(); }
+    }
+    if (jA > 6) {
+      comb_level<4, CT, SYM>(y, src, p0, cf[12], cf[13], 1.0);
+      if (jA > 7) { comb_publish<8, CT>(y, dst, p0); flip(); }
+    }
+    if (jA > 7) comb_level<8, CT, SYM>(y, src, p0, cf[14], cf[15], 1.0);
+    // transposition comb -> block (swizzled positions) into the buffer nobody reads now
 #pragma unroll
-    for (int e = 0; e < kE; ++e) tile[chk_sw(p0 + 16 * e)] = y[e];
-    bar_sync(gbar, GT);
+    for (int e = 0; e < kE; ++e) dst[chk_sw(p0 + 16 * e)] = y[e];
+    flip();
 #pragma unroll
-    for (int e = 0; e < kE; ++e) y[e] = tile[chk_sw(16 * t + e)];
-    // block levels j = 0 .. min(jA, 4) - 1 (h = 1 .. 8); the first reads the transposed tile
-    if (jA > 0) blk_step<1, false, CT, SYM>(y, tile, t, cf + 0, gbar);
-    if (jA > 1) blk_step<2, true, CT, SYM>(y, tile, t, cf + 2, gbar);
-    if (jA > 2) blk_step<4, true, CT, SYM>(y, tile, t, cf + 4, gbar);
-    if (jA > 3) blk_step<8, true, CT, SYM>(y, tile, t, cf + 6, gbar);
+    for (int e = 0; e < kE; ++e) y[e] = src[chk_sw(16 * t + e)];
+    // block levels j = 0 .. min(jA, 4) - 1 (h = 1 .. 8); the first reads the transposed values
+    if (jA > 0) {
+      const double2 p = cf[0], q = cf[1];
+      chunk_blk_level<1, CT, SYM>(y, src, t, p, q, (p.x != q.x || p.y != q.y) ? -1.0 : 1.0);
+      if (jA > 1) { blk_publish<2>(y, dst, t); flip(); }
+    }
+    if (jA > 1) {
+      chunk_blk_level<2, CT, SYM>(y, src, t, cf[2], cf[3], 1.0);
+      if (jA > 2) { blk_publish<4>(y, dst, t); flip(); }
+    }
+    if (jA > 2) {
+      chunk_blk_level<4, CT, SYM>(y, src, t, cf[4], cf[5], 1.0);
+      if (jA > 3) { blk_publish<8>(y, dst, t); flip(); }
+    }
+    if (jA > 3) chunk_blk_level<8, CT, SYM>(y, src, t, cf[6], cf[7], 1.0);
     // transposition block -> comb for coalesced stores of the core (blocks B = 1 .. CC/256)
-    bar_sync(gbar, GT);
 #pragma unroll
-    for (int e = 0; e < kE; ++e) tile[chk_sw(16 * t + e)] = y[e];
-    bar_sync(gbar, GT);
+    for (int e = 0; e < kE; ++e) dst[chk_sw(16 * t + e)] = y[e];
+    flip();
 #pragma unroll
-    for (int e = 0; e < kE; ++e) y[e] = tile[chk_sw(p0 + 16 * e)];
+    for (int e = 0; e < kE; ++e) y[e] = src[chk_sw(p0 + 16 * e)];
     fence_proxy_async_smem();
     bar_sync(gbar, GT);
     if (t == 0) issue(k + NS);
@@ -387,7 +401,8 @@ __global__ void __launch_bounds__(G * (CC + 2 * kCH) / kE, 1)
 }
 
 constexpr int kClsG = 2, kClsNS = 4;              // class pass: 2 groups of 128 threads, 4 x 32 KB slots
-constexpr int kChkCC = 2048, kChkG = 2, kChkNS = 4;  // chunk pass: 2 groups of 160 threads, 4 x 40 KB slots
+constexpr int kChkCC = 2048, kChkG = 2, kChkNS = 3;  // chunk pass: 2 groups of 160 threads, 3 x 40 KB slots
+                                                     // + a 40 KB exchange buffer per group
 
 }  // namespace
 
@@ -442,7 +457,7 @@ cudaError_t launch_pcr1d_pipe(const Geometry &g, const AlphaTables &at, double2 
   }
   {
     constexpr int CT = kChkCC + 2 * kCH;
-    const size_t smem = 1024 + kHdrBytes + (size_t)kChkNS * CT * sizeof(double2);
+    const size_t smem = 1024 + kHdrBytes + (size_t)(kChkNS + kChkG) * CT * sizeof(double2);
     const void *fn = sym ? (const void *)pcr_chunk_pipe_kernel<kChkCC, kChkG, true>
                          : (const void *)pcr_chunk_pipe_kernel<kChkCC, kChkG, false>;
     if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
