@@ -13,7 +13,12 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-9
 
 CASES = [W.CONFIGS[1], W.CONFIGS[2], W.reduced(3), W.reduced(4), W.reduced(5),
-         W.CONFIGS[3].replace(name="twopass_N16384_L8", nx=16384, L=8, iters=4)] + W.edge_cases()
+         W.CONFIGS[3].replace(name="twopass_N16384_L8", nx=16384, L=8, iters=4),
+         # the TMA-staged 1-D forward tile (L M in (512, 1024], L <= 256) and the pipelined PCR passes
+         W.CONFIGS[3].replace(name="fwd1d_N256_L256", nx=256, L=256, iters=3),
+         W.CONFIGS[3].replace(name="fwd1d_pcr1d_N8192_L256", nx=8192, L=256, iters=2),
+         # the 2-D plane passes
+         W.CONFIGS[4].replace(name="pipe_512sq_M2_L4", M=2, L=4, iters=3)] + W.edge_cases()
 
 
 def _alphas(p, u0):
