@@ -258,28 +258,32 @@ __global__ void __launch_bounds__(kFwdTmaGT * kFwdTmaG, 1)
     gp.sync();
     // (ii) L-point DIF FFT along l for the M*T columns, (iii) S_p^{-1} -> X
     fft_dif_g<3>(sm, M * T, 1, M * T, g.logL, tw, gp);
-    // (iii) S_p^{-1} in place, one (p, m) row per item: all reads, a group barrier, the writes
-    const int pstep = kFwdTmaGT / M;   // whole slots per pass: a slot's rows are read before any is written
-    const int mi = gp.tid % M, pi = gp.tid / M;
-    for (int p0 = 0; p0 < L; p0 += pstep) {
-      const int m = mi, p = p0 + pi;
-      const bool act = pi < pstep && p < L;
-      double2 acc[T];
-      if (act) {
-        double2 srow[M];
+    // (iii) S_p^{-1} in place, one (p, m) row per item; the M rows of a slot sit on adjacent lanes
+    // of one warp, so the reads of a slot precede its writes by a warp barrier (no group barrier)
+    {
+      constexpr int PPW = 32 / M;                 // slots per warp pass
+      const int lane = gp.tid & 31, wg = gp.tid >> 5, nwg = gp.nt >> 5;
+      const int pl = lane / M, m = lane - pl * M;
+      for (int p0 = wg * PPW; p0 < L; p0 += nwg * PPW) {
+        const int p = p0 + pl;
+        const bool act = pl < PPW && p < L;
+        double2 acc[T];
+        if (act) {
+          double2 srow[M];
 #pragma unroll
-        for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
+          for (int j = 0; j < M; ++j) srow[j] = __ldg(at.Sinv + ((size_t)p * M + m) * M + j);
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-          acc[t] = make_double2(0.0, 0.0);
+          for (int t = 0; t < T; ++t) {
+            acc[t] = make_double2(0.0, 0.0);
 #pragma unroll
-          for (int j = 0; j < M; ++j) acc[t] = cfma(srow[j], U(p, j, t), acc[t]);
+            for (int j = 0; j < M; ++j) acc[t] = cfma(srow[j], U(p, j, t), acc[t]);
+          }
         }
-      }
-      gp.sync();
-      if (act) {
+        __syncwarp();
+        if (act) {
 #pragma unroll
-        for (int t = 0; t < T; ++t) U(p, m, t) = acc[t];
+          for (int t = 0; t < T; ++t) U(p, m, t) = acc[t];
+        }
       }
     }
     fence_proxy_async_smem();   // the generic writes of the slot before the TMA store reads it
