@@ -119,7 +119,7 @@ bool fwd1d_tma_ok(const Geometry &g, const StaticTables &st, int T);
 bool pcr1d_pipe_supported(const Geometry &g, int R);
 bool pcr1d_path(const Geometry &g, const LaunchCfg &lc);
 cudaError_t launch_pcr1d_pipe(const Geometry &g, const AlphaTables &at, double2 *X, double2 *Y, const int *slots,
-                              int lines, int R, cudaStream_t s);
+                              int lines, int R, cudaStream_t s, int sm_reserve);
 
 // 2-D spatial solves as one persistent L2-resident pipeline (spatial2d.cu)
 struct SpatialPlan {

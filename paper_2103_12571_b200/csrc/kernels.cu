@@ -1714,7 +1714,7 @@ cudaError_t launch_solve(const Geometry &g, const LaunchCfg &lc, const StaticTab
       const int jOff = __builtin_ctz((unsigned)R);
       if (pcr1d_path(g, lc)) {   // pipelined class + chunk passes (pcr1d.cu), each launch recorded
         *out = b.Y;
-        return launch_pcr1d_pipe(g, at, b.X, b.Y, st.slots, lines, R, s);
+        return launch_pcr1d_pipe(g, at, b.X, b.Y, st.slots, lines, R, s, st.sm_reserve);
       }
       const int nq = g.N / R;
       size_t smem = (size_t)nq * T * sizeof(double2);

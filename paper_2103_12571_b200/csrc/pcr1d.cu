@@ -424,11 +424,12 @@ bool pcr1d_pipe_supported(const Geometry &g, int R) {
 }
 
 cudaError_t launch_pcr1d_pipe(const Geometry &g, const AlphaTables &at, double2 *X, double2 *Y, const int *slots,
-                              int lines, int R, cudaStream_t s) {
+                              int lines, int R, cudaStream_t s, int sm_reserve) {
   if (!pcr1d_pipe_supported(g, R)) return cudaErrorNotSupported;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sm_reserve > 0 && sms > 2 * sm_reserve) sms -= sm_reserve;   // NCCL ranks: leave SMs to the comm kernels
   const int jA = __builtin_ctz((unsigned)R);
   const bool sym = g.op == 0 || g.op == 1;   // centred 3-point heat / advection (see upd)
   auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
