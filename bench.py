@@ -39,12 +39,31 @@ ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32
               # pipelined time transforms (forward in place, inverse x2 + u -> u)
               "tfft_pipe_kernel<fwd>": 32, "tfft_pipe_kernel<inv>": 48,
               # fused R / C / I plane passes (one launch; compulsory 3 x 32 B, L2 reuse can only lower it)
-              "spatial_fused_kernel": 96}
+              "spatial_fused_kernel": 96,
+              # 1-D pipelined passes (TMA forward tile, two-pass PCR)
+              "fwd1d_tma_kernel": 32, "pcr_cls_pipe_kernel": 32, "pcr_chunk_pipe_kernel": 32,
+              # generic-grid path (paper's Table 1/2 sizes): one read + one write per pass
+              "resid_any_kernel": 32, "node_any_kernel<Sinv>": 32, "fft_any_kernel<fwd x>": 32,
+              "fft_any_kernel<fwd y>": 32, "divide_any_kernel": 32, "fft_any_kernel<inv y>": 32,
+              "fft_any_kernel<inv x>": 32, "node_any_kernel<SG>": 32}
 # direct form (u = C_a^{-1}((C_a - C)u + w)): no read of u, input synthesized from one N-vector
 ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
-                     "cols_direct_kernel": 16, "fft2d_rows_kernel<inv>": 32, "tfft_bwd_kernel": 32,
+                     "spec_blocked_kernel": 0, "cols_direct_kernel": 16, "cols_pipe_kernel<synth>": 16,
+                     "fft2d_rows_kernel<inv>": 32, "rows_pipe_kernel<inv>": 32, "tfft_bwd_kernel": 32,
                      "pcr_classes_kernel": 16, "pcr_chunk_kernel": 32, "bwd_kernel": 32,
                      "spatial2d_kernel": 48, "tfft_pipe_kernel<inv>": 32}
+# real-data (Hermitian) mode: u stored as real fp64 (8 B per unknown), time series packed two real
+# points per complex value (8 B per unknown), L/2 + 1 of the L frequencies solved (unit planes:
+# 8 B per unknown, up to a factor 1 + 2/L)
+ALGO_BYTES_HERM = {"residual2d_kernel": 16, "tfft_fwd_kernel": 16, "rows_pipe_kernel<fwd>": 16,
+                   "cols_pipe_kernel": 16, "rows_pipe_kernel<inv>": 16, "tfft_bwd_kernel": 24,
+                   "spatial2d_kernel": 48, "fwd_kernel": 16, "fwd1d_tma_kernel": 16, "pcr_classes_kernel": 16,
+                   "pcr_chunk_kernel": 16, "pcr_cls_pipe_kernel": 16, "pcr_chunk_pipe_kernel": 16,
+                   "bwd_kernel": 24}
+ALGO_BYTES_HERM_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_cols_dif_kernel": 0,
+                          "spec_blocked_kernel": 0, "cols_pipe_kernel<synth>": 8, "rows_pipe_kernel<inv>": 16,
+                          "tfft_bwd_kernel": 16, "spatial2d_kernel": 24, "pcr_classes_kernel": 8,
+                          "pcr_chunk_kernel": 16, "bwd_kernel": 16}
 
 
 def env_rank():
@@ -345,15 +364,11 @@ def main():
         phases = {k: max_over_ranks(v) for k, v in ph.items()}
     algo_tab = dict(ALGO_BYTES_DIRECT if args.form == "direct" else ALGO_BYTES)
     if args.hermitian:
-        # packed real data: time series of N/2 complex columns (8 B per unknown), L/2 + 1 of L
-        # frequencies solved (unit data ~8 B per unknown), u stays complex128 (16 B per unknown)
-        algo_tab.update({"residual2d_kernel": 24, "tfft_fwd_kernel": 16, "fwd_kernel": 24,
-                         "pcr_classes_kernel": 16, "pcr_chunk_kernel": 16, "spatial2d_kernel": 56,
-                         "tfft_bwd_kernel": 40, "bwd_kernel": 40})
-        if args.form == "direct":
-            algo_tab.update({"spatial2d_kernel": 24, "tfft_bwd_kernel": 24, "bwd_kernel": 24,
-                             "pcr_classes_kernel": 8, "pcr_chunk_kernel": 16})
-    model_bytes = sum(algo_tab.get(n_, 32) for n_ in names)
+        algo_tab.update(ALGO_BYTES_HERM_DIRECT if args.form == "direct" else ALGO_BYTES_HERM)
+    unknown = [n_ for n_ in names if n_ not in algo_tab]
+    if unknown:   # every launch of the iteration needs its byte model (no silent default)
+        sys.exit(f"bench.py: no algorithmic byte model for {unknown} (form {args.form}, hermitian {args.hermitian})")
+    model_bytes = sum(algo_tab[n_] for n_ in names)
     iteration_roof = {"model_bytes_per_unknown": model_bytes,
                       "achieved_gbs": model_bytes * p.U / world / (ms * 1e-3) / 1e9,
                       "frac": model_bytes * p.U / world / (ms * 1e-3) / 1e9 / peak,
@@ -365,7 +380,7 @@ def main():
                     "iteration": iteration_roof, "note": "multi-rank: per-launch profiling is single-rank only"}
     top = int(np.argmax(kms)) if kms is not None else 0
     top_name = names[top]
-    algo = algo_tab.get(top_name, 32) * p.U
+    algo = algo_tab[top_name] * p.U
     achieved = algo / (kms[top] * 1e-3) / 1e9 if kms is not None else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
