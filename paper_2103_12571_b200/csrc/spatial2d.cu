@@ -42,6 +42,7 @@ namespace pint {
 namespace {
 
 constexpr int kSpThreads = 256;
+constexpr int kColScal = 16;   // per-group scalar slot of cols_pipe_kernel: shift, sig, <= 8 x-symbols (+ pad)
 enum { kStR = 0, kStC = 1, kStI = 2 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
@@ -72,6 +73,7 @@ __device__ __forceinline__ void publish(unsigned *ctr) {
 __device__ __forceinline__ void copy_table(double2 *dst, const double2 *src, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
 }
+
 
 // 1 / ((1 - s lambda) nx ny) for natural frequencies (kx, ky)
 __device__ __forceinline__ double2 inv_symbol(const StaticTables &st, double2 s, double inv_n, int kx, int ky) {
@@ -783,23 +785,34 @@ __global__ void __launch_bounds__(PX::E == 32 ? 256 : 512, 1)
 // tile loaded is the item's block of r0hat itself (the same for every plane; `tmc` then maps the
 // blocked spectrum of r0, plane 0, L2-resident) read at the DIF output positions, times sig_q; no
 // y-DIF, the divide and the y-DIT follow.
+// the C item geometry is fixed by the column plan (pipe_plan makes the same choice at run time and
+// launch_pipe checks it): 8 columns per item if 8 lines of ny/16 threads fit 256 threads and the
+// tile 64 KB, else 4; line stride ny + 8/TC (+1 for TC = 8); TMA boxes of min(ny, 256) rows
+template <class PY>
+__host__ __device__ constexpr int cols_lt() { return (8 * (PY::N / 16) <= 256 && 8 * PY::N * 16 <= 64 * 1024) ? 3 : 2; }
+template <class PY>
+__host__ __device__ constexpr int cols_ls() { return PY::N + ((1 << cols_lt<PY>()) >= 8 ? 1 : 8 / (1 << cols_lt<PY>())); }
+
 template <class PX, class PY, int GC, bool SYN = false>
 __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 : 1), 1)
     cols_pipe_kernel(const __grid_constant__ CUtensorMap tmc, const Geometry g, StaticTables st, AlphaTables at,
-                     double2 *__restrict__ Yb, int lT, int NS, int ls, int BR, int nitems) {
+                     double2 *__restrict__ Yb, int NS, int nitems) {
   constexpr int NY = PY::N, TPL = PY::TPL, E = PY::E, R = 1 << PY::BL, TW = PY::twsize();
   constexpr int LX = PX::LOGN, LY = PY::LOGN, NX = PX::N, NBLK = NX / kBW;
+  static_assert(GC <= 2, "the scalar area holds two groups");
   extern __shared__ __align__(1024) unsigned char smraw_[];
   unsigned char *smraw = align_smem_1024(smraw_);   // swizzled TMA tiles need 1 KB-aligned slots
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
   volatile int *slot_item = reinterpret_cast<volatile int *>(smraw + 64);   // item held by slot s (ring_wait)
   double2 *twy = reinterpret_cast<double2 *>(smraw + 128);
   double2 *lamy = twy + TW;
+  double2 *scal = lamy + NY;   // per group: the current item's shift, sig and TC x-symbols (kColScal)
   double2 *ring = reinterpret_cast<double2 *>(
-      smraw + 1024 + (((size_t)(TW + NY) * sizeof(double2) + 1023) & ~(size_t)1023));
-  const int TC = 1 << lT, NH = kBW >> lT;   // columns per item, items per block
-  const int slot_elems = ((TC * ls * (int)sizeof(double2) + 1023) & ~1023) / (int)sizeof(double2);
-  const int GT = TC * TPL;
+      smraw + 1024 + (((size_t)(TW + NY + 2 * kColScal) * sizeof(double2) + 1023) & ~(size_t)1023));
+  constexpr int lT = cols_lt<PY>(), ls = cols_ls<PY>(), BR = NY < 256 ? NY : 256;
+  constexpr int TC = 1 << lT, NH = kBW >> lT;   // columns per item, items per block
+  constexpr int slot_elems = ((TC * ls * (int)sizeof(double2) + 1023) & ~1023) / (int)sizeof(double2);
+  constexpr int GT = TC * TPL;
   const int gid = threadIdx.x / GT, t = threadIdx.x - gid * GT, c = t / TPL, tau = t - c * TPL;
   const int gbar = 1 + gid, lid = GC + gid * TC + c;   // line_sync uses barrier 1 + lid
   const int M = g.M;
@@ -818,9 +831,36 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
   // eight 16-byte bank slots (a plain bit-reversed table read was 8-way conflicted)
   constexpr int SH = PY::BL > 3 ? PY::BL : 3;
   for (int P = threadIdx.x; P < NY; P += blockDim.x) lamy[P ^ ((P >> SH) & 7)] = __ldg(st.lamy + brev(P, LY));
-  __syncthreads();
   // CTA-local item k: block pair b = blockIdx + (k / NH) grid, half k mod NH
   auto item_of = [&](int k) { return (blockIdx.x + (k / NH) * gridDim.x) * NH + (k % NH); };
+  // the per-item scalars (plane shift s_q, sig_q, the x-symbol of each column) of the group's item
+  // kk, loaded by the column leaders one item ahead into the group's scal slot: the divide reads
+  // them from shared memory instead of waiting on dependent global loads in the middle of the item
+  double2 *my_scal = scal + gid * kColScal;
+  auto scal_load = [&](int kk, double2 &a, double2 &b, double2 &x) {
+    const int it2 = item_of(kk);
+    if (it2 >= nitems) return false;
+    const int bi2 = it2 / NH, half2 = it2 - bi2 * NH;
+    const int li2 = bi2 / NBLK, blk2 = bi2 - li2 * NBLK;
+    const int un2 = li2 / M, mm2 = li2 - un2 * M;
+    const int q2 = __ldg(st.slots + un2) * M + mm2;
+    a = __ldg(at.shift + q2);
+    b = SYN ? __ldg(at.sig + q2) : make_double2(0.0, 0.0);
+    x = __ldg(st.lamx + brev(rfft::slot_to_pos<PX>(blk2 * kBW + half2 * TC + c), LX));
+    return true;
+  };
+  auto scal_store = [&](const double2 &a, const double2 &b, const double2 &x) {
+    if (c == 0) {
+      my_scal[0] = a;
+      my_scal[1] = b;
+    }
+    my_scal[2 + c] = x;
+  };
+  if (tau == 0) {
+    double2 a, b, x;
+    if (scal_load(gid, a, b, x)) scal_store(a, b, x);
+  }
+  __syncthreads();
   auto issue = [&](int k) {
     const int it = item_of(k);
     if (it >= nitems) return;
@@ -848,14 +888,13 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
     const int q = __ldg(st.slots + un) * M + mm;   // table line (slot, node) == plane index
     const int q0 = blk * kBW + half * TC;          // first S-slot column of the item
     double2 *xb = Yb + (size_t)q * g.N + ((size_t)blk << (LY + 3)) + half * TC;
-    const double2 sh = __ldg(at.shift + q);
-    const double2 lx = __ldg(st.lamx + brev(rfft::slot_to_pos<PX>(q0 + c), LX));
+    (void)q0;
     ring_wait(full + s, slot_item, k, NS);
     double2 v[E];
     double2 *line = tile + (size_t)c * ls;
     // column c, row y of the swizzled TMA tile: 16-byte chunk c ^ ((y TC / 8) mod TC) of row y
     if constexpr (SYN) {   // the x1 spectrum sig_q r0hat at the DIF output positions (rows = P)
-      const double2 sg = __ldg(at.sig + q);
+      const double2 sg = my_scal[1];
 #pragma unroll
       for (int u = 0; u < E / R; ++u)
 #pragma unroll
@@ -873,6 +912,7 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
       named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
       rfft::forward_regs<PY>(v, line, lid, tau, twy);
     }
+    const double2 sh = my_scal[0], lx = my_scal[2 + c];
 #pragma unroll
     for (int u = 0; u < E / R; ++u)
 #pragma unroll
@@ -883,16 +923,22 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
         const double2 sl = cmul(sh, lam);
         const double dr = 1.0 - sl.x, di = -sl.y;
         const double qq = dr * dr + di * di;
-        const double den = inv_n * __drcp_rn(qq);   // correctly rounded reciprocal
+        const double den = inv_n * rcp_pos(qq);
         v[u * R + r] = cmul(v[u * R + r], make_double2(dr * den, -di * den));
       }
     rfft::inverse_in_regs<PY>(v, line, lid, tau, twy);
     rfft::to_smem<PY, 0>(v, line, tau);
-    named_sync(gbar, GT);
-    for (int i = t; i < (NY << lT); i += GT) {
-      const int cc = i & (TC - 1), y = i >> lT;
-      xb[((size_t)y << 3) + cc] = tile[(size_t)cc * ls + rfft::F<PY>(y)];
+    named_sync(gbar, GT);   // also: every divide of this item has read my_scal
+    double2 na, nb, nx;
+    const bool more = tau == 0 && scal_load(k + GC, na, nb, nx);   // in flight during the copy-out
+    {   // element (column cc, row y) of the item -> blocked row y; thread t: cc = t mod TC, rows t/TC + j TPL
+      const int cc = t & (TC - 1), y0 = t >> lT;
+      double2 *xo = xb + cc + ((size_t)y0 << 3);
+      const double2 *ti = tile + (size_t)cc * ls;
+#pragma unroll 8
+      for (int j = 0; j < NY / TPL; ++j) xo[(size_t)j * TPL * 8] = ti[rfft::F<PY>(y0 + j * TPL)];
     }
+    if (more) scal_store(na, nb, nx);
     fence_proxy_async_smem();
     named_sync(gbar, GT);
     if (t == 0) issue(k + NS);
@@ -1216,7 +1262,8 @@ bool pipe_plan(const Geometry &g, PipePlan &pp) {
   pp.NSC = pp.GC + 1 > 3 ? pp.GC + 1 : 3;
   pp.ls = g.ny + (TC >= 8 ? 1 : 8 / TC);
   pp.BR = g.ny < 256 ? g.ny : 256;
-  const size_t tw_c = ((size_t)(pass_twiddle_count(g.logny, pp.ry32 ? 5 : 4) + g.ny) * 16 + 1023) & ~(size_t)1023;
+  const size_t tw_c =
+      ((size_t)(pass_twiddle_count(g.logny, pp.ry32 ? 5 : 4) + g.ny + 2 * kColScal) * 16 + 1023) & ~(size_t)1023;
   const size_t cslot = ((size_t)TC * pp.ls * 16 + 1023) & ~(size_t)1023;
   pp.csmem = 1024 + 1024 + tw_c + (size_t)pp.NSC * cslot;
   const int lbr = tplx > 32 && !pp.rx32 ? pp.G * YR * g.M : 0, lbc = tply > 32 && !pp.ry32 ? pp.GC * TC : 0;   // named barrier ids
@@ -1300,14 +1347,14 @@ cudaError_t launch_pipe(const Geometry &g, const StaticTables &st, const AlphaTa
     const void *fn = spec ? (const void *)cols_pipe_kernel<PX, PY, GC, true> : (const void *)cols_pipe_kernel<PX, PY, GC>;
     if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.csmem)) != cudaSuccess)
       return e;
+    if (pp.lT != cols_lt<PY>() || pp.ls != cols_ls<PY>() || pp.BR != (PY::N < 256 ? PY::N : 256))
+      return cudaErrorInvalidValue;   // the kernel's compile-time item geometry must match the plan
     const int cthreads = GC * TC * PY::TPL;
     const int citems = units * g.M * (g.nx / TC);
     if (spec)
-      cols_pipe_kernel<PX, PY, GC, true><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls,
-                                                                         pp.BR, citems);
+      cols_pipe_kernel<PX, PY, GC, true><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.NSC, citems);
     else
-      cols_pipe_kernel<PX, PY, GC><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.lT, pp.NSC, pp.ls, pp.BR,
-                                                                   citems);
+      cols_pipe_kernel<PX, PY, GC><<<sms, cthreads, pp.csmem, s>>>(tmc, g, st, at, Yb, pp.NSC, citems);
     record_launch(s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
