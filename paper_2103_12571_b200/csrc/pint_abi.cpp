@@ -3,6 +3,7 @@
 // kernels of kernels.cu; this file only builds tables and enqueues launches.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <thread>
 
 #include <cmath>
 #include <cstdio>
@@ -200,6 +201,40 @@ static Layout make_layout(const Geometry &g, const LaunchCfg &lc, int P) {
       if (c) (c)->poisoned = true;                                                        \
       return fail(PINT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
     }                                                                                     \
+  } while (0)
+
+// Host wait on the context stream.  On an NCCL rank the wait polls the communicator's asynchronous
+// error state (ncclCommGetAsyncError): a failed peer or link surfaces as PINT_ERR_NCCL — the
+// communicator is aborted and the context poisoned — instead of leaving the host hanging in
+// cudaStreamSynchronize.
+static pint_status sync_stream(pint_ctx *c) {
+  if (!c->comm) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return PINT_OK;
+  }
+  for (;;) {
+    cudaError_t e = cudaStreamQuery(c->stream);
+    if (e == cudaSuccess) return PINT_OK;
+    if (e != cudaErrorNotReady) {
+      c->poisoned = true;
+      return fail(PINT_ERR_CUDA, std::string("cudaStreamQuery: ") + cudaGetErrorString(e));
+    }
+    ncclResult_t async = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(c->comm, &async);
+    if (r != ncclSuccess || (async != ncclSuccess && async != ncclInProgress)) {
+      c->poisoned = true;
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(PINT_ERR_NCCL, std::string("asynchronous communicator error: ") +
+                                     ncclGetErrorString(r != ncclSuccess ? r : async));
+    }
+    std::this_thread::yield();
+  }
+}
+#define PINT_SYNC(c)                       \
+  do {                                     \
+    pint_status _s = sync_stream(c);       \
+    if (_s != PINT_OK) return _s;          \
   } while (0)
 
 // pint_create error paths: free the half-built context and its communicator (nothing leaks)
@@ -464,7 +499,7 @@ pint_status pint_w_inf(pint_ctx *c, double *w_inf) {
   }
   double h = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&h, slot, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   if (!std::isfinite(h)) return fail(PINT_ERR_NUMERIC, "non-finite ||w||_inf");
   *w_inf = h;
   return PINT_OK;
@@ -631,7 +666,7 @@ pint_status pint_set_alpha_schedule(pint_ctx *c, const double *alpha, int32_t K)
     t.pcr = g.dim == 1 ? (const double2 *)(dst + off_pcr) : nullptr;
     t.inv_e = g.dim == 1 ? (const double2 *)(dst + off_inv) : nullptr;
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // host blobs go out of scope
+  PINT_SYNC(c);   // host blobs go out of scope
   c->at = tabs;
   c->alphas.assign(alpha, alpha + K);
   c->h_S = hS;
@@ -878,7 +913,7 @@ pint_status pint_iterate(pint_ctx *c, int32_t n_iter, double *last_step_diff_inf
       if (r != ncclSuccess) { c->poisoned = true; return fail(PINT_ERR_NCCL, ncclGetErrorString(r)); }
     }
     CUDA_TRY(c, cudaMemcpyAsync(last_step_diff_inf, slots, n_iter * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    PINT_SYNC(c);
     for (int i = 0; i < n_iter; ++i)   // the device max propagates NaN (nanmax): a diverged iterate
       if (!std::isfinite(last_step_diff_inf[i])) return fail(PINT_ERR_NUMERIC, "non-finite last-step difference");
   }
@@ -1061,7 +1096,7 @@ pint_status pint_residual_norm(pint_ctx *c, double *l2, double *linf) {
   }
   double h[2];
   CUDA_TRY(c, cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   if (l2) *l2 = h[0];
   if (linf) *linf = h[1];
   if (!std::isfinite(h[0]) || !std::isfinite(h[1])) return fail(PINT_ERR_NUMERIC, "non-finite residual");
@@ -1075,7 +1110,7 @@ pint_status pint_get_iterate(pint_ctx *c, double *u_host) {
   if (c->hermitian) {   // real storage: the first L M N doubles, expanded to (re, 0)
     const size_t n = (size_t)c->g.L * c->g.M * c->g.N;
     CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    PINT_SYNC(c);
     for (size_t i = n; i-- > 0;) {   // back to front: u_host[2i] never overwrites an unread u_host[j > i]
       u_host[2 * i] = u_host[i];
       u_host[2 * i + 1] = 0.0;
@@ -1083,7 +1118,7 @@ pint_status pint_get_iterate(pint_ctx *c, double *u_host) {
     return PINT_OK;
   }
   CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u, c->lay.vec_bytes, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   return PINT_OK;
 }
 
@@ -1096,7 +1131,7 @@ pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
     const size_t n = (size_t)c->g.N;
     CUDA_TRY(c, cudaMemcpyAsync(u_host, (const double *)c->u + off, n * sizeof(double), cudaMemcpyDeviceToHost,
                                 c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    PINT_SYNC(c);
     for (size_t i = n; i-- > 0;) {
       u_host[2 * i] = u_host[i];
       u_host[2 * i + 1] = 0.0;
@@ -1104,7 +1139,7 @@ pint_status pint_get_final_value(pint_ctx *c, double *u_host) {
     return PINT_OK;
   }
   CUDA_TRY(c, cudaMemcpyAsync(u_host, c->u + off, (size_t)c->g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   return PINT_OK;
 }
 
@@ -1144,7 +1179,7 @@ pint_status pint_next_window(pint_ctx *c) {
     CUDA_TRY(c, cudaMemcpyAsync(c->u0.data(), last, (size_t)g.N * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
   }
   CUDA_TRY(c, launch_init_iterate(c->g, c->st, buffers(c), c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   c->k = 0;
   return PINT_OK;
 }
@@ -1314,7 +1349,7 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
   }
   int *dsym = (int *)(c->work + c->lay.off_sym);
   CUDA_TRY(c, cudaMemcpyAsync(dsym, sym.data(), sym.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   c->st.nsolve = ns;
   c->st.packed = on ? 1 : 0;
   c->st.xpair = on && hermitian_pipe_path(g) ? 1 : 0;
@@ -1322,7 +1357,7 @@ pint_status pint_set_hermitian(pint_ctx *c, int32_t on) {
     // iterate storage: real fp64 in the Hermitian mode (its imaginary parts are zero in exact
     // arithmetic; roundoff-level ones are dropped), complex128 otherwise
     CUDA_TRY(c, launch_storage_convert(g, buffers(c), on != 0, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    PINT_SYNC(c);
   }
   c->hermitian = on != 0;
   return PINT_OK;
@@ -1439,7 +1474,7 @@ pint_status pint_sequential(pint_ctx *c) {
     else
       CUDA_TRY(c, launch_sequential_step(g, st, at, b, r0, c->u + (size_t)l * M * g.N, c->stream));
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   return PINT_OK;
 }
 
@@ -1471,7 +1506,7 @@ pint_status pint_debug_stage(pint_ctx *c, int32_t a, int32_t s) {
     double2 *x2 = (c->g.dim == 1 && c->lc.pcr_mode == 1) ? b.Y : b.X;
     CUDA_TRY(c, launch_backward(c->g, c->lc, c->st, at, b, x2, nullptr, c->stream, 0));
   } else return fail(PINT_ERR_INVALID, "stage must be 0, 1 or 2");
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   return PINT_OK;
 }
 
@@ -1481,7 +1516,7 @@ pint_status pint_debug_get_work(pint_ctx *c, int32_t which, double *host) {
   Buffers b = buffers(c);
   const double2 *src = which == 0 ? b.X : ((c->g.dim == 1 && c->lc.pcr_mode == 1) ? b.Y : b.X);
   CUDA_TRY(c, cudaMemcpyAsync(host, src, c->lay.vec_bytes, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PINT_SYNC(c);
   return PINT_OK;
 }
 

@@ -1384,17 +1384,21 @@ cudaError_t launch_pipe_dispatch(const Geometry &g, const StaticTables &st, cons
 // and T consecutive points n0.. over all L steps (rows at stride M N).  Tiles arrive by TMA in
 // 128-byte column boxes (8 points x up to 256 steps, 128-byte swizzle: conflict-free column
 // reads), two consumer groups run the register FFT engine on the T columns over a ring of three
-// slots, results leave through the slot in 128-byte row segments.
+// slots, results are put back into the slot in the boxes' layout and leave by the TMA unit.
 //   forward: X[p][m][n] = DIF_L(alpha^{l/L} r_l)[p]  (slot p holds frequency bitrev(p); the scale
-//            was applied by the residual kernel), P > 1: times the four-step twiddle twr[p]
-//   inverse: u[l][m][n] += alpha^{-l/L} / L * DIT_L(x2)[l]  (overwrite: = instead of +=), the
-//            last-step difference, and an L2 prefetch of the u tile when the x2 tile is issued.
+//            was applied by the residual kernel), P > 1: times the four-step twiddle twr[p];
+//            one tensor store per box.
+//   inverse: u[l][m][n] += alpha^{-l/L} / L * DIT_L(x2)[l]: the update is a TMA tensor
+//            REDUCTION (cp.reduce.async.bulk.tensor .add on the FLOAT64 map of u, UTMAREDG: the
+//            fp64 add happens at the L2, u never enters the SM); overwrite: a tensor store, the
+//            old last-step value read by the one thread per column that needs it; the last-step
+//            difference; optionally (pf) an L2 prefetch of the u tile when the x2 tile is issued.
 template <class PL, bool INV>
 __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     tfft_pipe_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmu,
                      const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X,
                      double2 *__restrict__ u, int lT, int G, int NS, int ls, int nitems,
-                     unsigned long long *diff_slot, int overwrite) {
+                     unsigned long long *diff_slot, int overwrite, int pf) {
   constexpr int NL = PL::N, TPL = PL::TPL, E = PL::E, R = 1 << PL::BL, TW = PL::twsize(), NP = PL::NP;
   constexpr int LB = NL < 256 ? NL : 256;   // steps per TMA box
   extern __shared__ __align__(1024) unsigned char smraw_[];
@@ -1402,7 +1406,10 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
   volatile int *slot_item = reinterpret_cast<volatile int *>(smraw + 64);   // item held by slot s (ring_wait)
   double2 *twl = reinterpret_cast<double2 *>(smraw + 128);
-  double2 *ring = reinterpret_cast<double2 *>(smraw + 1024 + (((size_t)TW * sizeof(double2) + 1023) & ~(size_t)1023));
+  constexpr size_t kTwBytes = ((size_t)TW * sizeof(double2) + 1023) & ~(size_t)1023;
+  constexpr size_t kScBytes = ((size_t)NL * sizeof(double) + 1023) & ~(size_t)1023;
+  double *sbw = reinterpret_cast<double *>(smraw + 1024 + kTwBytes);   // inverse: alpha^{-l/L} / L
+  double2 *ring = reinterpret_cast<double2 *>(smraw + 1024 + kTwBytes + kScBytes);
   __shared__ double red[16];
   const int T = 1 << lT, GT = T * TPL;
   const int tile_elems = NL * T, line_elems = T * ls;
@@ -1419,8 +1426,11 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     }
     mbar_init_fence();
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
+    if (INV) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmu) : "memory");
   }
   copy_table(twl, st.ptwL, TW);
+  if (INV)
+    for (int i = threadIdx.x; i < NL; i += blockDim.x) sbw[i] = __ldg(at.scale_bwd + i);
   __syncthreads();
   auto issue = [&](int k) {
     const int it = blockIdx.x + k * gridDim.x;
@@ -1432,7 +1442,7 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     for (int cb = 0; cb < T; cb += 8)
       for (int lb = 0; lb < NL; lb += LB) {
         tma_load_3d(dst + (size_t)cb * NL + lb * 8, &tmx, 2 * (n0 + cb), m, lb, bar);
-        if (INV && !overwrite)   // the epilogue's read of u: start it towards L2 now
+        if (INV && !overwrite && pf)   // the reduction's read of u: start it towards L2 now
           asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(&tmu),
                        "r"(2 * (n0 + cb)), "r"(m), "r"(lb)
                        : "memory");
@@ -1449,9 +1459,12 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     double2 *tile = ring + (size_t)s * slot_elems;
     const int m = it / per, n0 = (it - m * per) << lT;
     // column c of the tile: box c / 8, row l, 16-byte chunk (c mod 8) ^ (l mod 8)
-    const double2 *col = tile + (size_t)(c >> 3) * NL * 8;
+    double2 *col = tile + (size_t)(c >> 3) * NL * 8;
     const int cc = c & 7;
     double2 *line = tile + (size_t)c * ls;
+    double2 uold = make_double2(0.0, 0.0);
+    if (INV && overwrite && diff_slot && tau == TPL - 1)   // overwrite form: the old last-step value
+      uold = u[(size_t)(NL - 1) * lstride + (size_t)m * g.N + n0 + c];
     ring_wait(full + s, slot_item, k, NS);
     double2 v[E];
 #pragma unroll
@@ -1462,14 +1475,14 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     named_sync(gbar, GT);   // the slot becomes T exchange lines of stride ls
     if constexpr (!INV) {
       rfft::forward_regs<PL>(v, line, lid, tau, twl);
+      // slot order out: through the line once more so that every thread holds the slots
+      // tau + TPL i (the arrangement whose box rows are bank-conflict free)
       rfft::to_smem<PL, NP - 1>(v, line, tau);
-      named_sync(gbar, GT);
-      double2 *xo = X + (size_t)m * g.N + n0;
-      for (int i = t; i < (NL << lT); i += GT) {
-        const int cq = i & (T - 1), p = i >> lT;
-        double2 w = tile[(size_t)cq * ls + rfft::F<PL>(p)];
-        if (st.twr) w = cmul(w, __ldg(st.twr + p));   // P > 1: four-step twiddle
-        xo[(size_t)p * lstride + cq] = w;
+      rfft::line_sync<PL>(lid);
+      rfft::from_smem<PL, 0>(v, line, tau);
+      if (st.twr) {   // P > 1: four-step twiddle
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = cmul(v[i], __ldg(st.twr + rfft::natural_pos<PL>(tau, i)));
       }
     } else {
       // slot order in, natural steps out: place the values at their swizzled line positions,
@@ -1486,40 +1499,33 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
           v[uu * R + r] = w;
         }
       rfft::line_sync<PL>(lid);
-      rfft::inverse_in_regs<PL>(v, line, lid, tau, twl);
-      rfft::to_smem<PL, 0>(v, line, tau);
-      named_sync(gbar, GT);
-      double2 *ub = u + (size_t)m * g.N + n0;
-      constexpr int kB = 8;   // u loads in flight per thread
-      for (int b0 = t; b0 < (NL << lT); b0 += kB * GT) {
-        double2 uo[kB];
+      rfft::inverse_in_regs<PL>(v, line, lid, tau, twl);   // v[i]: step tau + TPL i
 #pragma unroll
-        for (int q = 0; q < kB; ++q) {
-          const int i = b0 + q * GT;
-          if (i < (NL << lT)) {
-            const int l = i >> lT;
-            const bool need_old = !overwrite || (diff_slot && l == NL - 1);
-            uo[q] = need_old ? ub[(size_t)l * lstride + (i & (T - 1))] : make_double2(0.0, 0.0);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < kB; ++q) {
-          const int i = b0 + q * GT;
-          if (i < (NL << lT)) {
-            const int cq = i & (T - 1), l = i >> lT;
-            const double2 cv = cscale(tile[(size_t)cq * ls + rfft::F<PL>(l)], __ldg(at.scale_bwd + l));
-            ub[(size_t)l * lstride + cq] = overwrite ? cv : cadd(uo[q], cv);
-            if (l == NL - 1) {
-              const double2 dd = overwrite ? csub(cv, uo[q]) : cv;
-              dmax = nanmax(dmax, hypot(dd.x, dd.y));
-            }
-          }
-        }
+      for (int i = 0; i < E; ++i) v[i] = cscale(v[i], sbw[rfft::natural_pos<PL>(tau, i)]);
+      if (tau == TPL - 1) {   // step L - 1
+        const double2 dd = overwrite ? csub(v[E - 1], uold) : v[E - 1];
+        dmax = nanmax(dmax, hypot(dd.x, dd.y));
       }
+    }
+    named_sync(gbar, GT);   // every line of the group read: the slot becomes the boxes again
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int l = rfft::natural_pos<PL>(tau, i);
+      col[l * 8 + (cc ^ (l & 7))] = v[i];
     }
     fence_proxy_async_smem();
     named_sync(gbar, GT);
-    if (t == 0) issue(k + NS);
+    if (t == 0) {
+      for (int cb = 0; cb < T; cb += 8)
+        for (int lb = 0; lb < NL; lb += LB) {
+          const double2 *src = tile + (size_t)cb * NL + lb * 8;
+          if (INV && !overwrite) tma_reduce_add_3d(&tmu, 2 * (n0 + cb), m, lb, src);
+          else tma_store_3d(INV ? &tmu : &tmx, 2 * (n0 + cb), m, lb, src);
+        }
+      bulk_commit();
+      bulk_wait_read();   // the TMA unit has read the slot: refill it
+      issue(k + NS);
+    }
   }
   if (INV && diff_slot) {
     for (int o = 16; o > 0; o >>= 1) dmax = nanmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -1531,6 +1537,16 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
       atomicMax(diff_slot, (unsigned long long)__double_as_longlong(vmax));
     }
   }
+}
+
+// A/B (experiments build): PINT_TFFT_PF=1 prefetches the u tile towards the L2 when the x2 tile is issued
+static int tfft_prefetch() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_TFFT_PF");
+    v = (e && atoi(e)) ? 1 : 0;
+  }
+  return v;
 }
 
 struct TfftPlan {
@@ -1553,7 +1569,8 @@ bool tfft_plan(const Geometry &g, TfftPlan &tp) {
   if (PL::TPL > 32 && tp.G * T + tp.G + 1 > 16) return false;   // named barrier ids
   const size_t tile = (size_t)PL::N * T * 16, lines = (size_t)T * tp.ls * 16;
   const size_t slot = ((tile > lines ? tile : lines) + 1023) & ~(size_t)1023;
-  tp.smem = 1024 + 1024 + (((size_t)PL::twsize() * 16 + 1023) & ~(size_t)1023) + tp.NS * slot;
+  tp.smem = 1024 + 1024 + (((size_t)PL::twsize() * 16 + 1023) & ~(size_t)1023) +
+            (((size_t)PL::N * 8 + 1023) & ~(size_t)1023) + tp.NS * slot;
   return tp.smem <= 227 * 1024;
 }
 
@@ -1590,10 +1607,10 @@ cudaError_t launch_tfft_l(const Geometry &g, const StaticTables &st, const Alpha
   AlphaTables a = at ? *at : AlphaTables{};
   if (inverse)
     tfft_pipe_kernel<PL, true><<<sms, threads, tp.smem, s>>>(tmx, tmu, g, st, a, X, u, tp.lT, tp.G, tp.NS, tp.ls,
-                                                             nitems, diff_slot, overwrite);
+                                                             nitems, diff_slot, overwrite, tfft_prefetch());
   else
     tfft_pipe_kernel<PL, false><<<sms, threads, tp.smem, s>>>(tmx, tmu, g, st, a, X, u, tp.lT, tp.G, tp.NS, tp.ls,
-                                                              nitems, nullptr, 0);
+                                                              nitems, nullptr, 0, 0);
   return cudaGetLastError();
 }
 
