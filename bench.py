@@ -38,6 +38,9 @@ ALGO_BYTES = {"fwd_kernel": 32, "pcr_classes_kernel": 32, "pcr_chunk_kernel": 32
               "rows_pipe_kernel<fwd>": 32, "cols_pipe_kernel": 32, "rows_pipe_kernel<inv>": 32,
               # pipelined time transforms (forward in place, inverse x2 + u -> u)
               "tfft_pipe_kernel<fwd>": 32, "tfft_pipe_kernel<inv>": 48,
+              # TMA-staged time tiles (the inverse's u += c is a TMA reduce-add at the L2: u is still read
+              # and written once in HBM)
+              "tfft_fwd_tma_kernel": 32, "tfft_bwd_tma_kernel": 48,
               # fused R / C / I plane passes (one launch; compulsory 3 x 32 B, L2 reuse can only lower it)
               "spatial_fused_kernel": 96,
               # 1-D pipelined passes (TMA forward tile, two-pass PCR)
@@ -51,7 +54,8 @@ ALGO_BYTES_DIRECT = {"direct_r0_kernel": 0, "plane_rows_dif_kernel": 0, "plane_c
                      "spec_blocked_kernel": 0, "cols_direct_kernel": 16, "cols_pipe_kernel<synth>": 16,
                      "fft2d_rows_kernel<inv>": 32, "rows_pipe_kernel<inv>": 32, "tfft_bwd_kernel": 32,
                      "pcr_classes_kernel": 16, "pcr_chunk_kernel": 32, "bwd_kernel": 32,
-                     "spatial2d_kernel": 48, "tfft_pipe_kernel<inv>": 32}
+                     "spatial2d_kernel": 48, "tfft_pipe_kernel<inv>": 32,
+                     "tfft_bwd_tma_kernel": 32}
 # real-data (Hermitian) mode: u stored as real fp64 (8 B per unknown), time series packed two real
 # points per complex value (8 B per unknown), L/2 + 1 of the L frequencies solved (unit planes:
 # 8 B per unknown, up to a factor 1 + 2/L)

@@ -590,6 +590,109 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 }
 
 // ---------------------------------------------------------------------------------------------
+// TMA variants of the 2-D time tiles (complex storage, one rank or sharded; 2 T <= 256 doubles
+// per box row).  The tile [L][T] is exactly the unswizzled box {2 T doubles, 1 node, min(L, 256)
+// steps} of the 3-D map over X / x2 / u, so one thread moves it with cp.async.bulk.tensor (no
+// per-thread address arithmetic or LSU traffic for the copies):
+//   forward: tensor load, DIF, (P > 1: four-step twiddle), tensor store in place;
+//   inverse: tensor load of x2, DIT, x alpha^{-l/L} / L in shared memory, and the update
+//            u += c leaves as a TMA tensor REDUCTION (cp.reduce.async.bulk.tensor .add on the
+//            FLOAT64 map, UTMAREDG): the fp64 add is performed at the L2, the old u never enters
+//            the SM, and the CTA retires without waiting for a u round trip (the exposed latency
+//            of tfft_bwd_kernel).  overwrite (direct form): a tensor store; the old last-step
+//            values (T of them) are read early for the difference.
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tfft_fwd_tma_kernel(const __grid_constant__ CUtensorMap tmx, Geometry g, StaticTables st, int T) {
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int lT = 31 - __clz(T);
+  const int per = g.N / T;
+  const int m = blockIdx.x / per;
+  const int n0 = (blockIdx.x - m * per) * T;
+  const int all = g.L * T, LB = g.L < 256 ? g.L : 256;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+    mbar_arrive_expect_tx(&bar, (unsigned)(all * sizeof(double2)));
+    for (int lb = 0; lb < g.L; lb += LB) tma_load_3d(sm + (size_t)lb * T, &tmx, 2 * n0, m, lb, &bar);
+  }
+  for (int i = threadIdx.x; i < g.L; i += blockDim.x) sm[all + i] = __ldg(st.twL + i);   // time twiddles
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  fft_dif<3, false>(sm, T, 1, T, g.L, g.logL, sm + all);
+  if (st.twr) {   // P > 1: four-step twiddle
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) sm[idx] = cmul(sm[idx], __ldg(st.twr + (idx >> lT)));
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int lb = 0; lb < g.L; lb += LB) tma_store_3d(&tmx, 2 * n0, m, lb, sm + (size_t)lb * T);
+    bulk_commit();
+    bulk_wait_read();   // the tile must stay in shared memory until the TMA unit has read it
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tfft_bwd_tma_kernel(const __grid_constant__ CUtensorMap tmx2, const __grid_constant__ CUtensorMap tmu, Geometry g,
+                        StaticTables st, AlphaTables at, const double2 *__restrict__ u, int T,
+                        unsigned long long *diff_slot, int overwrite) {
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double red[32];
+  __shared__ double2 uold[128];
+  const int lT = 31 - __clz(T);
+  const int per = g.N / T;
+  const int m = blockIdx.x / per;
+  const int n0 = (blockIdx.x - m * per) * T;
+  const int all = g.L * T, LB = g.L < 256 ? g.L : 256;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+    mbar_arrive_expect_tx(&bar, (unsigned)(all * sizeof(double2)));
+    for (int lb = 0; lb < g.L; lb += LB) tma_load_3d(sm + (size_t)lb * T, &tmx2, 2 * n0, m, lb, &bar);
+  }
+  if (overwrite && diff_slot && threadIdx.x < T)   // direct form: the old last-step values
+    uold[threadIdx.x] = u[((size_t)(g.L - 1) * g.M + m) * g.N + n0 + threadIdx.x];
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (st.twr) {  // P > 1: inverse four-step twiddle
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) sm[idx] = cmulc(sm[idx], __ldg(st.twr + (idx >> lT)));
+    __syncthreads();
+  }
+  fft_dit_inv<3, false>(sm, T, 1, T, g.L, g.logL, st.twL);
+  double dmax = 0.0;
+  for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+    const int l = idx >> lT;
+    const double2 c = cscale(sm[idx], __ldg(at.scale_bwd + l));
+    sm[idx] = c;
+    if (l == g.L - 1) {
+      const double2 dd = overwrite ? csub(c, uold[idx & (T - 1)]) : c;
+      dmax = nanmax(dmax, hypot(dd.x, dd.y));
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int lb = 0; lb < g.L; lb += LB) {
+      if (overwrite) tma_store_3d(&tmu, 2 * n0, m, lb, sm + (size_t)lb * T);
+      else tma_reduce_add_3d(&tmu, 2 * n0, m, lb, sm + (size_t)lb * T);
+    }
+    bulk_commit();
+  }
+  if (diff_slot) {
+    for (int o = 16; o > 0; o >>= 1) dmax = nanmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = nanmax(v, red[w]);
+      atomicMax(diff_slot, dbl_bits(v));
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_read();   // the tile must stay in shared memory until the TMA unit has read it
+}
+
+// ---------------------------------------------------------------------------------------------
 // 2-D residual: X[l][m][n] = alpha^{l/L} (w - C u)[l][m][n] on spatial blocks BY x BX with a
 // one-point halo staged in shared memory (all M nodes of one l per CTA).  Each warp stages whole
 // halo rows (lanes along x: no index divisions), each thread then evaluates BX*BY/256 points.
@@ -1409,6 +1512,29 @@ static bool legacy_tfft() {
   }
   return v == 1;
 }
+// TMA variants of the 2-D time tiles (tfft_fwd_tma_kernel / tfft_bwd_tma_kernel): complex storage,
+// box rows of 2 T <= 256 doubles, L <= 256 or a multiple of 256.  PINT_TFFT_TMA=0 (experiments
+// build) selects the per-thread copies for A/B runs.
+static bool tfft_tma_ok(const Geometry &g, const StaticTables &st, int T) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_TFFT_TMA");
+    v = (e && !atoi(e)) ? 0 : 1;
+  }
+  return v == 1 && g.dim == 2 && g.pow2 && !st.packed && T >= 1 && 2 * T <= 256 && T <= g.N && g.N % T == 0 &&
+         (g.L <= 256 || g.L % 256 == 0) && tma_encode_fn() != nullptr;
+}
+// 3-D map over a [L][M][N] complex array as doubles {2N, M, L}, box {2 T doubles, 1 node, min(L, 256) steps}
+static bool time_tile_map(const Geometry &g, const double2 *base, int T, CUtensorMap &tm) {
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * g.N, (cuuint64_t)g.M, (cuuint64_t)g.L};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.N * 16, (cuuint64_t)g.M * g.N * 16};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * T), 1, (cuuint32_t)(g.L < 256 ? g.L : 256)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 static bool legacy2d() {
   static int v = -1;
   if (v < 0) {
@@ -1510,11 +1636,22 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
   static const char *k2f[] = {"residual2d_kernel", "tfft_fwd_kernel", "spatial_fused_kernel", "tfft_bwd_kernel"};
   if (g.dim == 2) {
     if (pipe2d(g, st) && spatial_fused_supported(g, st)) return k2f[i];
-    if (pipe2d(g, st)) return tfft_pipe_supported(g, st) && !legacy_tfft() ? k2t[i] : k2q[i];
+    if (pipe2d(g, st)) {
+      if (tfft_pipe_supported(g, st) && !legacy_tfft()) return k2t[i];
+      if (tfft_tma_ok(g, st, lc.tfft_T)) {
+        if (i == 1) return "tfft_fwd_tma_kernel";
+        if (i == n - 1) return "tfft_bwd_tma_kernel";
+      }
+      return k2q[i];
+    }
     const char *nm = reg2d(g) ? k2p[i] : k2[i];
     if (tfft_pipe_supported(g, st) && !legacy_tfft()) {   // time transforms pipelined, spatial legacy
       if (i == 1) return "tfft_pipe_kernel<fwd>";
       if (i == n - 1) return "tfft_pipe_kernel<inv>";
+    }
+    if (tfft_tma_ok(g, st, lc.tfft_T)) {
+      if (i == 1) return "tfft_fwd_tma_kernel";
+      if (i == n - 1) return "tfft_bwd_tma_kernel";
     }
     return nm;
   }
@@ -1687,8 +1824,15 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     int T2 = lc.tfft_T;
     while (T2 > gt.N) T2 >>= 1;
     const size_t sm2 = (size_t)g.L * (T2 + 1) * sizeof(double2);   // tile + staged twiddles
-    e = set_smem((const void *)tfft_fwd_kernel, sm2);
-    if (e == cudaSuccess) tfft_fwd_kernel<<<g.M * (gt.N / T2), kTileThreads, sm2, s>>>(gt, st, b.X, T2);
+    if (T2 == lc.tfft_T && tfft_tma_ok(gt, st, T2)) {   // tile moved by the TMA unit
+      CUtensorMap tmx;
+      if (!time_tile_map(gt, b.X, T2, tmx)) return cudaErrorNotSupported;
+      e = set_smem((const void *)tfft_fwd_tma_kernel, sm2);
+      if (e == cudaSuccess) tfft_fwd_tma_kernel<<<g.M * (gt.N / T2), kTileThreads, sm2, s>>>(tmx, gt, st, T2);
+    } else {
+      e = set_smem((const void *)tfft_fwd_kernel, sm2);
+      if (e == cudaSuccess) tfft_fwd_kernel<<<g.M * (gt.N / T2), kTileThreads, sm2, s>>>(gt, st, b.X, T2);
+    }
     rec(s);
   }
   if (e != cudaSuccess) return e;
@@ -1804,10 +1948,19 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   if (!g.pow2) {   // generic grids: G^{-1} S was applied by the solve; inverse DFT on T | N columns
     const int T2 = lc.tfft_T;
     const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
-    e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
-    if (e == cudaSuccess)
-      tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
-                                                                           (unsigned long long *)diff_slot, overwrite);
+    if (tfft_tma_ok(g, st, T2)) {   // TMA tile in, u += c as a TMA reduce-add (overwrite: a store)
+      CUtensorMap tmx2, tmu;
+      if (!time_tile_map(g, x2, T2, tmx2) || !time_tile_map(g, b.u, T2, tmu)) return cudaErrorNotSupported;
+      e = set_smem((const void *)tfft_bwd_tma_kernel, sm2);
+      if (e == cudaSuccess)
+        tfft_bwd_tma_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(tmx2, tmu, g, st, at, b.u, T2,
+                                                                        (unsigned long long *)diff_slot, overwrite);
+    } else {
+      e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
+      if (e == cudaSuccess)
+        tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
+                                                                             (unsigned long long *)diff_slot, overwrite);
+    }
   } else if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
       if (st.packed) {
@@ -1866,6 +2019,7 @@ const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const Sta
   if (i < 0 || i >= n) return "";
   if (g.dim == 2) {
     if (i == n - 1 && tfft_pipe_supported(g, st) && !legacy_tfft()) return "tfft_pipe_kernel<inv>";
+    if (i == n - 1 && !st.packed && tfft_tma_ok(g, st, lc.tfft_T)) return "tfft_bwd_tma_kernel";
     if (pipe2d(g, st)) return k2q[i];
     return reg2d(g) ? k2p[i] : k2[i];
   }

@@ -1398,7 +1398,7 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     tfft_pipe_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmu,
                      const Geometry g, StaticTables st, AlphaTables at, double2 *__restrict__ X,
                      double2 *__restrict__ u, int lT, int G, int NS, int ls, int nitems,
-                     unsigned long long *diff_slot, int overwrite, int pf) {
+                     unsigned long long *diff_slot, int overwrite, int pf, int pair) {
   constexpr int NL = PL::N, TPL = PL::TPL, E = PL::E, R = 1 << PL::BL, TW = PL::twsize(), NP = PL::NP;
   constexpr int LB = NL < 256 ? NL : 256;   // steps per TMA box
   extern __shared__ __align__(1024) unsigned char smraw_[];
@@ -1432,8 +1432,12 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
   if (INV)
     for (int i = threadIdx.x; i < NL; i += blockDim.x) sbw[i] = __ldg(at.scale_bwd + i);
   __syncthreads();
+  // pair: the CTA's items k, k + 1 are neighbours in n (256 contiguous bytes per step between them)
+  auto item_of = [&](int k) {
+    return pair ? 2 * ((int)blockIdx.x + (k >> 1) * (int)gridDim.x) + (k & 1) : (int)blockIdx.x + k * (int)gridDim.x;
+  };
   auto issue = [&](int k) {
-    const int it = blockIdx.x + k * gridDim.x;
+    const int it = item_of(k);
     if (it >= nitems) return;
     const int m = it / per, n0 = (it - m * per) << lT;
     uint64_t *bar = full + k % NS;
@@ -1453,7 +1457,7 @@ __global__ void __launch_bounds__(PL::E == 32 ? 256 : 512, 1)
     for (int k = 0; k < NS; ++k) issue(k);
   double dmax = 0.0;
   for (int k = gid;; k += G) {
-    const int it = blockIdx.x + k * gridDim.x;
+    const int it = item_of(k);
     if (it >= nitems) break;
     const int s = k % NS;
     double2 *tile = ring + (size_t)s * slot_elems;
@@ -1549,6 +1553,23 @@ static int tfft_prefetch() {
   return v;
 }
 
+static int tfft_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_TFFT_PAIR");
+    v = (e && atoi(e)) ? 1 : 0;
+  }
+  return v;
+}
+static int tfft_promo256() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_TFFT_PROMO");
+    v = (e && atoi(e)) ? 1 : 0;
+  }
+  return v;
+}
+
 struct TfftPlan {
   int lT, G, NS, ls;
   size_t smem;
@@ -1583,7 +1604,8 @@ bool time_map(const Geometry &g, double2 *base, CUtensorMap &tm) {
   const cuuint32_t box[3] = {16, 1, (cuuint32_t)(g.L < 256 ? g.L : 256)};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             tfft_promo256() ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1607,10 +1629,10 @@ cudaError_t launch_tfft_l(const Geometry &g, const StaticTables &st, const Alpha
   AlphaTables a = at ? *at : AlphaTables{};
   if (inverse)
     tfft_pipe_kernel<PL, true><<<sms, threads, tp.smem, s>>>(tmx, tmu, g, st, a, X, u, tp.lT, tp.G, tp.NS, tp.ls,
-                                                             nitems, diff_slot, overwrite, tfft_prefetch());
+                                                             nitems, diff_slot, overwrite, tfft_prefetch(), tfft_pair());
   else
     tfft_pipe_kernel<PL, false><<<sms, threads, tp.smem, s>>>(tmx, tmu, g, st, a, X, u, tp.lT, tp.G, tp.NS, tp.ls,
-                                                              nitems, nullptr, 0, 0);
+                                                              nitems, nullptr, 0, 0, tfft_pair());
   return cudaGetLastError();
 }
 
