@@ -894,15 +894,22 @@ __global__ void __launch_bounds__(GC * 256 / (PY::TPL == 32 && PY::E == 32 ? 2 :
     double2 *line = tile + (size_t)c * ls;
     // column c, row y of the swizzled TMA tile: 16-byte chunk c ^ ((y TC / 8) mod TC) of row y
     if constexpr (SYN) {   // the x1 spectrum sig_q r0hat at the DIF output positions (rows = P)
+      // read in the natural arrangement (consecutive rows on consecutive lanes: conflict free) and
+      // regroup through the exchange line; reading the last pass's rows R_L g + r straight from the
+      // tile put all eight lanes of a quarter warp on one bank slot
       const double2 sg = my_scal[1];
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int y = rfft::natural_pos<PY>(tau, i);
+        v[i] = cmul(sg, tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))]);
+      }
+      named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
+      rfft::to_smem<PY, 0>(v, line, tau);
+      rfft::line_sync<PY>(lid);
 #pragma unroll
       for (int u = 0; u < E / R; ++u)
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int y = rfft::last_pos<PY>(tau, u, r);
-          v[u * R + r] = cmul(sg, tile[(y << lT) + (c ^ (((y << lT) >> 3) & (TC - 1)))]);
-        }
-      named_sync(gbar, GT);   // the slot is re-used as TC exchange lines of stride ls
+        for (int r = 0; r < R; ++r) v[u * R + r] = line[rfft::F<PY>(rfft::last_pos<PY>(tau, u, r))];
     } else {
 #pragma unroll
       for (int i = 0; i < E; ++i) {
