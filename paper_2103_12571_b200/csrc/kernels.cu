@@ -702,10 +702,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 // HW: halo width (1 for the 3-point operators, up to 3 for the kappa-6 / upwind-5 stencils);
 // weights outside [-hx0, hx1] x [-hy0, hy1] are zero in g.wx / g.wy.
 template <int M, bool PACK, int HW>
-__global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometry g, StaticTables st, AlphaTables at,
+__global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(const __grid_constant__ CUtensorMap tmu, int tma,
+                                                         Geometry g, StaticTables st, AlphaTables at,
                                                          const double2 *__restrict__ u,
                                                          double2 *__restrict__ X, int BX, int BY, int LG) {
-  extern __shared__ double2 sm[];  // [1 + PACK][M][BY+2HW][BX+2HW]
+  extern __shared__ __align__(128) double2 sm[];  // [1 + PACK][M][BY+2HW][BX+2HW]
+  __shared__ __align__(8) uint64_t bar;
   const bool xp = PACK && st.xpair;   // packed partner (y, x + nx/2) instead of (y + ny/2, x)
   const int bxs = (xp ? g.nx / 2 : g.nx) / BX, bys = (PACK && !xp ? g.ny / 2 : g.ny) / BY;
   int b = blockIdx.x;
@@ -777,12 +779,25 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
     return;
   } else {
   const double2 *ul = u + (size_t)l * plane;
-  for (int r = warp; r < M * H; r += blockDim.x >> 5) {
-    const int j = r / H, yy = r - j * H;
-    const int y = (y0 + yy - HW) & (g.ny - 1);
-    const double2 *src = ul + (size_t)j * g.N + ((size_t)y << g.lognx);
-    double2 *dst = sm + r * W;
-    for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
+  // a block whose halo does not wrap around the periodic boundary is one tensor box {2 W doubles, H
+  // rows, M nodes} of u: one thread hands it to the TMA unit; the blocks on the boundary (2 of the
+  // nx / BX block columns, 2 of the ny / BY block rows) stage their rows with cp.async
+  const bool box = tma && x0 >= HW && x0 + BX + HW <= g.nx && y0 >= HW && y0 + BY + HW <= g.ny;
+  if (box) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_init_fence();
+      mbar_arrive_expect_tx(&bar, (unsigned)(M * H * W * sizeof(double2)));
+      tma_load_3d(sm, &tmu, 2 * (x0 - HW), y0 - HW, l * M, &bar);
+    }
+  } else {
+    for (int r = warp; r < M * H; r += blockDim.x >> 5) {
+      const int j = r / H, yy = r - j * H;
+      const int y = (y0 + yy - HW) & (g.ny - 1);
+      const double2 *src = ul + (size_t)j * g.N + ((size_t)y << g.lognx);
+      double2 *dst = sm + r * W;
+      for (int xx = lane; xx < W; xx += 32) cp_async16(dst + xx, src + ((x0 + xx - HW) & (g.nx - 1)));
+    }
   }
   // the H-term block (last node of step l - 1, or u0 for global step 0) is staged with the tile, so
   // the point loop below has no global load whose latency it would expose
@@ -797,6 +812,7 @@ __global__ void __launch_bounds__(256, M <= 4 ? 4 : 2) residual2d_kernel(Geometr
   }
   cp_async_wait_all();
   __syncthreads();
+  if (box) mbar_wait(&bar, 0);
   for (int pt = threadIdx.x; pt < BX * BY; pt += blockDim.x) {
     const int ty = pt / BX, tx = pt - ty * BX;
     const int n = ((y0 + ty) << g.lognx) + x0 + tx;
@@ -1799,9 +1815,24 @@ cudaError_t launch_forward(const Geometry &g, const LaunchCfg &lc, const StaticT
     // 14.3 -> 13.6 ms measured in round 1; config 4's 4 MB planes: slower, so not there)
     int lg = (size_t)g.N * sizeof(double2) >= ((size_t)8 << 20) ? 8 : 1;
     while (lg > 1 && g.L % lg) lg >>= 1;
+    // complex storage: the halo tile of an interior block is one tensor box of u (TMA); PINT_RES_TMA=0
+    // (experiments build) keeps the cp.async staging everywhere for A/B runs
+    CUtensorMap tmu{};
+    int tma = 0;
+    if (!pk && 2 * (BX + 2 * hw) <= 256 && BY + 2 * hw <= 256 && g.M <= 256) {
+      const char *ev = experiment_env("PINT_RES_TMA");
+      auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
+      const cuuint64_t dims[3] = {(cuuint64_t)2 * g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.L * g.M};
+      const cuuint64_t strides[2] = {(cuuint64_t)g.nx * 16, (cuuint64_t)g.N * 16};
+      const cuuint32_t box[3] = {(cuuint32_t)(2 * (BX + 2 * hw)), (cuuint32_t)(BY + 2 * hw), (cuuint32_t)g.M};
+      const cuuint32_t es[3] = {1, 1, 1};
+      tma = enc && !(ev && !atoi(ev)) &&
+            enc(&tmu, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.u, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
 #define PINT_RES2D(MM_, PK_, HW_)                                                                   \
   e = set_smem((const void *)residual2d_kernel<MM_, PK_, HW_>, rs, true);                            \
-  if (e == cudaSuccess) residual2d_kernel<MM_, PK_, HW_><<<rgrid, 256, rs, s>>>(g, st, at, b.u, b.X, BX, BY, lg);
+  if (e == cudaSuccess) residual2d_kernel<MM_, PK_, HW_><<<rgrid, 256, rs, s>>>(tmu, tma, g, st, at, b.u, b.X, BX, BY, lg);
     PINT_DISPATCH_M(g.M, {
       if (pk) {
         if (hw == 1) { PINT_RES2D(MM, true, 1) } else if (hw == 2) { PINT_RES2D(MM, true, 2) } else { PINT_RES2D(MM, true, 3) }
