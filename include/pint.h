@@ -71,7 +71,8 @@ typedef enum {
   PINT_ERR_NOT_DIAGONALIZABLE = 3,  /* cond(S_k) > 1e8 or eigenvalue gap < 1e-8 rho(B_k)     */
   PINT_ERR_NUMERIC = 4,             /* non-finite u0, residual norm or last-step difference     */
   PINT_ERR_CUDA = 5,                /* CUDA runtime error (context poisoned)                   */
-  PINT_ERR_NCCL = 6,                /* communication error (context poisoned)                  */
+  PINT_ERR_NCCL = 6,                /* communication error, also an asynchronous one found while
+                                       waiting on the stream (communicator aborted, context poisoned) */
   PINT_ERR_STATE = 7                /* context poisoned by an earlier CUDA/NCCL error          */
 } pint_status;
 

@@ -1540,6 +1540,15 @@ static bool tfft_tma_ok(const Geometry &g, const StaticTables &st, int T) {
   return v == 1 && g.dim == 2 && g.pow2 && !st.packed && T >= 1 && 2 * T <= 256 && T <= g.N && g.N % T == 0 &&
          (g.L <= 256 || g.L % 256 == 0) && tma_encode_fn() != nullptr;
 }
+// the inverse's TMA variant alone can be switched off (PINT_TFFT_BWD_TMA=0, experiments build)
+static bool tfft_bwd_tma_ok(const Geometry &g, const StaticTables &st, int T) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_TFFT_BWD_TMA");
+    v = (e && !atoi(e)) ? 0 : 1;
+  }
+  return v == 1 && tfft_tma_ok(g, st, T);
+}
 // 3-D map over a [L][M][N] complex array as doubles {2N, M, L}, box {2 T doubles, 1 node, min(L, 256) steps}
 static bool time_tile_map(const Geometry &g, const double2 *base, int T, CUtensorMap &tm) {
   auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
@@ -1656,7 +1665,7 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
       if (tfft_pipe_supported(g, st) && !legacy_tfft()) return k2t[i];
       if (tfft_tma_ok(g, st, lc.tfft_T)) {
         if (i == 1) return "tfft_fwd_tma_kernel";
-        if (i == n - 1) return "tfft_bwd_tma_kernel";
+        if (i == n - 1 && tfft_bwd_tma_ok(g, st, lc.tfft_T)) return "tfft_bwd_tma_kernel";
       }
       return k2q[i];
     }
@@ -1667,7 +1676,7 @@ const char *kernel_name(const Geometry &g, const LaunchCfg &lc, const StaticTabl
     }
     if (tfft_tma_ok(g, st, lc.tfft_T)) {
       if (i == 1) return "tfft_fwd_tma_kernel";
-      if (i == n - 1) return "tfft_bwd_tma_kernel";
+      if (i == n - 1 && tfft_bwd_tma_ok(g, st, lc.tfft_T)) return "tfft_bwd_tma_kernel";
     }
     return nm;
   }
@@ -1979,19 +1988,10 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   if (!g.pow2) {   // generic grids: G^{-1} S was applied by the solve; inverse DFT on T | N columns
     const int T2 = lc.tfft_T;
     const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
-    if (tfft_tma_ok(g, st, T2)) {   // TMA tile in, u += c as a TMA reduce-add (overwrite: a store)
-      CUtensorMap tmx2, tmu;
-      if (!time_tile_map(g, x2, T2, tmx2) || !time_tile_map(g, b.u, T2, tmu)) return cudaErrorNotSupported;
-      e = set_smem((const void *)tfft_bwd_tma_kernel, sm2);
-      if (e == cudaSuccess)
-        tfft_bwd_tma_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(tmx2, tmu, g, st, at, b.u, T2,
-                                                                        (unsigned long long *)diff_slot, overwrite);
-    } else {
-      e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
-      if (e == cudaSuccess)
-        tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
-                                                                             (unsigned long long *)diff_slot, overwrite);
-    }
+    e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
+    if (e == cudaSuccess)
+      tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
+                                                                           (unsigned long long *)diff_slot, overwrite);
   } else if (g.dim == 1) {
     PINT_DISPATCH_M(g.M, {
       if (st.packed) {
@@ -2021,10 +2021,19 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
   } else {
     const int T2 = lc.tfft_T;
     const size_t sm2 = (size_t)g.L * T2 * sizeof(double2);
-    e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
-    if (e == cudaSuccess)
-      tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
-                                                                           (unsigned long long *)diff_slot, overwrite);
+    if (tfft_bwd_tma_ok(g, st, T2)) {   // TMA tile in, u += c as a TMA reduce-add (overwrite: a store)
+      CUtensorMap tmx2, tmu;
+      if (!time_tile_map(g, x2, T2, tmx2) || !time_tile_map(g, b.u, T2, tmu)) return cudaErrorNotSupported;
+      e = set_smem((const void *)tfft_bwd_tma_kernel, sm2);
+      if (e == cudaSuccess)
+        tfft_bwd_tma_kernel<<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(tmx2, tmu, g, st, at, b.u, T2,
+                                                                        (unsigned long long *)diff_slot, overwrite);
+    } else {
+      e = set_smem((const void *)tfft_bwd_kernel<false>, sm2);
+      if (e == cudaSuccess)
+        tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
+                                                                             (unsigned long long *)diff_slot, overwrite);
+    }
   }
   rec(s);
   if (e != cudaSuccess) return e;
@@ -2050,7 +2059,7 @@ const char *kernel_name_direct(const Geometry &g, const LaunchCfg &lc, const Sta
   if (i < 0 || i >= n) return "";
   if (g.dim == 2) {
     if (i == n - 1 && tfft_pipe_supported(g, st) && !legacy_tfft()) return "tfft_pipe_kernel<inv>";
-    if (i == n - 1 && !st.packed && tfft_tma_ok(g, st, lc.tfft_T)) return "tfft_bwd_tma_kernel";
+    if (i == n - 1 && !st.packed && tfft_bwd_tma_ok(g, st, lc.tfft_T)) return "tfft_bwd_tma_kernel";
     if (pipe2d(g, st)) return k2q[i];
     return reg2d(g) ? k2p[i] : k2[i];
   }

@@ -39,6 +39,15 @@ def test_operator_parity(p):
     assert max(errs) <= TOL, errs
 
 
+@pytest.mark.parametrize("p", W.halo_box_cases(), ids=lambda p: p.name)
+def test_residual_halo_boxes(p):
+    """residual2d_kernel stages the halo tile of a block that does not wrap the periodic boundary
+    as one TMA tensor box and the boundary blocks row by row: 256 x 32 grids hold both kinds, for
+    halo widths 1, 2 and 3 (the small operator cases above only have wrapping blocks)."""
+    errs = _run(p, p.u0(), iters=2)
+    assert max(errs) <= TOL, errs
+
+
 @pytest.mark.parametrize("name", ["disc_heat6_2d_M3", "disc_upwind5_2d_M3", "disc_upwind3_1d_M2",
                                   "disc_heat6_1d_N16384"])
 def test_operator_parity_direct_form(name):

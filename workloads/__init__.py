@@ -210,6 +210,19 @@ def discretisation_cases():
     return out
 
 
+def halo_box_cases():
+    """2-D grids wide and tall enough (256 x 32, residual blocks of 64 x 8) to have residual blocks
+    whose halo does not wrap the periodic boundary next to blocks whose halo does, for every halo
+    width of the paper's stencils (1: kappa 2, upwind 1; 2: kappa 4, upwind 3; 3: kappa 6, upwind 5,
+    with a mirrored one): the two staging paths of the residual kernel side by side.  L = 4, seeded
+    random complex u0."""
+    base = Problem("halo", 2, 256, 32, "heat", 1e-2, 0.0, 0.0, 0.02, 4, 2, "random", "fixed", 1e-3, 2)
+    out = [base.replace(name=f"halo_{op}_M{M}", op=op, M=M) for op, M in (("heat", 1), ("heat4", 2), ("heat6", 3))]
+    adv = base.replace(nu=0.0, cx=1.0, cy=-0.5, T=0.002)
+    out += [adv.replace(name=f"halo_{op}_M{M}", op=op, M=M) for op, M in (("upwind1", 4), ("upwind3", 2), ("upwind5", 3))]
+    return out
+
+
 def table_cases():
     """The paper's own test problems at their Table 1/2 sizes:
     heat u_t = Laplace(u) (nu = 1, centred kappa 2/4/6) and advection u_t + u_x + u_y = 0 (upwind
