@@ -305,10 +305,15 @@ __device__ __forceinline__ unsigned long long dbl_bits(double v) { return (unsig
 // conjugate counterpart); the inverse FFT's real / imaginary parts update u at n' and n' + N/2.
 template <int M, bool NODE, bool PACK = false>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
-    bwd_kernel(Geometry g, StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
+    bwd_kernel(const __grid_constant__ CUtensorMap tmx2, const __grid_constant__ CUtensorMap tmu, int tma, Geometry g,
+               StaticTables st, AlphaTables at, const double2 *__restrict__ X2,
                double2 *__restrict__ u, int T, unsigned long long *diff_slot, int overwrite) {
-  extern __shared__ double2 sm[];
+  // tma (complex storage): the tile [L][M][T] is the unswizzled tensor box {2 T doubles, M nodes,
+  // min(L, 256) steps} of X2 / u: tensor load in, and the update u += c leaves as a TMA tensor
+  // reduce-add performed at the L2 (overwrite: a tensor store), as in tfft_bwd_tma_kernel
+  extern __shared__ __align__(128) double2 sm[];
   __shared__ double red[32];
+  __shared__ __align__(8) uint64_t bar;
   const int lT = 31 - __clz(T);
   const int n0 = blockIdx.x * T;
   const int L = g.L;
@@ -341,6 +346,16 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     }
     __syncthreads();
   } else {
+    if (tma) {
+      if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+        mbar_arrive_expect_tx(&bar, (unsigned)(all * sizeof(double2)));
+        for (int lb = 0; lb < L; lb += 256) tma_load_3d(sm + (size_t)lb * M * T, &tmx2, 2 * n0, 0, lb, &bar);
+      }
+      __syncthreads();
+      mbar_wait(&bar, 0);
+    } else {
     // async tile load X2[p][m][n0..n0+T) -> sm, and an L2 prefetch of the u tile for the update
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
       const int t = idx & (T - 1), row = idx >> lT;
@@ -350,6 +365,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       for (int row = threadIdx.x; row < rows; row += blockDim.x) prefetch_l2(u + (size_t)row * g.N + n0);
     cp_async_wait_all();
     __syncthreads();
+    }
   }
   if (!NODE && st.twr) {  // P > 1: inverse four-step twiddle e^{+2 pi i rank kappa/L}
     for (int idx = threadIdx.x; idx < all; idx += blockDim.x)
@@ -380,6 +396,26 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
   // (v-c) u += alpha^{-l/L}/L c, loads batched for memory-level parallelism
   double dmax = 0.0;
   constexpr int kB = 8;
+  if (!PACK && tma) {
+    for (int idx = threadIdx.x; idx < all; idx += blockDim.x) {
+      const int row = idx >> lT, l = row / M;
+      const double2 c = cscale(sm[idx], __ldg(at.scale_bwd + l));
+      sm[idx] = c;
+      if (l == L - 1 && diff_slot) {
+        const double2 dd = overwrite ? csub(c, u[(size_t)row * g.N + n0 + (idx & (T - 1))]) : c;
+        dmax = nanmax(dmax, hypot(dd.x, dd.y));
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();   // also: the old last-step values (overwrite form) were read before the store
+    if (threadIdx.x == 0) {
+      for (int lb = 0; lb < L; lb += 256) {
+        if (overwrite) tma_store_3d(&tmu, 2 * n0, 0, lb, sm + (size_t)lb * M * T);
+        else tma_reduce_add_3d(&tmu, 2 * n0, 0, lb, sm + (size_t)lb * M * T);
+      }
+      bulk_commit();
+    }
+  } else
   for (int base = threadIdx.x; base < all; base += kB * blockDim.x) {
     double2 uo[kB], uo2[kB];
     double sc[kB];
@@ -432,6 +468,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       atomicMax(diff_slot, dbl_bits(v));  // non-negative doubles order like their bit patterns
     }
   }
+  if (!PACK && tma && threadIdx.x == 0) bulk_wait_read();   // the tile stays until the TMA unit has read it
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1499,6 +1536,17 @@ static int num_sms() {
 
 size_t fwd_smem_bytes(const Geometry &g, int T) { return (size_t)g.L * g.M * T * sizeof(double2); }
 
+// the 1-D backward tile moved by the TMA unit (bwd_kernel, tma = 1): complex storage, box rows of
+// 2 T <= 256 doubles, L <= 256 or a multiple of 256.  PINT_BWD_TMA=1 (experiments build) selects it.
+static bool bwd1d_tma_ok(const Geometry &g, const StaticTables &st, int T) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = experiment_env("PINT_BWD_TMA");
+    v = (e && atoi(e)) ? 1 : 0;   // opt-in until measured and parity-checked on the GPU
+  }
+  return v == 1 && g.dim == 1 && g.pow2 && !st.packed && T >= 1 && 2 * T <= 256 && g.N % T == 0 && g.M <= 8 &&
+         (g.L <= 256 || g.L % 256 == 0) && tma_encode_fn() != nullptr;
+}
 // the TMA-staged 1-D forward tile (fwd1d_tma_kernel): one rank, complex storage, 3-point stencil,
 // T = 4, L <= 256 (one step per thread), 128-byte aligned halo arrays, >= 3 CTAs per SM
 bool fwd1d_tma_ok(const Geometry &g, const StaticTables &st, int T) {
@@ -1993,19 +2041,33 @@ cudaError_t launch_backward(const Geometry &g, const LaunchCfg &lc, const Static
       tfft_bwd_kernel<false><<<g.M * (g.N / T2), kTileThreads, sm2, s>>>(g, st, at, x2, b.u, T2,
                                                                            (unsigned long long *)diff_slot, overwrite);
   } else if (g.dim == 1) {
+    // complex storage: tile in by a tensor load, u += c out as a TMA reduce-add (bwd1d_tma_ok)
+    CUtensorMap tmx2{}, tmu{};
+    int tma = 0;
+    if (bwd1d_tma_ok(g, st, T)) {
+      auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_fn());
+      const cuuint64_t dims[3] = {(cuuint64_t)2 * g.N, (cuuint64_t)g.M, (cuuint64_t)g.L};
+      const cuuint64_t strides[2] = {(cuuint64_t)g.N * 16, (cuuint64_t)g.M * g.N * 16};
+      const cuuint32_t box[3] = {(cuuint32_t)(2 * T), (cuuint32_t)g.M, (cuuint32_t)(g.L < 256 ? g.L : 256)};
+      const cuuint32_t es[3] = {1, 1, 1};
+      tma = enc(&tmx2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)x2, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+            enc(&tmu, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)b.u, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     PINT_DISPATCH_M(g.M, {
       if (st.packed) {
         e = set_smem((const void *)bwd_kernel<MM, true, true>, smem);
         if (e == cudaSuccess)
-          bwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
+          bwd_kernel<MM, true, true><<<grid, kTileThreads, smem, s>>>(tmx2, tmu, 0, g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
       } else if (st.P == 1) {
         e = set_smem((const void *)bwd_kernel<MM, true>, smem);
         if (e == cudaSuccess)
-          bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
+          bwd_kernel<MM, true><<<grid, kTileThreads, smem, s>>>(tmx2, tmu, tma, g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
       } else {
         e = set_smem((const void *)bwd_kernel<MM, false>, smem);
         if (e == cudaSuccess)
-          bwd_kernel<MM, false><<<grid, kTileThreads, smem, s>>>(g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
+          bwd_kernel<MM, false><<<grid, kTileThreads, smem, s>>>(tmx2, tmu, tma, g, st, at, x2, b.u, T, (unsigned long long *)diff_slot, overwrite);
       }
     });
   } else if (st.packed) {
