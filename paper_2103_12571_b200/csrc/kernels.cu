@@ -1537,12 +1537,12 @@ static int num_sms() {
 size_t fwd_smem_bytes(const Geometry &g, int T) { return (size_t)g.L * g.M * T * sizeof(double2); }
 
 // the 1-D backward tile moved by the TMA unit (bwd_kernel, tma = 1): complex storage, box rows of
-// 2 T <= 256 doubles, L <= 256 or a multiple of 256.  PINT_BWD_TMA=1 (experiments build) selects it.
+// 2 T <= 256 doubles, L <= 256 or a multiple of 256.  PINT_BWD_TMA=0 (experiments build): A/B.
 static bool bwd1d_tma_ok(const Geometry &g, const StaticTables &st, int T) {
   static int v = -1;
   if (v < 0) {
     const char *e = experiment_env("PINT_BWD_TMA");
-    v = (e && atoi(e)) ? 1 : 0;   // opt-in until measured and parity-checked on the GPU
+    v = (e && !atoi(e)) ? 0 : 1;
   }
   return v == 1 && g.dim == 1 && g.pow2 && !st.packed && T >= 1 && 2 * T <= 256 && g.N % T == 0 && g.M <= 8 &&
          (g.L <= 256 || g.L % 256 == 0) && tma_encode_fn() != nullptr;
